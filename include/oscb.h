@@ -1,0 +1,143 @@
+/*
+ * oscb.h -- C ABI of the B200 oscillator Ising/Potts machine (liboscb.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference package `oscim`
+ * (paths below are relative to /root/reference/pkg/src/oscim/).  The reference has no FFI
+ * layer of its own (it is numpy + numba); the seam it does have is the set of private kernel
+ * signatures under its public solver API, and each entry point here replaces one of them:
+ *
+ *   oscb_graph_create_csr    CouplingMatrix CSR arrays handed to the kernels
+ *                            (model.py:135-149, dynamics.py:250-251) and the canonical pair
+ *                            list J.pairs() (model.py:238-242)
+ *   oscb_graph_create_dense  the same couplings as a dense J (model.py:196-199), optionally one
+ *                            row shard of it (multi-GPU dense path)
+ *   oscb_initial_phases      NoiseSource.initial_phases             dynamics.py:127-129
+ *   oscb_step                trig precompute + _step_serial/_step_parallel, as called by
+ *                            euler_step                             dynamics.py:155-190, 303-312
+ *   oscb_score               _score_kernel                          dynamics.py:193-223
+ *   oscb_energy              sample() energy                        dynamics.py:380
+ *   oscb_run                 _simulate (time loop, noise, schedule, scoring cadence, best
+ *                            tracking, traces, finite check)        dynamics.py:333-431
+ *   oscb_dense_*             row-sharded dense step for one oversized graph
+ *
+ * Conventions: plain C types; all array arguments are caller-owned HOST buffers unless the
+ * name says `_dev`; phases are float64 [R, n] row-major (replica-major) like the reference's
+ * `phi`; every call returns 0 on success or one of the OSCB_E* codes, with a message in
+ * oscb_last_error() (thread-local).  A handle owns one device, one CUDA stream and its
+ * workspaces; calls on one handle must not overlap, different handles are independent.
+ * There is no CPU fallback: without a usable CUDA device every call fails with OSCB_ECUDA.
+ */
+#ifndef OSCB_H_
+#define OSCB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSCB_OK 0
+#define OSCB_EINVAL 1    /* bad argument            -> ValueError     (dynamics.py:434-440) */
+#define OSCB_ECUDA 2     /* CUDA / driver failure   -> RuntimeError                         */
+#define OSCB_ENONFINITE 3 /* non-finite phase        -> NumericalError (dynamics.py:276-283) */
+#define OSCB_ENOMEM 4
+
+#define OSCB_OBJ_MAXCUT 0
+#define OSCB_OBJ_COLORING 1
+
+#define OSCB_PREC_F32 32 /* throughput mode: fp32 state and arithmetic                    */
+#define OSCB_PREC_F64 64 /* parity mode: fp64, reference operation order                 */
+
+#define OSCB_NOISE_DEVICE 0 /* counter-based Philox4x32-10 + Box-Muller, f(seed, step, i) */
+#define OSCB_NOISE_HOST 1   /* caller supplies normals [steps, R, n] (parity hook)        */
+#define OSCB_NOISE_NONE 2   /* kn treated as 0                                            */
+
+#define OSCB_KERNEL_AUTO 0
+#define OSCB_KERNEL_STREAM 1   /* one launch per step, phases in HBM/L2                   */
+#define OSCB_KERNEL_RESIDENT 2 /* persistent CTA per replica tile, phases' (cos,sin) in smem */
+
+typedef struct oscb_graph oscb_graph;
+
+typedef struct oscb_graph_info {
+    int64_t n;
+    int64_t nnz;          /* directed nonzeros (2 per pair)                     */
+    int64_t pairs;        /* canonical pairs i<j                                */
+    int32_t device;
+    int32_t is_dense;     /* 1 when created by oscb_graph_create_dense          */
+    int32_t unit_weights; /* every stored coupling == 1.0                       */
+    int32_t int_weights;  /* every stored coupling integer valued (exact scoring) */
+    int64_t row_begin;    /* dense row shard [row_begin, row_end)               */
+    int64_t row_end;
+    int64_t max_degree;
+} oscb_graph_info;
+
+typedef struct oscb_run_params {
+    double K, ks_max, ks_period, kn, h, t_stop; /* SolverParams fields (model.py:328-336)     */
+    int32_t n_states;                           /* N                                          */
+    int32_t objective;                          /* OSCB_OBJ_*                                 */
+    int32_t precision;                          /* OSCB_PREC_*                                */
+    int32_t noise_mode;                         /* OSCB_NOISE_*                               */
+    int32_t kernel;                             /* OSCB_KERNEL_*                              */
+    int32_t use_target;                         /* record first step reaching target_objective */
+    int64_t steps;                              /* 0 => ceil(t_stop / h) (dynamics.py:349)    */
+    int64_t cadence;                            /* 0 => reference rule (dynamics.py:325-330); <0 => never score between samples */
+    double trace_stride;                        /* <= 0 => ks_period / 2 (dynamics.py:346)    */
+    double target_objective;
+    int64_t first_step;                         /* global index of the first step (restart)   */
+    int32_t replicas_per_cta;                   /* 0 auto; resident kernel tile width         */
+    int32_t reserved;
+} oscb_run_params;
+
+typedef struct oscb_run_outputs {
+    /* any pointer may be NULL to skip that output */
+    double *final_phases;    /* [R, n]                                                   */
+    uint8_t *best_states;    /* [R, n]  state per oscillator of the best-scored sample   */
+    double *best_objective;  /* [R]     objective of best_states (dynamics.py:421)       */
+    double *trace_t;         /* [max_samples]                                            */
+    double *trace_ks;        /* [max_samples]                                            */
+    double *energy;          /* [R, max_samples]  (dynamics.py:380)                      */
+    double *best_trace;      /* [R, max_samples]  best-so-far at each sample             */
+    int64_t *first_hit_step; /* [R] first scored step with objective >= / <= target, -1 if never */
+    int64_t max_samples;
+    /* filled by the call */
+    int64_t n_samples;
+    int64_t steps_executed;
+    int64_t nonfinite[3];    /* {replica row, oscillator, step} when OSCB_ENONFINITE     */
+    double device_ms;        /* CUDA-event time of the integrate loop only               */
+    int64_t kernel_launches; /* kernels launched inside that region                      */
+    int32_t kernel_used;     /* OSCB_KERNEL_*                                            */
+    int32_t replicas_per_cta;
+    int64_t smem_bytes;
+} oscb_run_outputs;
+
+const char *oscb_last_error(void);
+int oscb_version(void);
+int oscb_device_count(int *count);
+
+int oscb_graph_create_csr(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
+                          const double *data, oscb_graph **out);
+int oscb_graph_create_dense(int device, int64_t n, const double *J, int64_t row_begin,
+                            int64_t row_end, oscb_graph **out);
+int oscb_graph_destroy(oscb_graph *g);
+int oscb_graph_get_info(const oscb_graph *g, oscb_graph_info *info);
+
+int oscb_initial_phases(oscb_graph *g, const uint64_t *seeds, int64_t R, double *phi_out);
+
+int oscb_step(oscb_graph *g, int64_t R, const double *phi_in, const double *noise, double K,
+              double ks, double h, double kn_sqrt_h, int32_t n_states, int32_t precision,
+              double *phi_out, int64_t *nonfinite /* [2] replica, oscillator; -1 if none */);
+
+int oscb_score(oscb_graph *g, int64_t R, const double *phi, int32_t n_states, int32_t maximize,
+               int64_t *states /* [R, n] or NULL */, double *objective /* [R] */);
+
+int oscb_energy(oscb_graph *g, int64_t R, const double *phi, double *energy /* [R] */);
+
+int oscb_run(oscb_graph *g, const oscb_run_params *params, const uint64_t *seeds, int64_t R,
+             const double *phi0 /* [R, n] or NULL => Philox initial phases */,
+             const double *noise /* [steps, R, n] when noise_mode == OSCB_NOISE_HOST */,
+             oscb_run_outputs *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OSCB_H_ */
