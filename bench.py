@@ -1,0 +1,325 @@
+#!/usr/bin/env python
+"""bench.py -- oscillator-edge updates/s of the OIM/OPM Euler integrator on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
+
+A "step" is one pass of the hot path over one batch: `--window` consecutive Euler steps
+(default 2048) of ALL replicas of the workload, including threshold + cut scoring at the
+reference cadence and best-state tracking (SURVEY.md 8d "unit of work").  The default
+workload is BASELINE.json configs[1]: G22-shape max-cut (n=2000, 19990 edges, synthetic
+G(n,m), OIM N=2, GSET tuning K=0.2 ks_max=1.0 kn=0.15), 1024 replicas per GPU.
+
+  value   : updates/s = replicas * nnz * window * K / (device time of the K steps), phases
+            resident on the device (Philox initial phases generated there), CUDA events on
+            the stream the kernels run on, max over ranks.
+  e2e     : the same metric through the public API with HOST buffers: initial phases
+            handed in from host memory, final phases / best states / objectives / traces
+            copied back, wall clock around the K calls.
+  roofline: algorithmic HBM bytes (2*R*n*4 + nnz*(4+0|4) + (n+1)*4 per Euler step)
+            / kernel time, against MEASURED_PEAKS.json hbm_gbs.
+  cpu_baseline / --impl reference: the CPU oracle port of the reference algorithm
+            (oracle/, C + OpenMP, numpy's own Ziggurat) on the box's host cores, bounded sample.
+
+Multi-GPU (torchrun, one process per GPU): independent replicas shard across ranks with no
+data-path collective (weak scaling: 1024 replicas per GPU); the only communication is the
+barrier and the max-over-ranks of the timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (shape, replicas per GPU, tuning overrides)
+    "G22x1024": ("G22", 1024, dict(K=0.2, ks_max=1.0, kn=0.15)),
+    "G1x1": ("G1", 1, dict(K=0.2, ks_max=1.0, kn=0.15)),
+    "flat200x4096": ("flat200", 4096, {}),
+    "G81x296": ("G81", 296, {}),
+}
+
+
+def load_workload(name):
+    from paper_2505_22631_b200 import workloads
+    from paper_2505_22631_b200.model import CouplingMatrix, SolverParams
+    shape, R, tune = WORKLOADS[name]
+    n, (u, v, w), N, kind = workloads.shape_graph(shape)
+    J = CouplingMatrix.from_edges(n, (u, v, w))
+    params = SolverParams.tuned_for(n, N, seed=0, **tune)
+    return shape, J, params, kind, R
+
+
+def algorithmic_bytes_per_euler_step(J, R, unit_weights, s_phi=4):
+    """every phase read once and written once, graph read once per step."""
+    return 2 * R * J.n * s_phi + J.nnz * (4 + (0 if unit_weights else 4)) + (J.n + 1) * 4
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return json.loads(p.read_text()), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 7:
+                    continue
+                try:
+                    sm.append(float(f[0])); mx.append(float(f[1]))
+                except ValueError:
+                    continue
+                for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), f[3:7]):
+                    if val.lower().startswith("active"):
+                        reasons.add(name)
+            os.unlink(self.path)
+        except Exception:
+            pass
+        if sm:
+            out.update(sm_mhz=statistics.median(sm), sm_max_mhz=max(mx), reasons=sorted(reasons), samples=len(sm))
+        return out
+
+
+def cpu_oracle_throughput(J, params, kind, R_cpu, window, threads=None):
+    """The CPU port of the reference algorithm (oracle/) on the host cores: one bounded sample."""
+    from oracle import oracle as O
+    O.build()
+    threads = threads or O.max_threads()
+    t0 = time.perf_counter()
+    O.simulate(J.indptr, J.indices, J.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period,
+               kn=params.kn, h=params.h, t_stop=window * params.h, n_states=params.n_states,
+               seeds=list(range(R_cpu)), objective=kind, threads=threads)
+    dt = time.perf_counter() - t0
+    return R_cpu * J.nnz * window / dt, dt, threads
+
+
+def cpu_sample_size(J, window):
+    """Replicas for ~10-20 s of CPU work at ~80 M updates/s/core."""
+    cores = os.cpu_count() or 1
+    target_updates = 12.0 * 80e6 * cores
+    return int(max(1, min(256, target_updates / (J.nnz * window))))
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    shape, J, params, kind, R = load_workload(args.workload)
+    window = args.window
+    R_cpu = max(1, cpu_sample_size(J, window) // 2)
+    for _ in range(args.warmup):
+        cpu_oracle_throughput(J, params, kind, max(1, R_cpu // 8), max(32, window // 16))
+    t_all, upd, threads = 0.0, 0.0, 1
+    for _ in range(args.steps):
+        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, window)
+        t_all += dt
+        upd += R_cpu * J.nnz * window
+    value = upd / t_all
+    sample = f"{R_cpu} replicas x {window} Euler steps per step (of {R} replicas/GPU), linear in replicas"
+    line = {
+        "impl": "reference", "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{shape}-shape x {R} replicas/GPU, window {window} Euler steps", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="G22x1024", choices=sorted(WORKLOADS))
+    ap.add_argument("--window", type=int, default=2048, help="Euler steps per bench step")
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "resident"])
+    ap.add_argument("--replicas", type=int, default=0, help="override replicas per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-target", action="store_true", help="skip the time-to-99%%-best-cut run")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    from paper_2505_22631_b200 import _native as nat
+    from paper_2505_22631_b200 import dynamics as dyn
+    shape, J, params, kind, R = load_workload(args.workload)
+    if args.replicas:
+        R = args.replicas
+    window = args.window
+    seeds = [rank * R + r for r in range(R)]           # contiguous replica-index block per rank
+    g = dyn.device_graph(J, local_rank)
+    info = g.info()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local_rank}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def device_step(first_step):
+        # phases generated on the device, nothing copied back: inputs resident when the clock starts
+        return dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                             steps=window, first_step=first_step, want_phases=False, want_states=False, want_traces=False)
+
+    for w in range(args.warmup):
+        device_step(0)
+        flush.zero_()
+    barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    dev_ms, launches, wall0 = 0.0, 0, time.perf_counter()
+    last = None
+    for k in range(args.steps):
+        last = device_step(0)
+        dev_ms += last.device_ms
+        launches += last.kernel_launches
+        flush.zero_()                                   # L2 flush between timed iterations
+    barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+
+    # end to end through the public API with host buffers
+    phi0 = np.stack([dyn.NoiseSource(0, device=local_rank).initial_phases(J.n)] * 1)  # warm the path
+    phi0 = dyn._initial_phases_host(local_rank, seeds, J.n)
+    barrier()
+    e2e0 = time.perf_counter()
+    h2d = d2h = 0
+    for k in range(args.steps):
+        b = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                          steps=window, phi0=phi0)
+        h2d = phi0.nbytes + 8 * R
+        d2h = b.final_phases.nbytes + b.best_states.nbytes + b.best_objective.nbytes + b.energy.nbytes + b.best_trace.nbytes + 8 * R
+    barrier()
+    e2e_s = time.perf_counter() - e2e0
+
+    t_dev = torch.tensor([dev_ms / 1e3, e2e_s, wall], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if dist is not None:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+    t_dev_s, t_e2e_s, t_wall_s = (float(x) for x in t_dev.cpu())
+    updates_per_step = world * R * J.nnz * window
+    value = updates_per_step * args.steps / t_dev_s
+    e2e_value = updates_per_step * args.steps / t_e2e_s
+
+    peaks, peak_kind = measured_peaks()
+    s_phi = 4 if args.precision == "f32" else 8
+    bytes_per_launch = algorithmic_bytes_per_euler_step(J, R, bool(info.unit_weights), s_phi) * window
+    step_launches = max(1, (launches // args.steps))
+    if last.kernel == "resident":
+        kernel_ms = dev_ms / args.steps           # one persistent launch integrates the whole window
+        launch_bytes = bytes_per_launch
+    else:
+        kernel_ms = dev_ms / args.steps / window  # per Euler-step launch (scoring launches included in the time)
+        launch_bytes = bytes_per_launch / window
+    achieved = launch_bytes / (kernel_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind,
+                "kernel": last.kernel, "bytes_per_update": launch_bytes / (R * J.nnz * (window if last.kernel == "resident" else 1)),
+                "note": "phases stay in shared memory / L2 for the whole window, so DRAM traffic is ~0 by design; "
+                        "the binding resource is shared-memory gather bandwidth (DESIGN.md)"}
+
+    line = {
+        "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_dev_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": f"{shape}-shape max-cut/colouring graph n={J.n} nnz={J.nnz} N={params.n_states}, "
+                               f"{R} replicas per GPU, window {window} Euler steps incl. scoring every "
+                               f"{'ref-cadence'} steps", "replicas_per_gpu": R, "window": window,
+                   "kernel": last.kernel, "replicas_per_cta": last.replicas_per_cta, "smem_bytes": last.smem_bytes,
+                   "l2": "256 MB flush write between timed iterations", "parallelism": f"replica-shard x{world}",
+                   "wall_s_timed_region": t_wall_s},
+        "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
+        "roofline": roofline,
+    }
+
+    if rank == 0 and not args.no_target and shape == "G22":
+        # time-to-99%-best-cut: full default schedule, target = 0.99 x best cut of this batch
+        full = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                             want_phases=False, want_states=False, want_traces=False)
+        best = float(full.best_objective.max())
+        hit = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                            target=0.99 * best, want_phases=False, want_states=False, want_traces=False)
+        hits = hit.first_hit_step[hit.first_hit_step >= 0]
+        first = int(hits.min()) if len(hits) else -1
+        line["time_to_99pct_best_cut"] = {
+            "best_cut": best, "target": 0.99 * best, "first_hit_step": first, "steps_total": hit.steps,
+            "seconds": (hit.device_ms / 1e3) * (first + 1) / hit.steps if first >= 0 else None,
+            "full_run_seconds": hit.device_ms / 1e3, "replicas": R}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        R_cpu = cpu_sample_size(J, window)
+        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, window)
+        line["cpu_baseline"] = {"value": v, "unit": "updates/s", "cores": threads, "kind": "port",
+                                "sample": f"{R_cpu} replicas x {window} Euler steps of the same workload in {dt:.1f} s "
+                                          f"(oracle/ C+OpenMP port of the reference; linear in replicas)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -12,6 +12,7 @@
  *   oscb_graph_create_dense  the same couplings as a dense J (model.py:196-199), optionally one
  *                            row shard of it (multi-GPU dense path)
  *   oscb_initial_phases      NoiseSource.initial_phases             dynamics.py:127-129
+ *   oscb_device_normals      NoiseSource.step_normals               dynamics.py:121-125
  *   oscb_step                trig precompute + _step_serial/_step_parallel, as called by
  *                            euler_step                             dynamics.py:155-190, 303-312
  *   oscb_score               _score_kernel                          dynamics.py:193-223
@@ -122,6 +123,12 @@ int oscb_graph_destroy(oscb_graph *g);
 int oscb_graph_get_info(const oscb_graph *g, oscb_graph_info *info);
 
 int oscb_initial_phases(oscb_graph *g, const uint64_t *seeds, int64_t R, double *phi_out);
+
+/* The device noise source (replaces NoiseSource.step_normals, dynamics.py:121-125): the standard
+ * normals the integrator draws for `seed` at `step`, oscillators 0..n-1, in the arithmetic of
+ * `precision`, widened to float64.  A pure function of (seed, step, oscillator). */
+int oscb_device_normals(int device, uint64_t seed, int64_t step, int64_t n, int32_t precision,
+                        double *out /* [n] */);
 
 int oscb_step(oscb_graph *g, int64_t R, const double *phi_in, const double *noise, double K,
               double ks, double h, double kn_sqrt_h, int32_t n_states, int32_t precision,

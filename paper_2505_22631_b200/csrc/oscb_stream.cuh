@@ -58,6 +58,19 @@ __global__ void k_initial_phases(const uint64_t *__restrict__ seeds, double *__r
     }
 }
 
+// the integrator's own normals for (seed, step, oscillators 0..n-1), widened to float64
+template <typename T>
+__global__ void k_device_normals(uint64_t seed, uint64_t step, int n, double *__restrict__ out)
+{
+    const int quad = blockIdx.x * blockDim.x + threadIdx.x;
+    if (quad >= (n + 3) / 4) return;
+    T z[4];
+    normals4(noise_block(seed, step, (uint32_t)quad), z);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (4 * quad + k < n) out[4 * quad + k] = (double)z[k];
+}
+
 // (cos, sin) of every phase: cs[i*R + r] = {cos 2pi phi, sin 2pi phi}
 template <typename T>
 __global__ void k_trig(const T *__restrict__ phi, typename Vec2<T>::type *__restrict__ cs, long long total)
@@ -170,23 +183,55 @@ __device__ __forceinline__ double block_sum_256(double v, double *scratch /* [8]
     return tot; // valid in thread 0
 }
 
-// objective per replica over the canonical pairs (dynamics.py:214-223): one block per replica.
+// objective per replica over the canonical pairs (dynamics.py:214-223), replica index on the
+// lanes so every state read is a coalesced 32-byte segment of the [n, R] layout.
+// grid = (ceil(R/32), P): block (x, p) covers replicas 32x..32x+31 and the p-th chunk of pairs;
+// its 8 warps stride through the chunk.  partial[p * R + r] is summed in index order by
+// k_best_flag, so the result does not depend on scheduling.
 // maximize: sum w [s_u != s_v];  else: count [s_u == s_v].
 __global__ void __launch_bounds__(256)
-k_objective(const uint8_t *__restrict__ states, int R, const int *__restrict__ iu,
-            const int *__restrict__ jv, const double *__restrict__ w, int m, int maximize,
-            double *__restrict__ obj)
+k_objective_partial(const uint8_t *__restrict__ states, int R, const int *__restrict__ iu,
+                    const int *__restrict__ jv, const double *__restrict__ w, int m, int chunk,
+                    int maximize, double *__restrict__ partial)
 {
-    __shared__ double scratch[8];
-    const int r = blockIdx.x;
-    double part = 0.0;
-    for (int e = threadIdx.x; e < m; e += blockDim.x) {
-        const bool same = states[(long long)iu[e] * R + r] == states[(long long)jv[e] * R + r];
-        if (maximize) { if (!same) part += w[e]; }
-        else          { if (same) part += 1.0; }
+    __shared__ double part[8][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = blockIdx.x * 32 + lane;
+    const int e0 = blockIdx.y * chunk, e1 = min(m, e0 + chunk);
+    double acc = 0.0;
+    if (r < R) {
+        for (int e = e0 + warp; e < e1; e += 8) {
+            const bool same = states[(long long)iu[e] * R + r] == states[(long long)jv[e] * R + r];
+            if (maximize) { if (!same) acc += w[e]; }
+            else          { if (same) acc += 1.0; }
+        }
     }
-    const double tot = block_sum_256(part, scratch);
-    if (threadIdx.x == 0) obj[r] = tot;
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && r < R) {
+        double tot = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tot += part[k][lane];
+        partial[(long long)blockIdx.y * R + r] = tot;
+    }
+}
+
+// the reference's own summation order (one thread walks all pairs of one replica): used by
+// oscb_score when the couplings are not integer valued, where the order is visible in the
+// last bits of the sum.
+__global__ void k_objective_seq(const uint8_t *__restrict__ states, int R, const int *__restrict__ iu,
+                                const int *__restrict__ jv, const double *__restrict__ w, int m,
+                                int maximize, double *__restrict__ obj)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= R) return;
+    double acc = 0.0;
+    for (int e = 0; e < m; ++e) {
+        const bool same = states[(long long)iu[e] * R + r] == states[(long long)jv[e] * R + r];
+        if (maximize) { if (!same) acc = __dadd_rn(acc, w[e]); }
+        else          { if (same) acc += 1.0; }
+    }
+    obj[r] = acc;
 }
 
 // continuous energy per replica (dynamics.py:380): sum_e w_e cos(2 pi (phi_u - phi_v))
@@ -206,14 +251,20 @@ k_energy(const T *__restrict__ phi, int R, const int *__restrict__ iu, const int
     if (threadIdx.x == 0) out[(long long)r * out_stride] = tot;
 }
 
-// best-so-far bookkeeping (dynamics.py:370-375): strict improvement only.
-__global__ void k_best_flag(const double *__restrict__ obj, double *__restrict__ best_obj,
-                            uint8_t *__restrict__ improved, long long *__restrict__ first_hit,
-                            int R, int maximize, int use_target, double target, long long step)
+// best-so-far bookkeeping (dynamics.py:370-375): strict improvement only.  obj[r] is the
+// in-order sum of the P partials of k_objective_partial (P == 1: obj already final).
+__global__ void k_best_flag(const double *__restrict__ partial, int P, double *__restrict__ obj,
+                            double *__restrict__ best_obj, uint8_t *__restrict__ improved,
+                            long long *__restrict__ first_hit, int R, int maximize, int use_target,
+                            double target, long long step)
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= R) return;
-    const double o = obj[r], b = best_obj[r];
+    double o = 0.0;
+    for (int p = 0; p < P; ++p) o += partial[(long long)p * R + r];
+    obj[r] = o;
+    if (!best_obj) return;
+    const double b = best_obj[r];
     const bool better = maximize ? (o > b) : (o < b);
     improved[r] = better ? 1 : 0;
     if (better) {
