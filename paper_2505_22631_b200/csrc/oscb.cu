@@ -264,8 +264,7 @@ static void step_impl(oscb_graph *g, int64_t R, const double *phi_in, const doub
     wk.load_from_io(s);
     StepScalars sc;
     sc.K = K; sc.ks = ks; sc.h = h; sc.kn_sqrt_h = kn_sqrt_h;
-    sc.tc.n_states = n_states;
-    sc.tc.two_pi_n = OSCB_TWO_PI * (double)n_states;
+    sc.tc = make_trig_const(n_states);
     sc.step = 0;
     sc.noise_mode = noise ? OSCB_NOISE_HOST : OSCB_NOISE_NONE;
     launch_stream_step<T, STRICT>(g, wk, nullptr, d_noise.p, sc);
@@ -363,8 +362,7 @@ static void run_stream(oscb_graph *g, const oscb_run_params *p, const RunPlan &r
     size_t next_sample = 0;
     StepScalars sc;
     sc.K = p->K; sc.h = p->h; sc.kn_sqrt_h = p->kn * std::sqrt(p->h);
-    sc.tc.n_states = p->n_states;
-    sc.tc.two_pi_n = OSCB_TWO_PI * (double)p->n_states;
+    sc.tc = make_trig_const(p->n_states);
     sc.noise_mode = p->noise_mode;
     if (p->kn == 0.0 && p->noise_mode == OSCB_NOISE_DEVICE) sc.noise_mode = OSCB_NOISE_NONE;
     for (int64_t step = 0; step < rp.steps; ++step) {
@@ -385,7 +383,7 @@ static void run_stream(oscb_graph *g, const oscb_run_params *p, const RunPlan &r
         if (next_sample < rp.sample_steps.size() && rp.sample_steps[next_sample] == step) {
             sample(gstep, 1 + (int64_t)next_sample);
             ++next_sample;
-        } else if (rp.cadence > 0 && step % rp.cadence == 0) {
+        } else if (rp.cadence > 0 && gstep % rp.cadence == 0) {
             score(gstep);
         }
     }
@@ -655,6 +653,42 @@ int oscb_energy(oscb_graph *g, int64_t R, const double *phi, double *energy)
         check_launch("oscb_energy");
         en.download(energy, R, s);
         OSCB_CUDA(cudaStreamSynchronize(s));
+        return OSCB_OK;
+    });
+}
+
+int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t replicas_per_cta,
+                            int32_t max_threads, int32_t *warps, int32_t *rounds, int64_t *group_rows,
+                            int32_t *warp_start, int32_t *quad_of, uint32_t *ginfo, uint16_t *ids)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(n >= 1 && n <= 65534 && indptr && warps && rounds && group_rows, "bad argument");
+        const int RT = replicas_per_cta;
+        OSCB_REQUIRE(RT >= 1 && RT <= 32 && (RT & (RT - 1)) == 0, "replicas_per_cta must be a power of two <= 32");
+        OSCB_REQUIRE(max_threads >= 32 && max_threads <= 1024 && max_threads % 32 == 0, "bad max_threads");
+        const int64_t nnz = indptr[n];
+        std::vector<int> ip(n + 1), ix(nnz);
+        for (int64_t i = 0; i <= n; ++i) ip[i] = (int)indptr[i];
+        for (int64_t e = 0; e < nnz; ++e) ix[e] = (int)indices[e];
+        int W, T;
+        tile_shape(n, RT, max_threads, &W, &T);
+        ResidentStreamHost h;
+        compile_resident_stream((int)n, ip.data(), ix.data(), nullptr, RT, W, T, &h);
+        *warps = W;
+        *rounds = T;
+        *group_rows = h.n_group_rows;
+        if (ids) {
+            OSCB_REQUIRE(warp_start && quad_of && ginfo, "NULL output");
+            std::copy(h.warp_start.begin(), h.warp_start.end(), warp_start);
+            std::copy(h.quad_of.begin(), h.quad_of.end(), quad_of);
+            std::copy(h.ginfo.begin(), h.ginfo.end(), ginfo);
+            for (size_t q = 0; q < h.stream.size(); ++q) {
+                ids[4 * q + 0] = (uint16_t)(h.stream[q].x & 0xffffu);
+                ids[4 * q + 1] = (uint16_t)(h.stream[q].x >> 16);
+                ids[4 * q + 2] = (uint16_t)(h.stream[q].y & 0xffffu);
+                ids[4 * q + 3] = (uint16_t)(h.stream[q].y >> 16);
+            }
+        }
         return OSCB_OK;
     });
 }

@@ -104,6 +104,13 @@ struct TrigConst {
     double two_pi_n; // (2*pi) * N, rounded once like the reference's (TWO_PI * n_states)
     int n_states;
 };
+__host__ __device__ inline TrigConst make_trig_const(int n_states)
+{
+    TrigConst tc;
+    tc.two_pi_n = OSCB_TWO_PI * (double)n_states;
+    tc.n_states = n_states;
+    return tc;
+}
 
 __device__ __forceinline__ void phase_trig(double phi, double &s, double &c)
 {
@@ -138,6 +145,9 @@ template <typename T> __device__ __forceinline__ T wrap_unit(T x)
 // reference's bit for bit for any phase representable in the kernel's precision.
 __device__ __forceinline__ int threshold_state(double p, int n_states)
 {
+    // N = 2: d0 = min(p, 1-p), d1 = |p - 0.5|, both differences exact where the comparison is
+    // close (Sterbenz), so "d1 < d0" is exactly 0.25 < p < 0.75 (ties at 0.25 / 0.75 -> state 0)
+    if (n_states == 2) return (p > 0.25 && p < 0.75) ? 1 : 0;
     int best_k = 0;
     double best_d = 2.0;
     for (int k = 0; k < n_states; ++k) {

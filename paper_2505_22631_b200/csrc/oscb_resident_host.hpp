@@ -1,20 +1,382 @@
-// oscb_resident_host.hpp -- host side of the persistent shared-memory kernel (stub until built).
+// oscb_resident_host.hpp -- host side of the persistent shared-memory kernel: the graph
+// "compiler" that turns the canonical CSR into the sliced-ELL neighbour stream the kernel
+// walks (see oscb_resident.cuh), the tile-shape chooser and the launcher.
 #pragma once
 #include "oscb_host.hpp"
+#include "oscb_resident.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <numeric>
 
 namespace oscb {
 
 struct ResidentPlan {
-    int dummy = 0;
+    int RT = 1, log2RT = 0, C = 32, T = 1, W = 1;
+    int n_group_rows = 0;
+    bool weighted = false;
+    double fill = 1.0; // real neighbours / stream entries
+    DevBuf<int> warp_start, quad_of;
+    DevBuf<uint32_t> ginfo;
+    DevBuf<uint2> stream;
+    DevBuf<float> w32;
+    DevBuf<double> w64;
 };
 
-static bool resident_fits(const oscb_graph *, const oscb_run_params *, int64_t) { return false; }
+static inline int state_bits_for(int n_states) { return n_states <= 2 ? 1 : n_states <= 4 ? 2 : n_states <= 16 ? 4 : 8; }
+static inline int words_per_row(int RT, int SB) { return std::max(1, RT * SB / 32); }
 
-static void run_resident(oscb_graph *, const oscb_run_params *, int64_t, int64_t, const std::vector<long long> &,
-                         const uint64_t *, int64_t, const double *, const double *, oscb_run_outputs *)
+// warps per CTA for a tile of RT replicas: as many slots as there are quads to hand out, in
+// the fewest rounds the thread limit allows
+static void tile_shape(int64_t n, int RT, int max_threads, int *W, int *T)
 {
-    set_error("resident kernel not built");
-    throw OscbFail{OSCB_ECUDA};
+    const int C = 32 / RT;
+    const int64_t Q = (n + 3) / 4;
+    const int64_t s_max = (int64_t)(max_threads / 32) * C;
+    const int64_t rounds = std::max<int64_t>(1, (Q + s_max - 1) / s_max);
+    const int64_t slots = (Q + rounds - 1) / rounds;
+    *W = (int)std::max<int64_t>(1, (slots + C - 1) / C);
+    *T = (int)std::max<int64_t>(1, (Q + (int64_t)(*W) * C - 1) / ((int64_t)(*W) * C));
+}
+
+// pure host result of the graph compiler (also exported for CPU-side tests)
+struct ResidentStreamHost {
+    std::vector<int> warp_start, quad_of;
+    std::vector<uint32_t> ginfo;
+    std::vector<uint2> stream;
+    std::vector<double> weights;
+    int n_group_rows = 0;
+    int64_t real = 0;
+};
+
+static void compile_resident_stream(int n, const int *indptr, const int *indices, const double *wts, int RT, int W,
+                                    int T, ResidentStreamHost *out)
+{
+    const int C = 32 / RT, S = W * C;
+    const int Q = (n + 3) / 4;
+    auto deg = [&](int i) { return i < n ? indptr[i + 1] - indptr[i] : 0; };
+
+    // quads by total degree, heaviest first, dealt to the slots boustrophedon so that slot loads
+    // balance and the C slots of a warp hold neighbours in the sorted order (look-alike rows)
+    std::vector<int> order(Q);
+    std::iota(order.begin(), order.end(), 0);
+    std::vector<int> qdeg(Q);
+    for (int q = 0; q < Q; ++q) qdeg[q] = deg(4 * q) + deg(4 * q + 1) + deg(4 * q + 2) + deg(4 * q + 3);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return qdeg[x] > qdeg[y]; });
+    std::vector<int> &quad_of = out->quad_of;
+    quad_of.assign((size_t)W * T * C, -1);
+    for (int64_t pos = 0; pos < (int64_t)T * S; ++pos) {
+        const int t = (int)(pos / S), s_in = (int)(pos % S);
+        const int slot = (t & 1) ? S - 1 - s_in : s_in;
+        const int w = slot / C, c = slot % C;
+        if (pos < Q) quad_of[((size_t)w * T + t) * C + c] = order[pos];
+    }
+
+    out->warp_start.assign(W, 0);
+    out->ginfo.assign((size_t)W * T, 0);
+    out->stream.clear();
+    out->weights.clear();
+    out->real = 0;
+    int group_rows = 0;
+    for (int w = 0; w < W; ++w) {
+        out->warp_start[w] = group_rows;
+        for (int t = 0; t < T; ++t) {
+            int rows[32][4]; // [c][kk] row visited kk-th by slot c (or -1)
+            int G[4] = {0, 0, 0, 0};
+            for (int c = 0; c < C; ++c) {
+                int &qw = quad_of[((size_t)w * T + t) * C + c];
+                if (qw < 0) {
+                    for (int kk = 0; kk < 4; ++kk) rows[c][kk] = -1;
+                    continue;
+                }
+                const int quad = qw;
+                int ks[4] = {0, 1, 2, 3};
+                std::stable_sort(ks, ks + 4, [&](int x, int y) { return deg(4 * quad + x) > deg(4 * quad + y); });
+                int ord = 0;
+                for (int kk = 0; kk < 4; ++kk) {
+                    ord |= ks[kk] << (2 * kk);
+                    const int i = 4 * quad + ks[kk];
+                    rows[c][kk] = i < n ? i : -1;
+                    G[kk] = std::max(G[kk], (deg(i) + 3) / 4);
+                }
+                qw = quad | (ord << 20);
+            }
+            for (int kk = 0; kk < 4; ++kk) {
+                OSCB_REQUIRE(G[kk] <= 255, "row degree too large for the resident kernel");
+                out->ginfo[(size_t)w * T + t] |= (uint32_t)G[kk] << (8 * kk);
+                for (int gidx = 0; gidx < G[kk]; ++gidx) {
+                    for (int c = 0; c < C; ++c) {
+                        uint32_t ids[4];
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = rows[c][kk];
+                            const int e = i >= 0 ? indptr[i] + 4 * gidx + u : -1;
+                            if (i >= 0 && e < indptr[i + 1]) {
+                                ids[u] = (uint32_t)indices[e];
+                                out->weights.push_back(wts ? wts[e] : 1.0);
+                                ++out->real;
+                            } else {
+                                ids[u] = (uint32_t)n; // the zero pair
+                                out->weights.push_back(0.0);
+                            }
+                        }
+                        out->stream.push_back(make_uint2(ids[0] | (ids[1] << 16), ids[2] | (ids[3] << 16)));
+                    }
+                    ++group_rows;
+                }
+            }
+        }
+    }
+    out->n_group_rows = group_rows;
+}
+
+static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, int W, int T)
+{
+    auto plan = std::make_shared<ResidentPlan>();
+    plan->RT = RT;
+    plan->log2RT = 0;
+    while ((1 << plan->log2RT) < RT) ++plan->log2RT;
+    plan->C = 32 / RT;
+    plan->W = W;
+    plan->T = T;
+    plan->weighted = !g->unit_weights;
+    ResidentStreamHost h;
+    compile_resident_stream((int)g->n, g->h_indptr.data(), g->h_indices.data(), g->h_w.data(), RT, W, T, &h);
+    OSCB_REQUIRE(h.real == g->nnz, "internal: resident plan lost neighbours (%lld of %lld)", (long long)h.real, (long long)g->nnz);
+    plan->n_group_rows = h.n_group_rows;
+    plan->fill = h.stream.empty() ? 1.0 : (double)h.real / (4.0 * (double)h.stream.size());
+    cudaStream_t s = g->stream;
+    plan->warp_start.alloc(W);                plan->warp_start.upload(h.warp_start.data(), W, s);
+    plan->quad_of.alloc(h.quad_of.size());    plan->quad_of.upload(h.quad_of.data(), h.quad_of.size(), s);
+    plan->ginfo.alloc(h.ginfo.size());        plan->ginfo.upload(h.ginfo.data(), h.ginfo.size(), s);
+    plan->stream.alloc(h.stream.size());      plan->stream.upload(h.stream.data(), h.stream.size(), s);
+    std::vector<float> wf(h.weights.begin(), h.weights.end());
+    if (plan->weighted) {
+        plan->w64.alloc(h.weights.size());    plan->w64.upload(h.weights.data(), h.weights.size(), s);
+        plan->w32.alloc(wf.size());           plan->w32.upload(wf.data(), wf.size(), s);
+    }
+    OSCB_CUDA(cudaStreamSynchronize(s));
+    return plan;
+}
+
+static std::shared_ptr<ResidentPlan> get_resident_plan(oscb_graph *g, int RT, int W, int T)
+{
+    const uint64_t key = ((uint64_t)RT << 40) | ((uint64_t)W << 20) | (uint64_t)T;
+    auto it = g->plans.find(key);
+    if (it != g->plans.end()) return it->second;
+    auto plan = build_resident_plan(g, RT, W, T);
+    g->plans[key] = plan;
+    return plan;
+}
+
+struct ResidentConfig {
+    int RT = 0, W = 0, T = 0, max_threads = 1024;
+    size_t smem_min = 0; // without the stream staged in shared memory
+};
+
+static inline int max_threads_for(int precision) { return precision == OSCB_PREC_F64 ? 512 : 1024; }
+
+static size_t resident_smem_bytes(const oscb_graph *g, int precision, int n_states, int RT, int W, int T,
+                                  int n_group_rows, bool idx_smem)
+{
+    const size_t pair = precision == OSCB_PREC_F64 ? 16 : 8;
+    const int SB = state_bits_for(n_states);
+    return ResidentSmem::make((int)g->n, RT, 32 / RT, T, W, words_per_row(RT, SB), pair, pair / 2, n_group_rows,
+                              idx_smem, !g->unit_weights).total;
+}
+
+// tile width: the candidate with the lowest estimated time
+static bool choose_resident_config(const oscb_graph *g, int precision, int n_states, int64_t R, int requested_rt,
+                                   ResidentConfig *out)
+{
+    if (g->n > 65534 || g->max_degree > 1020 || n_states > 255) return false;
+    static const double eff[6] = {0.35, 0.5, 0.7, 0.85, 1.0, 1.0}; // gather efficiency by log2(RT)
+    const int max_threads = max_threads_for(precision);
+    double best_cost = std::numeric_limits<double>::infinity();
+    bool found = false;
+    for (int l = 5; l >= 0; --l) {
+        const int RT = 1 << l;
+        if (requested_rt > 0 && RT != requested_rt) continue;
+        if (requested_rt <= 0 && RT > 1 && RT / 2 >= R) continue; // do not pad a tile more than 2x
+        int W, T;
+        tile_shape(g->n, RT, max_threads, &W, &T);
+        const size_t need = resident_smem_bytes(g, precision, n_states, RT, W, T, 0, false);
+        if (need > (size_t)g->smem_optin) continue;
+        const int64_t tiles = (R + RT - 1) / RT;
+        const int by_smem = (int)std::max<size_t>(1, (size_t)(g->smem_optin + 1024) / (need + 1024));
+        const int by_threads = std::max(1, 2048 / (W * 32));
+        const int cps = std::min(by_smem, by_threads);
+        const int64_t slots = (int64_t)g->sm_count * cps;
+        const int64_t waves = (tiles + slots - 1) / slots;
+        const int64_t per_sm = std::min<int64_t>(cps, (tiles + g->sm_count - 1) / g->sm_count);
+        const double cost = (double)waves * (double)per_sm * RT / eff[l];
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            out->RT = RT;
+            out->W = W;
+            out->T = T;
+            out->max_threads = max_threads;
+            out->smem_min = need;
+            found = true;
+        }
+    }
+    return found;
+}
+
+static bool resident_fits(const oscb_graph *g, const oscb_run_params *p, int64_t R)
+{
+    ResidentConfig cfg;
+    return choose_resident_config(g, p->precision, p->n_states, R, p->replicas_per_cta, &cfg);
+}
+
+template <typename T, int MAXT, bool STRICT>
+static void launch_resident(oscb_graph *g, const ResidentArgs &args, int tiles, int threads, size_t smem, bool idx_smem,
+                            bool weighted)
+{
+    auto go = [&](auto kernel) {
+        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kernel<<<tiles, threads, smem, g->stream>>>(args);
+    };
+    if (idx_smem) {
+        if (weighted) go(k_resident<T, MAXT, true, true, STRICT>);
+        else go(k_resident<T, MAXT, true, false, STRICT>);
+    } else {
+        if (weighted) go(k_resident<T, MAXT, false, true, STRICT>);
+        else go(k_resident<T, MAXT, false, false, STRICT>);
+    }
+}
+
+template <typename T, int MAXT, bool STRICT>
+static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const ResidentConfig &cfg, int64_t steps,
+                              int64_t cadence, const std::vector<long long> &sample_steps, const uint64_t *seeds,
+                              int64_t R64, const double *phi0, const double *noise, oscb_run_outputs *out)
+{
+    cudaStream_t s = g->stream;
+    const int n = (int)g->n, R = (int)R64;
+    auto plan = get_resident_plan(g, cfg.RT, cfg.W, cfg.T);
+    const int RT = plan->RT, tiles = (R + RT - 1) / RT, R_pad = tiles * RT;
+    const int SB = state_bits_for(p->n_states), wpr = words_per_row(RT, SB);
+    bool idx_smem = true;
+    size_t smem = resident_smem_bytes(g, p->precision, p->n_states, RT, plan->W, plan->T, plan->n_group_rows, true);
+    if (smem > (size_t)g->smem_optin) {
+        idx_smem = false;
+        smem = resident_smem_bytes(g, p->precision, p->n_states, RT, plan->W, plan->T, plan->n_group_rows, false);
+    }
+    OSCB_REQUIRE(smem <= (size_t)g->smem_optin, "resident kernel does not fit in shared memory (%zu bytes)", smem);
+    const int maximize = p->objective == OSCB_OBJ_MAXCUT;
+    const int64_t S = 1 + (int64_t)sample_steps.size();
+    const size_t tot = (size_t)n * R, tot_pad = (size_t)n * R_pad;
+
+    DevBuf<T> d_phi(tot_pad);
+    DevBuf<double> d_io(tot);
+    std::vector<uint64_t> h_seeds(R_pad, 0);
+    std::copy(seeds, seeds + R, h_seeds.begin());
+    DevBuf<uint64_t> d_seeds(R_pad);
+    d_seeds.upload(h_seeds.data(), R_pad, s);
+    DevBuf<double> d_best(R_pad), d_energy((size_t)R_pad * S), d_btrace((size_t)R_pad * S), d_noise;
+    DevBuf<uint8_t> d_best_states(tot_pad);
+    DevBuf<long long> d_first(R_pad), d_samples(std::max<size_t>(1, sample_steps.size()));
+    std::vector<double> h_best(R_pad, maximize ? -std::numeric_limits<double>::infinity()
+                                               : std::numeric_limits<double>::infinity());
+    std::vector<long long> h_first(R_pad, -1), h_samples(sample_steps);
+    for (auto &v : h_samples) v += p->first_step;
+    d_best.upload(h_best.data(), R_pad, s);
+    d_first.upload(h_first.data(), R_pad, s);
+    d_samples.upload(h_samples.data(), h_samples.size(), s);
+    d_best_states.zero(s);
+    const unsigned long long none = ~0ull;
+    OSCB_CUDA(cudaMemcpyAsync(g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    if (phi0) d_io.upload(phi0, tot, s);
+    else k_initial_phases<<<(unsigned)(((long long)((n + 3) / 4) * R + 127) / 128), 128, 0, s>>>(d_seeds.p, d_io.p, n, R);
+    k_to_tile_layout<T><<<(unsigned)((tot_pad + 255) / 256), 256, 0, s>>>(d_io.p, d_phi.p, n, R, RT, (long long)tot_pad);
+    if (p->noise_mode == OSCB_NOISE_HOST) {
+        d_noise.alloc((size_t)steps * tot);
+        d_noise.upload(noise, (size_t)steps * tot, s);
+    }
+
+    ResidentArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = n; a.R_real = R; a.RT = RT; a.log2RT = plan->log2RT; a.C = plan->C; a.T = plan->T; a.W = plan->W;
+    a.SB = SB; a.wpr = wpr; a.n_group_rows = plan->n_group_rows;
+    a.warp_start = plan->warp_start.p; a.quad_of = plan->quad_of.p; a.ginfo = plan->ginfo.p; a.stream = plan->stream.p;
+    a.wstream = plan->weighted ? (sizeof(T) == 8 ? (const void *)plan->w64.p : (const void *)plan->w32.p) : nullptr;
+    a.phi = d_phi.p; a.seeds = d_seeds.p;
+    a.step_begin = p->first_step; a.step_end = p->first_step + steps; a.noise_step0 = p->first_step;
+    a.K = p->K; a.h = p->h; a.kn_sqrt_h = p->kn * std::sqrt(p->h); a.ks_max = p->ks_max; a.ks_period = p->ks_period;
+    a.tc = make_trig_const(p->n_states);
+    a.noise_mode = p->noise_mode;
+    if (p->kn == 0.0 && p->noise_mode == OSCB_NOISE_DEVICE) a.noise_mode = OSCB_NOISE_NONE;
+    a.noise_host = d_noise.p;
+    a.cadence = cadence;
+    a.sample_steps = d_samples.p; a.n_sample_steps = (int)sample_steps.size(); a.sample_offset = 1; a.initial_sample = 1;
+    a.maximize = maximize;
+    a.best_obj = d_best.p; a.best_states = d_best_states.p; a.energy = d_energy.p; a.best_trace = d_btrace.p;
+    a.trace_stride = S; a.first_hit = d_first.p; a.use_target = p->use_target; a.target = p->target_objective;
+    a.nonfinite = g->d_nonfinite.p;
+
+    cudaEvent_t ev0, ev1;
+    OSCB_CUDA(cudaEventCreate(&ev0));
+    OSCB_CUDA(cudaEventCreate(&ev1));
+    OSCB_CUDA(cudaEventRecord(ev0, s));
+    launch_resident<T, MAXT, STRICT>(g, a, tiles, plan->W * 32, smem, idx_smem, plan->weighted);
+    OSCB_CUDA(cudaEventRecord(ev1, s));
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            set_error("oscb_run(resident): kernel launch failed: %s (tiles %d, threads %d, smem %zu)", cudaGetErrorString(e),
+                      tiles, plan->W * 32, smem);
+            throw OscbFail{OSCB_ECUDA};
+        }
+    }
+    k_from_tile_layout<T><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(d_phi.p, d_io.p, n, R, RT);
+    if (out->final_phases) d_io.download(out->final_phases, tot, s);
+    if (out->best_states) d_best_states.download(out->best_states, tot, s);
+    if (out->best_objective) d_best.download(out->best_objective, R, s);
+    std::vector<double> h_energy, h_btrace;
+    if (out->energy) { h_energy.resize((size_t)R * S); d_energy.download(h_energy.data(), h_energy.size(), s); }
+    if (out->best_trace) { h_btrace.resize((size_t)R * S); d_btrace.download(h_btrace.data(), h_btrace.size(), s); }
+    if (out->first_hit_step) d_first.download(h_first.data(), R, s);
+    unsigned long long flag = none;
+    OSCB_CUDA(cudaMemcpyAsync(&flag, g->d_nonfinite.p, sizeof(flag), cudaMemcpyDeviceToHost, s));
+    OSCB_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    OSCB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    for (int r = 0; r < R; ++r)
+        for (int64_t k = 0; k < S; ++k) {
+            if (out->energy) out->energy[(size_t)r * out->max_samples + k] = h_energy[(size_t)r * S + k];
+            if (out->best_trace) out->best_trace[(size_t)r * out->max_samples + k] = h_btrace[(size_t)r * S + k];
+        }
+    if (out->first_hit_step)
+        for (int r = 0; r < R; ++r) out->first_hit_step[r] = h_first[r];
+    out->device_ms = ms;
+    out->kernel_launches = 1;
+    out->kernel_used = OSCB_KERNEL_RESIDENT;
+    out->replicas_per_cta = RT;
+    out->smem_bytes = (int64_t)smem;
+    if (flag != none) {
+        out->nonfinite[2] = (int64_t)(flag >> 36);
+        out->nonfinite[0] = (int64_t)((flag >> 20) & 0xFFFFull);
+        out->nonfinite[1] = (int64_t)(flag & 0xFFFFFull);
+        set_error("non-finite phase for oscillator %lld (replica row %lld) after step %lld; parameters are numerically unstable",
+                  (long long)out->nonfinite[1], (long long)out->nonfinite[0], (long long)out->nonfinite[2]);
+        throw OscbFail{OSCB_ENONFINITE};
+    }
+}
+
+static void run_resident(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t cadence,
+                         const std::vector<long long> &sample_steps, const uint64_t *seeds, int64_t R,
+                         const double *phi0, const double *noise, oscb_run_outputs *out)
+{
+    ResidentConfig cfg;
+    OSCB_REQUIRE(choose_resident_config(g, p->precision, p->n_states, R, p->replicas_per_cta, &cfg),
+                 "the resident kernel cannot hold this problem (n = %lld, max degree %lld); use the streaming kernel",
+                 (long long)g->n, (long long)g->max_degree);
+    if (p->precision == OSCB_PREC_F64)
+        run_resident_impl<double, 512, true>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
+    else
+        run_resident_impl<float, 1024, false>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
 }
 
 } // namespace oscb

@@ -268,8 +268,8 @@ def test_noise_increment_std(pkg, kernel):
     """reference test_dynamics.py:386-399: with K ~ 0 and ks = 0 the per-step increment has
     std kn*sqrt(h)."""
     J = pkg.CouplingMatrix.from_edges(4000, [(0, 1, 1.0)])
-    params = pkg.SolverParams(K=1e-12, ks_max=0.0, kn=0.5, h=0.01, t_stop=0.01, seed=3)
-    b = pkg.run_batch(J, params, "maxcut", [3, 4, 5, 6], kernel=kernel)
+    params = pkg.SolverParams(K=1e-12, ks_max=0.0, kn=0.5, h=0.01, t_stop=1.0, seed=3)
+    b = pkg.run_batch(J, params, "maxcut", [3, 4, 5, 6], kernel=kernel, steps=1)
     start = np.stack([pkg.NoiseSource(s).initial_phases(4000) for s in (3, 4, 5, 6)])
     d = b.final_phases - start
     d -= np.round(d)
