@@ -146,13 +146,16 @@ int oscb_run(oscb_graph *g, const oscb_run_params *params, const uint64_t *seeds
 
 /* Host-only: the graph compiler of the persistent kernel (no GPU needed).  Turns a canonical CSR
  * (model.py:135-149) into the sliced-ELL neighbour stream for tiles of `replicas_per_cta`
- * replicas and CTAs of at most `max_threads` threads.  Call once with ids == NULL to get the
- * sizes, then again with buffers: warp_start [warps], quad_of [warps*rounds*(32/replicas_per_cta)],
- * ginfo [warps*rounds], ids [4*group_rows*(32/replicas_per_cta)] (u16; id n = padding). */
+ * replicas, CTAs of at most `max_threads` threads and (cos, sin) pairs of `pair_bytes` bytes.
+ * keep_order != 0 keeps every row in CSR order (float64 parity mode).  Call once with
+ * ids == NULL for the sizes, then with buffers: warp_start [warps], rows [warps*rounds*4*C],
+ * ginfo [warps*rounds], ids [4*(group_rows+1)*C] with C = 32/replicas_per_cta.  Row and
+ * neighbour ids are pre-multiplied by replicas_per_cta; values >= n*replicas_per_cta are padding. */
 int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices,
-                            int32_t replicas_per_cta, int32_t max_threads, int32_t *warps,
-                            int32_t *rounds, int64_t *group_rows, int32_t *warp_start,
-                            int32_t *quad_of, uint32_t *ginfo, uint16_t *ids);
+                            int32_t replicas_per_cta, int32_t max_threads, int32_t pair_bytes,
+                            int32_t keep_order, int32_t *warps, int32_t *rounds, int64_t *group_rows,
+                            int64_t *bank_conflicts, int32_t *warp_start, uint16_t *rows,
+                            uint32_t *ginfo, uint16_t *ids);
 
 #ifdef __cplusplus
 }

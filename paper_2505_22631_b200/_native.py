@@ -71,8 +71,9 @@ SYMBOLS = {
                             C.c_int32, C.c_int32, _P, _P]),
     "oscb_score": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P]),
     "oscb_energy": (C.c_int, [_P, C.c_int64, _P, _P]),
-    "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
-                                          C.POINTER(C.c_int32), C.POINTER(C.c_int64), _P, _P, _P, _P]),
+    "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64), _P, _P, _P, _P]),
     "oscb_run": (C.c_int, [_P, C.POINTER(RunParams), _P, C.c_int64, _P, _P, C.POINTER(RunOutputs)]),
 }
 

@@ -658,14 +658,16 @@ int oscb_energy(oscb_graph *g, int64_t R, const double *phi, double *energy)
 }
 
 int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t replicas_per_cta,
-                            int32_t max_threads, int32_t *warps, int32_t *rounds, int64_t *group_rows,
-                            int32_t *warp_start, int32_t *quad_of, uint32_t *ginfo, uint16_t *ids)
+                            int32_t max_threads, int32_t pair_bytes, int32_t keep_order, int32_t *warps,
+                            int32_t *rounds, int64_t *group_rows, int64_t *bank_conflicts, int32_t *warp_start,
+                            uint16_t *rows, uint32_t *ginfo, uint16_t *ids)
 {
     return guarded([&]() -> int {
-        OSCB_REQUIRE(n >= 1 && n <= 65534 && indptr && warps && rounds && group_rows, "bad argument");
+        OSCB_REQUIRE(n >= 1 && indptr && warps && rounds && group_rows, "bad argument");
         const int RT = replicas_per_cta;
         OSCB_REQUIRE(RT >= 1 && RT <= 32 && (RT & (RT - 1)) == 0, "replicas_per_cta must be a power of two <= 32");
         OSCB_REQUIRE(max_threads >= 32 && max_threads <= 1024 && max_threads % 32 == 0, "bad max_threads");
+        OSCB_REQUIRE(pair_bytes == 8 || pair_bytes == 16, "pair_bytes must be 8 or 16");
         const int64_t nnz = indptr[n];
         std::vector<int> ip(n + 1), ix(nnz);
         for (int64_t i = 0; i <= n; ++i) ip[i] = (int)indptr[i];
@@ -673,14 +675,15 @@ int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *ind
         int W, T;
         tile_shape(n, RT, max_threads, &W, &T);
         ResidentStreamHost h;
-        compile_resident_stream((int)n, ip.data(), ix.data(), nullptr, RT, W, T, &h);
+        compile_resident_stream((int)n, ip.data(), ix.data(), nullptr, RT, W, T, pair_bytes, keep_order != 0, &h);
         *warps = W;
         *rounds = T;
         *group_rows = h.n_group_rows;
+        if (bank_conflicts) *bank_conflicts = h.conflicts;
         if (ids) {
-            OSCB_REQUIRE(warp_start && quad_of && ginfo, "NULL output");
+            OSCB_REQUIRE(warp_start && rows && ginfo, "NULL output");
             std::copy(h.warp_start.begin(), h.warp_start.end(), warp_start);
-            std::copy(h.quad_of.begin(), h.quad_of.end(), quad_of);
+            std::copy(h.rows.begin(), h.rows.end(), rows);
             std::copy(h.ginfo.begin(), h.ginfo.end(), ginfo);
             for (size_t q = 0; q < h.stream.size(); ++q) {
                 ids[4 * q + 0] = (uint16_t)(h.stream[q].x & 0xffffu);

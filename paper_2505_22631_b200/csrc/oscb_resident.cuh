@@ -14,15 +14,18 @@
 // every (warp, round, row position) the C rows are padded to a common number G of 4-neighbour
 // groups.  So the inner loop has a warp-uniform trip count, needs no row pointers, and reads
 // the stream as one contiguous C*8-byte run per group:
-//     stream[gp * C + slot_in_warp] = four u16 neighbour ids   (dummy id n -> a zero pair)
+//     stream[gp * C + slot_in_warp] = four u16 ids, each already multiplied by RT
+// (ids >= n*RT name all-zero padding rows, one per shared-memory bank class, so padding never
+// adds a bank conflict).  In the throughput mode the compiler also orders every row's
+// neighbours so that the slots that share a shared-memory wavefront hit disjoint banks.
 //
 // Per step:
-//   pass A: per own row, gather sum_j w c_j / sum_j w s_j over the stream, apply
-//           K, SHIL(ks(t)), Philox noise and the wrap, store the new phase (the tile's phase
-//           slab [n][RT] in global memory, L2 resident -- each element is touched by one thread);
+//   pass A: per own row, gather sum_j w (c_j, s_j) over the stream with packed f32x2 adds,
+//           apply K, SHIL(ks(t)), Philox noise and the wrap, store the new phase (the tile's
+//           phase slab [n][RT] in global memory, L2 resident -- one thread per element);
 //   barrier (every gather of the old pairs is done)
 //   pass B: recompute the (cos, sin) pairs of the own rows into shared memory; on scoring
-//           steps also the lattice states (dynamics.py:203-213), bit-packed;
+//           steps also the lattice states (dynamics.py:203-213), one byte per cell;
 //   barrier
 //   scoring steps (reference cadence / trace samples): cut or conflict count over each own
 //           row's neighbours j > i, fixed-order reduction per replica, strict-improvement best
@@ -36,6 +39,8 @@
 
 namespace oscb {
 
+#define OSCB_PAD_ROWS 16 // all-zero rows after row n-1, one per bank class
+
 struct ResidentArgs {
     int n;
     int R_real;                 // replicas that exist; tiles are padded up to RT
@@ -43,13 +48,12 @@ struct ResidentArgs {
     int C;                      // slots per warp = 32 / RT
     int T;                      // rounds (quads per slot)
     int W;                      // warps per CTA
-    int SB, wpr;                // state bits per cell, 32-bit state words per row
-    int n_group_rows;           // stream length in units of C groups
-    const int *warp_start;      // [W]      first group row of each warp's stream
-    const int *quad_of;         // [W*T*C]  quad | visiting order << 24, or -1
-    const uint32_t *ginfo;      // [W*T]    G of the four row positions, one byte each
-    const uint2 *stream;        // [n_group_rows * C]
-    const void *wstream;        // [n_group_rows * C * 4] weights in T (stream order); null = unit
+    int n_group_rows;           // stream length in units of C groups (without the prefetch pad)
+    const int *warp_start;      // [W]         first group row of each warp's stream
+    const uint16_t *rows;       // [W*T*4*C]   own row * RT of (warp, round, position, slot); >= n*RT: none
+    const uint32_t *ginfo;      // [W*T]       G of the four row positions, one byte each
+    const uint2 *stream;        // [(n_group_rows + 1) * C]
+    const void *wstream;        // [(n_group_rows + 1) * C * 4] weights in T (stream order); null = unit
     void *phi;                  // [tiles][n][RT] in T
     const uint64_t *seeds;      // [R_pad]
     long long step_begin, step_end;
@@ -77,22 +81,21 @@ struct ResidentArgs {
 
 // byte offsets of the regions inside dynamic shared memory (host and device agree on this)
 struct ResidentSmem {
-    size_t cs, st, quad, ginfo, wstart, part, misc, stream, wstream, total;
-    __host__ __device__ static ResidentSmem make(int n, int RT, int C, int T, int W, int wpr, size_t pair_bytes,
+    size_t cs, st, rows, ginfo, part, misc, stream, wstream, total;
+    __host__ __device__ static ResidentSmem make(int n, int RT, int C, int T, int W, size_t pair_bytes,
                                                  size_t weight_bytes, int n_group_rows, bool idx_smem, bool weighted)
     {
         ResidentSmem s;
         size_t o = 0;
         auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~(size_t)15; return at; };
-        s.cs = take((size_t)(n + 1) * RT * pair_bytes);
-        s.st = take((size_t)(n + 1) * wpr * 4);
-        s.quad = take((size_t)W * T * C * 4);
+        s.cs = take((size_t)(n + OSCB_PAD_ROWS) * RT * pair_bytes);
+        s.st = take((size_t)(n + OSCB_PAD_ROWS) * RT);
+        s.rows = take((size_t)W * T * 4 * C * 2);
         s.ginfo = take((size_t)W * T * 4);
-        s.wstart = take((size_t)W * 4);
         s.part = take((size_t)W * RT * 8);
         s.misc = take((size_t)RT * 16 + 32);
-        s.stream = take(idx_smem ? (size_t)n_group_rows * C * 8 : 0);
-        s.wstream = take(idx_smem && weighted ? (size_t)n_group_rows * C * 4 * weight_bytes : 0);
+        s.stream = take(idx_smem ? (size_t)(n_group_rows + 1) * C * 8 : 0);
+        s.wstream = take(idx_smem && weighted ? (size_t)(n_group_rows + 1) * C * 4 * weight_bytes : 0);
         s.total = o;
         return s;
     }
@@ -113,17 +116,44 @@ __device__ __forceinline__ double tile_reduce(double v, int RT, double *part, in
     return tot;
 }
 
+// shared-memory pair load at a 32-bit shared address; the address of row id*RT is one IMAD/LEA
+// off the lane's base (PTX mad.lo keeps ptxas from splitting it into shift + mask + add)
+__device__ __forceinline__ void lds_pair(uint32_t addr, float2 &v)
+{
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void lds_pair(uint32_t addr, double2 &v)
+{
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+}
+template <int PSH> __device__ __forceinline__ uint32_t pair_addr(uint32_t id, uint32_t base)
+{
+    uint32_t a;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(a) : "r"(id), "n"(1 << PSH), "r"(base));
+    return a;
+}
+
+// packed pair arithmetic: one FADD2 / FFMA2 per (cos, sin) pair on sm_100a
+__device__ __forceinline__ float2 pair_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ double2 pair_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 pair_fma(float w, float2 v, float2 acc) { return __ffma2_rn(make_float2(w, w), v, acc); }
+__device__ __forceinline__ double2 pair_fma(double w, double2 v, double2 acc)
+{
+    return make_double2(fma(w, v.x, acc.x), fma(w, v.y, acc.y));
+}
+
 template <typename T, int MAXT, bool IDX_SMEM, bool WEIGHTED, bool STRICT>
 __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
 {
     using T2 = typename Vec2<T>::type;
+    constexpr int PSH = sizeof(T2) == 8 ? 3 : 4;   // log2 bytes per pair
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, NT = blockDim.x, W = a.W;
-    const int RT = a.RT, n = a.n, C = a.C, TR = a.T, SB = a.SB, wpr = a.wpr;
-    const ResidentSmem L = ResidentSmem::make(n, RT, C, TR, W, wpr, sizeof(T2), sizeof(T), a.n_group_rows, IDX_SMEM, WEIGHTED);
+    const int RT = a.RT, n = a.n, C = a.C, TR = a.T;
+    const ResidentSmem L = ResidentSmem::make(n, RT, C, TR, W, sizeof(T2), sizeof(T), a.n_group_rows, IDX_SMEM, WEIGHTED);
     T2 *cs = reinterpret_cast<T2 *>(smem_raw + L.cs);
-    uint32_t *stw = reinterpret_cast<uint32_t *>(smem_raw + L.st);
-    int *quad_s = reinterpret_cast<int *>(smem_raw + L.quad);
+    uint8_t *stb = smem_raw + L.st;
+    uint16_t *rows_s = reinterpret_cast<uint16_t *>(smem_raw + L.rows);
     uint32_t *ginfo_s = reinterpret_cast<uint32_t *>(smem_raw + L.ginfo);
     double *part = reinterpret_cast<double *>(smem_raw + L.part);
     double *best_s = reinterpret_cast<double *>(smem_raw + L.misc);          // [RT]
@@ -139,33 +169,40 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
     const int rg = tile * RT + r;                  // global replica index
     const bool live = rg < a.R_real;
     const uint64_t seed = a.seeds[rg];
-    T *phi = reinterpret_cast<T *>(a.phi) + (size_t)tile * n * RT;
-    const uint32_t smask = (SB >= 32) ? 0xffffffffu : ((1u << SB) - 1u);
-    const int sshift = (r * SB) & 31, sword = (r * SB) >> 5;
-    int cells_per_word = 32 / SB;                  // lanes whose cells share one state word
-    if (cells_per_word > RT) cells_per_word = RT;
+    T *phi = reinterpret_cast<T *>(a.phi) + (size_t)tile * n * RT + r;       // + (row * RT)
+    unsigned char *cs_lane = smem_raw + L.cs + r * sizeof(T2);               // + (row * RT) << PSH
+    const uint32_t cs_lane32 = (uint32_t)__cvta_generic_to_shared(cs_lane);  // same, as a shared address
+    auto pair_at = [&](uint32_t idRT) -> T2 { T2 v; lds_pair(pair_addr<PSH>(idRT, cs_lane32), v); return v; };
+    uint8_t *st_lane = stb + r;                                              // + (row * RT)
+    const int nRT = n * RT;
 
     // ---- prologue: stage the plan, build (cos, sin) of the current phases --------------------
-    for (int q = tid; q < W * TR * C; q += NT) quad_s[q] = a.quad_of[q];
+    for (int q = tid; q < W * TR * 4 * C; q += NT) rows_s[q] = a.rows[q];
     for (int q = tid; q < W * TR; q += NT) ginfo_s[q] = a.ginfo[q];
     if (IDX_SMEM) {
         uint2 *dst = reinterpret_cast<uint2 *>(smem_raw + L.stream);
-        for (int q = tid; q < a.n_group_rows * C; q += NT) dst[q] = a.stream[q];
+        for (int q = tid; q < (a.n_group_rows + 1) * C; q += NT) dst[q] = a.stream[q];
         if (WEIGHTED) {
             T *wd = reinterpret_cast<T *>(smem_raw + L.wstream);
             const T *ws = reinterpret_cast<const T *>(a.wstream);
-            for (int q = tid; q < a.n_group_rows * C * 4; q += NT) wd[q] = ws[q];
+            for (int q = tid; q < (a.n_group_rows + 1) * C * 4; q += NT) wd[q] = ws[q];
         }
     }
-    for (int q = tid; q < n * RT; q += NT) {
-        T s, co;
-        phase_trig(phi[q], s, co);
-        T2 v; v.x = co; v.y = s;
-        cs[q] = v;
+    {
+        const T *slab = reinterpret_cast<const T *>(a.phi) + (size_t)tile * n * RT;
+        for (int q = tid; q < nRT; q += NT) {
+            T s, co;
+            phase_trig(slab[q], s, co);
+            T2 v; v.x = co; v.y = s;
+            cs[q] = v;
+        }
+        for (int q = tid; q < OSCB_PAD_ROWS * RT; q += NT) {      // padding rows: zero pairs, state 255
+            T2 zero; zero.x = T(0); zero.y = T(0);
+            cs[nRT + q] = zero;
+            stb[nRT + q] = 255;
+        }
     }
     if (tid < RT) {
-        T2 zero; zero.x = T(0); zero.y = T(0);
-        cs[n * RT + tid] = zero;                   // the dummy neighbour used by stream padding
         best_s[tid] = a.best_obj[tile * RT + tid];
         improved_s[tid] = 0;
     }
@@ -173,61 +210,59 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
     const int gp0 = a.warp_start[warp];
     __syncthreads();
 
-    // own-row iteration helpers -------------------------------------------------------------
-    // quad word of (round t): quad index | order << 20, or -1 when the slot has no quad
-    auto quad_word = [&](int t) -> int { return quad_s[(warp * TR + t) * C + c]; };
+    // own row (pre-multiplied by RT) of (round t, position kk); >= nRT when the slot has none
+    auto own_row = [&](int t, int kk) -> int { return rows_s[((warp * TR + t) * 4 + kk) * C + c]; };
 
-    // lattice states of the own rows -> stw (bit-packed, one word group per row)
+    // lattice states of the own rows -> stb
     auto write_states = [&]() {
-        for (int t = 0; t < TR; ++t) {
-            const int qw = quad_word(t);
-            const int quad = qw & 0xFFFFF;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = 4 * quad + k;
-                const bool valid = qw >= 0 && i < n;
-                uint32_t v = 0;
-                if (valid) v = (uint32_t)threshold_state((double)phi[i * RT + r], a.tc.n_states) << sshift;
-                for (int off = 1; off < cells_per_word; off <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, off);
-                if (valid && (r & (cells_per_word - 1)) == 0) stw[i * wpr + sword] = v;
+        for (int t = 0; t < TR; ++t)
+            for (int kk = 0; kk < 4; ++kk) {
+                const int iRT = own_row(t, kk);
+                if (iRT < nRT) st_lane[iRT] = (uint8_t)threshold_state((double)phi[iRT], a.tc.n_states);
             }
-        }
     };
-    auto load_state = [&](int j) -> uint32_t { return (stw[j * wpr + sword] >> sshift) & smask; };
 
-    // score the state currently in cs / phi / stw; sample_col >= 0 also records that trace column
+    // score the state currently in cs / stb; sample_col >= 0 also records that trace column
     auto score_current = [&](long long step_label, int sample_col) {
         double obj_part = 0.0, en_part = 0.0;
         int gp = gp0;
         for (int t = 0; t < TR; ++t) {
-            const int qw = quad_word(t);
             const uint32_t g4 = ginfo_s[warp * TR + t];
-            const int quad = qw & 0xFFFFF, order = (qw >> 20) & 0xFF;
             for (int kk = 0; kk < 4; ++kk) {
                 const int G = (g4 >> (8 * kk)) & 0xFF;
-                const int i = 4 * quad + ((order >> (2 * kk)) & 3);
-                const bool valid = qw >= 0 && i < n;
-                if (valid) {
-                    const uint32_t si = load_state(i);
-                    const T2 own = cs[i * RT + r];
+                const int iRT = own_row(t, kk);
+                if (iRT < nRT) {
+                    const uint32_t si = st_lane[iRT];
+                    const T2 own = pair_at(iRT);
+                    int count = 0;
+                    double wsum = 0.0;
                     for (int g = 0; g < G; ++g) {
                         const uint2 pk = stream[(gp + g) * C + c];
                         const int jj[4] = {(int)(pk.x & 0xffffu), (int)(pk.x >> 16), (int)(pk.y & 0xffffu), (int)(pk.y >> 16)};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const int j = jj[u];
-                            if (j > i && j < n) {
-                                const double w = WEIGHTED ? (double)wstream[((size_t)(gp + g) * C + c) * 4 + u] : 1.0;
-                                const bool same = load_state(j) == si;
-                                if (a.maximize) { if (!same) obj_part += w; }
-                                else            { if (same) obj_part += 1.0; }
-                                if (sample_col >= 0) {
-                                    const T2 v = cs[j * RT + r];
-                                    en_part += w * ((double)own.x * (double)v.x + (double)own.y * (double)v.y);
+                            const int jRT = jj[u];
+                            if (jRT > iRT && jRT < nRT) {                  // canonical pairs i < j only
+                                const bool same = st_lane[jRT] == si;
+                                const bool hit = a.maximize ? !same : same;
+                                if (WEIGHTED) {
+                                    const double w = (double)wstream[((size_t)(gp + g) * C + c) * 4 + u];
+                                    if (hit) wsum += a.maximize ? w : 1.0;
+                                    if (sample_col >= 0) {
+                                        const T2 v = pair_at(jRT);
+                                        en_part += w * ((double)own.x * (double)v.x + (double)own.y * (double)v.y);
+                                    }
+                                } else {
+                                    count += hit ? 1 : 0;
+                                    if (sample_col >= 0) {
+                                        const T2 v = pair_at(jRT);
+                                        en_part += (double)own.x * (double)v.x + (double)own.y * (double)v.y;
+                                    }
                                 }
                             }
                         }
                     }
+                    obj_part += WEIGHTED ? wsum : (double)count;
                 }
                 gp += G;
             }
@@ -247,16 +282,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
         __syncthreads();
         if (improved_s[r] && live) {           // strict improvement: publish this replica's states
             uint8_t *dst = a.best_states + (size_t)rg * n;
-            for (int t = 0; t < TR; ++t) {
-                const int qw = quad_word(t);
-                if (qw < 0) continue;
-                const int quad = qw & 0xFFFFF;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int i = 4 * quad + k;
-                    if (i < n) dst[i] = (uint8_t)load_state(i);
+            for (int t = 0; t < TR; ++t)
+                for (int kk = 0; kk < 4; ++kk) {
+                    const int iRT = own_row(t, kk);
+                    if (iRT < nRT) dst[iRT >> a.log2RT] = st_lane[iRT];
                 }
-            }
         }
         if (sample_col >= 0) {
             const double en = tile_reduce(en_part, RT, part, tid, W);
@@ -286,66 +316,70 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
         const double ks = ks_s[step & 1];
         const T hks = (T)(a.h * ks);
         const bool is_sample = sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] == step;
-        const bool do_score = is_sample || (a.cadence > 0 && (step - a.step_begin + a.step_begin) % a.cadence == 0);
-        int gp = gp0;
-        // pass A: gather + update
+        const bool do_score = is_sample || (a.cadence > 0 && step % a.cadence == 0);
+        // pass A: gather + update.  The stream of a warp is contiguous, so the next group is
+        // always prefetched one iteration ahead (the pad row covers the last one).
+        const uint2 *sp = stream + (size_t)gp0 * C + c;
+        const T *wp = WEIGHTED ? wstream + ((size_t)gp0 * C + c) * 4 : nullptr;
+        uint2 pk = *sp;
 #pragma unroll 1
         for (int t = 0; t < TR; ++t) {
-            const int qw = quad_word(t);
             const uint32_t g4 = ginfo_s[warp * TR + t];
-            const int quad = qw & 0xFFFFF, order = (qw >> 20) & 0xFF;
             T z[4] = {T(0), T(0), T(0), T(0)};
-            if (a.noise_mode == 0 && qw >= 0) normals4(noise_block(seed, (uint64_t)step, (uint32_t)quad), z);
+            if (a.noise_mode == 0) {
+                const int first = own_row(t, 0);
+                if (first < nRT) normals4(noise_block(seed, (uint64_t)step, (uint32_t)(first >> a.log2RT) >> 2), z);
+            }
 #pragma unroll 1
             for (int kk = 0; kk < 4; ++kk) {
                 const int G = (g4 >> (8 * kk)) & 0xFF;      // warp-uniform trip count
-                const int k = (order >> (2 * kk)) & 3;
-                const int i = 4 * quad + k;
-                const bool valid = qw >= 0 && i < n;
-                const int io = valid ? i : n;               // invalid rows read the zero pair
-                const T p = valid ? phi[i * RT + r] : T(0);
-                const T2 own = cs[io * RT + r];
+                const int iRT = own_row(t, kk);
+                const bool valid = iRT < nRT;
+                const T p = valid ? phi[iRT] : T(0);
+                const T2 own = pair_at(iRT);
                 const T ci = own.x, si = own.y;
                 T acc;
                 if (STRICT) {
                     // reference order: acc += w * (s_i c_j - c_i s_j), one neighbour at a time
                     double accd = 0.0;
                     for (int g = 0; g < G; ++g) {
-                        const uint2 pk = stream[(gp + g) * C + c];
-                        const int jj[4] = {(int)(pk.x & 0xffffu), (int)(pk.x >> 16), (int)(pk.y & 0xffffu), (int)(pk.y >> 16)};
+                        sp += C;
+                        const uint2 nx = *sp;
+                        const uint32_t jj[4] = {pk.x & 0xffffu, pk.x >> 16, pk.y & 0xffffu, pk.y >> 16};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
-                            const T2 v = cs[jj[u] * RT + r];
-                            const double w = WEIGHTED ? (double)wstream[((size_t)(gp + g) * C + c) * 4 + u] : 1.0;
+                            const T2 v = pair_at(jj[u]);
+                            const double w = WEIGHTED ? (double)wp[u] : 1.0;
                             const double term = __dsub_rn(__dmul_rn((double)si, (double)v.x), __dmul_rn((double)ci, (double)v.y));
                             accd = __dadd_rn(accd, __dmul_rn(w, term));
                         }
+                        if (WEIGHTED) wp += 4 * C;
+                        pk = nx;
                     }
                     acc = (T)accd;
                 } else {
-                    T ac = T(0), as = T(0);
+                    T2 sum; sum.x = T(0); sum.y = T(0);
+#pragma unroll 2
                     for (int g = 0; g < G; ++g) {
-                        const uint2 pk = stream[(gp + g) * C + c];
-                        const T2 v0 = cs[(int)(pk.x & 0xffffu) * RT + r];
-                        const T2 v1 = cs[(int)(pk.x >> 16) * RT + r];
-                        const T2 v2 = cs[(int)(pk.y & 0xffffu) * RT + r];
-                        const T2 v3 = cs[(int)(pk.y >> 16) * RT + r];
+                        sp += C;
+                        const uint2 nx = *sp;
+                        const T2 v0 = pair_at(pk.x & 0xffffu), v1 = pair_at(pk.x >> 16);
+                        const T2 v2 = pair_at(pk.y & 0xffffu), v3 = pair_at(pk.y >> 16);
                         if (WEIGHTED) {
-                            const T *wp = wstream + ((size_t)(gp + g) * C + c) * 4;
-                            const T w0 = wp[0], w1 = wp[1], w2 = wp[2], w3 = wp[3];
-                            ac = fma(w0, v0.x, ac); as = fma(w0, v0.y, as);
-                            ac = fma(w1, v1.x, ac); as = fma(w1, v1.y, as);
-                            ac = fma(w2, v2.x, ac); as = fma(w2, v2.y, as);
-                            ac = fma(w3, v3.x, ac); as = fma(w3, v3.y, as);
+                            sum = pair_fma(wp[0], v0, sum);
+                            sum = pair_fma(wp[1], v1, sum);
+                            sum = pair_fma(wp[2], v2, sum);
+                            sum = pair_fma(wp[3], v3, sum);
+                            wp += 4 * C;
                         } else {
-                            ac += (v0.x + v1.x) + (v2.x + v3.x);
-                            as += (v0.y + v1.y) + (v2.y + v3.y);
+                            sum = pair_add(sum, pair_add(pair_add(v0, v1), pair_add(v2, v3)));
                         }
+                        pk = nx;
                     }
-                    acc = si * ac - ci * as;
+                    acc = si * sum.x - ci * sum.y;
                 }
-                gp += G;
                 if (valid) {
+                    const int i = iRT >> a.log2RT, k = i & 3;
                     const T shil = shil_term(p, si, ci, a.tc);
                     T kick = (k == 0) ? z[0] : (k == 1) ? z[1] : (k == 2) ? z[2] : z[3];
                     if (a.noise_mode == 1)
@@ -358,7 +392,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
                         x = fma(hK, acc, fma(-hks, shil, fma(knsh, kick, p)));
                     }
                     if (!isfinite(x) && live) flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)rg, (uint32_t)i);
-                    phi[i * RT + r] = wrap_unit(x);
+                    phi[iRT] = wrap_unit(x);
                 }
             }
         }
@@ -367,25 +401,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_resident(const ResidentArgs a)
         // pass B: (cos, sin) of the new phases; lattice states when this step is scored
 #pragma unroll 1
         for (int t = 0; t < TR; ++t) {
-            const int qw = quad_word(t);
-            const int quad = qw & 0xFFFFF;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int i = 4 * quad + k;
-                const bool valid = qw >= 0 && i < n;
-                T p = T(0);
-                if (valid) {
-                    p = phi[i * RT + r];
+            for (int kk = 0; kk < 4; ++kk) {
+                const int iRT = own_row(t, kk);
+                if (iRT < nRT) {
+                    const T p = phi[iRT];
                     T s, co;
                     phase_trig(p, s, co);
                     T2 v; v.x = co; v.y = s;
-                    cs[i * RT + r] = v;
-                }
-                if (do_score) {                            // CTA-uniform branch
-                    uint32_t v = 0;
-                    if (valid) v = (uint32_t)threshold_state((double)p, a.tc.n_states) << sshift;
-                    for (int off = 1; off < cells_per_word; off <<= 1) v |= __shfl_xor_sync(0xffffffffu, v, off);
-                    if (valid && (r & (cells_per_word - 1)) == 0) stw[i * wpr + sword] = v;
+                    *reinterpret_cast<T2 *>(cs_lane + ((size_t)iRT << PSH)) = v;
+                    if (do_score) st_lane[iRT] = (uint8_t)threshold_state((double)p, a.tc.n_states);
                 }
             }
         }

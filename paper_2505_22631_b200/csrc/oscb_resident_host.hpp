@@ -16,16 +16,15 @@ struct ResidentPlan {
     int RT = 1, log2RT = 0, C = 32, T = 1, W = 1;
     int n_group_rows = 0;
     bool weighted = false;
-    double fill = 1.0; // real neighbours / stream entries
-    DevBuf<int> warp_start, quad_of;
+    double fill = 1.0;          // real neighbours / stream entries
+    double bank_conflicts = 0;  // stream positions whose slots collide on a bank class / all positions
+    DevBuf<int> warp_start;
+    DevBuf<uint16_t> rows;
     DevBuf<uint32_t> ginfo;
     DevBuf<uint2> stream;
     DevBuf<float> w32;
     DevBuf<double> w64;
 };
-
-static inline int state_bits_for(int n_states) { return n_states <= 2 ? 1 : n_states <= 4 ? 2 : n_states <= 16 ? 4 : 8; }
-static inline int words_per_row(int RT, int SB) { return std::max(1, RT * SB / 32); }
 
 // warps per CTA for a tile of RT replicas: as many slots as there are quads to hand out, in
 // the fewest rounds the thread limit allows
@@ -42,19 +41,28 @@ static void tile_shape(int64_t n, int RT, int max_threads, int *W, int *T)
 
 // pure host result of the graph compiler (also exported for CPU-side tests)
 struct ResidentStreamHost {
-    std::vector<int> warp_start, quad_of;
-    std::vector<uint32_t> ginfo;
-    std::vector<uint2> stream;
-    std::vector<double> weights;
+    std::vector<int> warp_start;
+    std::vector<uint16_t> rows;     // [W*T*4*C] own row * RT, n*RT when the slot has none
+    std::vector<uint32_t> ginfo;    // [W*T]
+    std::vector<uint2> stream;      // [(n_group_rows + 1) * C] ids * RT; >= n*RT: zero padding rows
+    std::vector<double> weights;    // [(n_group_rows + 1) * C * 4]
     int n_group_rows = 0;
-    int64_t real = 0;
+    int64_t real = 0, positions = 0, conflicts = 0;
 };
 
+// `pair_bytes` (8: float2, 16: double2) fixes which slots share a shared-memory wavefront:
+// 128 bytes = 16 (8) lanes = H = max(1, 16 (8) / RT) consecutive slots, and row j sits in bank
+// class j mod H of that wavefront.  `keep_order` (parity mode) keeps every row in CSR order and
+// only picks conflict-free padding rows; otherwise each row's neighbours are also reordered so
+// that the H slots of a wavefront hit H different classes wherever the lists allow it.
 static void compile_resident_stream(int n, const int *indptr, const int *indices, const double *wts, int RT, int W,
-                                    int T, ResidentStreamHost *out)
+                                    int T, int pair_bytes, bool keep_order, ResidentStreamHost *out)
 {
     const int C = 32 / RT, S = W * C;
     const int Q = (n + 3) / 4;
+    const int H = std::max(1, std::min(C, (128 / pair_bytes) / RT));
+    OSCB_REQUIRE((int64_t)(n + OSCB_PAD_ROWS) * RT <= 65535, "n * replicas_per_cta too large for 16-bit stream ids");
+    OSCB_REQUIRE(H <= OSCB_PAD_ROWS, "internal: not enough padding rows");
     auto deg = [&](int i) { return i < n ? indptr[i + 1] - indptr[i] : 0; };
 
     // quads by total degree, heaviest first, dealt to the slots boustrophedon so that slot loads
@@ -64,8 +72,7 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
     std::vector<int> qdeg(Q);
     for (int q = 0; q < Q; ++q) qdeg[q] = deg(4 * q) + deg(4 * q + 1) + deg(4 * q + 2) + deg(4 * q + 3);
     std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return qdeg[x] > qdeg[y]; });
-    std::vector<int> &quad_of = out->quad_of;
-    quad_of.assign((size_t)W * T * C, -1);
+    std::vector<int> quad_of((size_t)W * T * C, -1);
     for (int64_t pos = 0; pos < (int64_t)T * S; ++pos) {
         const int t = (int)(pos / S), s_in = (int)(pos % S);
         const int slot = (t & 1) ? S - 1 - s_in : s_in;
@@ -74,51 +81,105 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
     }
 
     out->warp_start.assign(W, 0);
+    out->rows.assign((size_t)W * T * 4 * C, (uint16_t)(n * RT));
     out->ginfo.assign((size_t)W * T, 0);
     out->stream.clear();
     out->weights.clear();
-    out->real = 0;
+    out->real = out->positions = out->conflicts = 0;
     int group_rows = 0;
+    struct Item { int j; double w; };
     for (int w = 0; w < W; ++w) {
         out->warp_start[w] = group_rows;
         for (int t = 0; t < T; ++t) {
             int rows[32][4]; // [c][kk] row visited kk-th by slot c (or -1)
             int G[4] = {0, 0, 0, 0};
             for (int c = 0; c < C; ++c) {
-                int &qw = quad_of[((size_t)w * T + t) * C + c];
-                if (qw < 0) {
-                    for (int kk = 0; kk < 4; ++kk) rows[c][kk] = -1;
-                    continue;
-                }
-                const int quad = qw;
+                const int quad = quad_of[((size_t)w * T + t) * C + c];
+                for (int kk = 0; kk < 4; ++kk) rows[c][kk] = -1;
+                if (quad < 0) continue;
                 int ks[4] = {0, 1, 2, 3};
                 std::stable_sort(ks, ks + 4, [&](int x, int y) { return deg(4 * quad + x) > deg(4 * quad + y); });
-                int ord = 0;
                 for (int kk = 0; kk < 4; ++kk) {
-                    ord |= ks[kk] << (2 * kk);
                     const int i = 4 * quad + ks[kk];
                     rows[c][kk] = i < n ? i : -1;
                     G[kk] = std::max(G[kk], (deg(i) + 3) / 4);
                 }
-                qw = quad | (ord << 20);
             }
             for (int kk = 0; kk < 4; ++kk) {
                 OSCB_REQUIRE(G[kk] <= 255, "row degree too large for the resident kernel");
                 out->ginfo[(size_t)w * T + t] |= (uint32_t)G[kk] << (8 * kk);
+                const int P = 4 * G[kk];
+                // laid[c][p]: the entry slot c reads at position p (j = -1 - class for padding)
+                std::vector<std::vector<Item>> laid(C, std::vector<Item>(P, Item{-1, 0.0}));
+                for (int c = 0; c < C; ++c) {
+                    const int i = rows[c][kk];
+                    if (i >= 0) out->rows[(((size_t)w * T + t) * 4 + kk) * C + c] = (uint16_t)(i * RT);
+                }
+                for (int c0 = 0; c0 < C; c0 += H) {
+                    // remaining items of each slot of this wavefront group, bucketed by bank class
+                    std::vector<std::vector<std::vector<Item>>> bucket(H, std::vector<std::vector<Item>>(H));
+                    std::vector<int> left(H, 0);
+                    for (int hc = 0; hc < H; ++hc) {
+                        const int i = rows[c0 + hc][kk];
+                        if (i < 0) continue;
+                        for (int e = indptr[i + 1] - 1; e >= indptr[i]; --e)        // reversed: pop_back() yields CSR order
+                            bucket[hc][keep_order ? 0 : indices[e] % H].push_back(Item{indices[e], wts ? wts[e] : 1.0});
+                        left[hc] = deg(i);
+                    }
+                    for (int p = 0; p < P; ++p) {
+                        std::vector<char> used(H, 0);
+                        std::vector<int> who(H);
+                        std::iota(who.begin(), who.end(), 0);
+                        // the slot with the least slack (fewest spare padding positions) chooses first
+                        std::stable_sort(who.begin(), who.end(), [&](int x, int y) { return left[x] > left[y]; });
+                        std::vector<int> pad_slots;
+                        for (int hc : who) {
+                            Item pick{-1, 0.0};
+                            if (left[hc] > 0) {
+                                if (keep_order) {
+                                    pick = bucket[hc][0].back();
+                                    bucket[hc][0].pop_back();
+                                } else {
+                                    int best = -1;
+                                    for (int cls = 0; cls < H; ++cls)
+                                        if (!used[cls] && !bucket[hc][cls].empty() &&
+                                            (best < 0 || bucket[hc][cls].size() > bucket[hc][best].size()))
+                                            best = cls;
+                                    const bool spare = (P - p) > left[hc];
+                                    if (best < 0 && spare) { pad_slots.push_back(hc); continue; }
+                                    if (best < 0)   // forced conflict: take from the fullest bucket
+                                        for (int cls = 0; cls < H; ++cls)
+                                            if (!bucket[hc][cls].empty() && (best < 0 || bucket[hc][cls].size() > bucket[hc][best].size()))
+                                                best = cls;
+                                    pick = bucket[hc][best].back();
+                                    bucket[hc][best].pop_back();
+                                }
+                                --left[hc];
+                                const int cls = pick.j % H;
+                                if (used[cls]) ++out->conflicts;
+                                used[cls] = 1;
+                                laid[c0 + hc][p] = pick;
+                                ++out->real;
+                            } else {
+                                pad_slots.push_back(hc);
+                            }
+                        }
+                        for (int hc : pad_slots) {         // padding takes a class nobody reads
+                            int cls = 0;
+                            while (cls < H - 1 && used[cls]) ++cls;
+                            used[cls] = 1;
+                            laid[c0 + hc][p] = Item{-1 - cls, 0.0};
+                        }
+                        ++out->positions;
+                    }
+                }
                 for (int gidx = 0; gidx < G[kk]; ++gidx) {
                     for (int c = 0; c < C; ++c) {
                         uint32_t ids[4];
                         for (int u = 0; u < 4; ++u) {
-                            const int i = rows[c][kk];
-                            const int e = i >= 0 ? indptr[i] + 4 * gidx + u : -1;
-                            if (i >= 0 && e < indptr[i + 1]) {
-                                ids[u] = (uint32_t)indices[e];
-                                out->weights.push_back(wts ? wts[e] : 1.0);
-                                ++out->real;
-                            } else {
-                                ids[u] = (uint32_t)n; // the zero pair
-                                out->weights.push_back(0.0);
-                            }
+                            const Item &it = laid[c][4 * gidx + u];
+                            ids[u] = it.j >= 0 ? (uint32_t)(it.j * RT) : (uint32_t)((n + (-1 - it.j)) * RT);
+                            out->weights.push_back(it.j >= 0 ? it.w : 0.0);
                         }
                         out->stream.push_back(make_uint2(ids[0] | (ids[1] << 16), ids[2] | (ids[3] << 16)));
                     }
@@ -128,9 +189,14 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
         }
     }
     out->n_group_rows = group_rows;
+    for (int c = 0; c < C; ++c) {          // the prefetch pad row
+        const uint32_t pad = (uint32_t)(n * RT);
+        out->stream.push_back(make_uint2(pad | (pad << 16), pad | (pad << 16)));
+        for (int u = 0; u < 4; ++u) out->weights.push_back(0.0);
+    }
 }
 
-static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, int W, int T)
+static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, int W, int T, int pair_bytes, bool keep_order)
 {
     auto plan = std::make_shared<ResidentPlan>();
     plan->RT = RT;
@@ -141,13 +207,15 @@ static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, 
     plan->T = T;
     plan->weighted = !g->unit_weights;
     ResidentStreamHost h;
-    compile_resident_stream((int)g->n, g->h_indptr.data(), g->h_indices.data(), g->h_w.data(), RT, W, T, &h);
+    compile_resident_stream((int)g->n, g->h_indptr.data(), g->h_indices.data(), g->h_w.data(), RT, W, T, pair_bytes,
+                            keep_order, &h);
     OSCB_REQUIRE(h.real == g->nnz, "internal: resident plan lost neighbours (%lld of %lld)", (long long)h.real, (long long)g->nnz);
     plan->n_group_rows = h.n_group_rows;
-    plan->fill = h.stream.empty() ? 1.0 : (double)h.real / (4.0 * (double)h.stream.size());
+    plan->fill = h.n_group_rows == 0 ? 1.0 : (double)h.real / (4.0 * (double)h.n_group_rows * plan->C);
+    plan->bank_conflicts = h.positions ? (double)h.conflicts / (double)h.positions : 0.0;
     cudaStream_t s = g->stream;
     plan->warp_start.alloc(W);                plan->warp_start.upload(h.warp_start.data(), W, s);
-    plan->quad_of.alloc(h.quad_of.size());    plan->quad_of.upload(h.quad_of.data(), h.quad_of.size(), s);
+    plan->rows.alloc(h.rows.size());          plan->rows.upload(h.rows.data(), h.rows.size(), s);
     plan->ginfo.alloc(h.ginfo.size());        plan->ginfo.upload(h.ginfo.data(), h.ginfo.size(), s);
     plan->stream.alloc(h.stream.size());      plan->stream.upload(h.stream.data(), h.stream.size(), s);
     std::vector<float> wf(h.weights.begin(), h.weights.end());
@@ -159,12 +227,13 @@ static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, 
     return plan;
 }
 
-static std::shared_ptr<ResidentPlan> get_resident_plan(oscb_graph *g, int RT, int W, int T)
+static std::shared_ptr<ResidentPlan> get_resident_plan(oscb_graph *g, int RT, int W, int T, int pair_bytes, bool keep_order)
 {
-    const uint64_t key = ((uint64_t)RT << 40) | ((uint64_t)W << 20) | (uint64_t)T;
+    const uint64_t key = ((uint64_t)RT << 40) | ((uint64_t)W << 20) | ((uint64_t)T << 8) | ((uint64_t)pair_bytes << 1) |
+                         (keep_order ? 1u : 0u);
     auto it = g->plans.find(key);
     if (it != g->plans.end()) return it->second;
-    auto plan = build_resident_plan(g, RT, W, T);
+    auto plan = build_resident_plan(g, RT, W, T, pair_bytes, keep_order);
     g->plans[key] = plan;
     return plan;
 }
@@ -180,16 +249,15 @@ static size_t resident_smem_bytes(const oscb_graph *g, int precision, int n_stat
                                   int n_group_rows, bool idx_smem)
 {
     const size_t pair = precision == OSCB_PREC_F64 ? 16 : 8;
-    const int SB = state_bits_for(n_states);
-    return ResidentSmem::make((int)g->n, RT, 32 / RT, T, W, words_per_row(RT, SB), pair, pair / 2, n_group_rows,
-                              idx_smem, !g->unit_weights).total;
+    (void)n_states;
+    return ResidentSmem::make((int)g->n, RT, 32 / RT, T, W, pair, pair / 2, n_group_rows, idx_smem, !g->unit_weights).total;
 }
 
 // tile width: the candidate with the lowest estimated time
 static bool choose_resident_config(const oscb_graph *g, int precision, int n_states, int64_t R, int requested_rt,
                                    ResidentConfig *out)
 {
-    if (g->n > 65534 || g->max_degree > 1020 || n_states > 255) return false;
+    if (g->n > 60000 || g->max_degree > 1020 || n_states > 254) return false;
     static const double eff[6] = {0.35, 0.5, 0.7, 0.85, 1.0, 1.0}; // gather efficiency by log2(RT)
     const int max_threads = max_threads_for(precision);
     double best_cost = std::numeric_limits<double>::infinity();
@@ -200,6 +268,7 @@ static bool choose_resident_config(const oscb_graph *g, int precision, int n_sta
         if (requested_rt <= 0 && RT > 1 && RT / 2 >= R) continue; // do not pad a tile more than 2x
         int W, T;
         tile_shape(g->n, RT, max_threads, &W, &T);
+        if ((g->n + OSCB_PAD_ROWS) * RT > 65535) continue;
         const size_t need = resident_smem_bytes(g, precision, n_states, RT, W, T, 0, false);
         if (need > (size_t)g->smem_optin) continue;
         const int64_t tiles = (R + RT - 1) / RT;
@@ -253,9 +322,8 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
 {
     cudaStream_t s = g->stream;
     const int n = (int)g->n, R = (int)R64;
-    auto plan = get_resident_plan(g, cfg.RT, cfg.W, cfg.T);
+    auto plan = get_resident_plan(g, cfg.RT, cfg.W, cfg.T, (int)(2 * sizeof(T)), STRICT);
     const int RT = plan->RT, tiles = (R + RT - 1) / RT, R_pad = tiles * RT;
-    const int SB = state_bits_for(p->n_states), wpr = words_per_row(RT, SB);
     bool idx_smem = true;
     size_t smem = resident_smem_bytes(g, p->precision, p->n_states, RT, plan->W, plan->T, plan->n_group_rows, true);
     if (smem > (size_t)g->smem_optin) {
@@ -297,8 +365,8 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     ResidentArgs a;
     memset(&a, 0, sizeof(a));
     a.n = n; a.R_real = R; a.RT = RT; a.log2RT = plan->log2RT; a.C = plan->C; a.T = plan->T; a.W = plan->W;
-    a.SB = SB; a.wpr = wpr; a.n_group_rows = plan->n_group_rows;
-    a.warp_start = plan->warp_start.p; a.quad_of = plan->quad_of.p; a.ginfo = plan->ginfo.p; a.stream = plan->stream.p;
+    a.n_group_rows = plan->n_group_rows;
+    a.warp_start = plan->warp_start.p; a.rows = plan->rows.p; a.ginfo = plan->ginfo.p; a.stream = plan->stream.p;
     a.wstream = plan->weighted ? (sizeof(T) == 8 ? (const void *)plan->w64.p : (const void *)plan->w32.p) : nullptr;
     a.phi = d_phi.p; a.seeds = d_seeds.p;
     a.step_begin = p->first_step; a.step_end = p->first_step + steps; a.noise_step0 = p->first_step;
