@@ -86,7 +86,7 @@ typedef struct oscb_run_params {
     double target_objective;
     int64_t first_step;                         /* global index of the first step (restart)   */
     int32_t replicas_per_cta;                   /* 0 auto; resident kernel tile width         */
-    int32_t reserved;
+    int32_t variant;                            /* 0 auto; 1 = generic resident kernel even where the specialised float32 one applies */
 } oscb_run_params;
 
 typedef struct oscb_run_outputs {
@@ -143,6 +143,11 @@ int oscb_run(oscb_graph *g, const oscb_run_params *params, const uint64_t *seeds
              const double *phi0 /* [R, n] or NULL => Philox initial phases */,
              const double *noise /* [steps, R, n] when noise_mode == OSCB_NOISE_HOST */,
              oscb_run_outputs *out);
+
+/* Device self-test behind the N = 2 scoring shortcut of the float32 kernel: counts the float32
+ * phases in [0, 1) (all 2^30-ish of them) whose sign-of-cosine state differs from the reference
+ * threshold (dynamics.py:203-213).  Must return 0 mismatches. */
+int oscb_selftest_sign_state(int device, uint64_t *mismatches);
 
 /* Host-only: the graph compiler of the persistent kernel (no GPU needed).  Turns a canonical CSR
  * (model.py:135-149) into the sliced-ELL neighbour stream for tiles of `replicas_per_cta`

@@ -23,8 +23,8 @@ OK, EINVAL, ECUDA, ENONFINITE, ENOMEM = 0, 1, 2, 3, 4
 OBJ = {"maxcut": 0, "coloring": 1}
 PREC = {"f32": 32, "f64": 64}
 NOISE_DEVICE, NOISE_HOST, NOISE_NONE = 0, 1, 2
-KERNEL = {"auto": 0, "stream": 1, "resident": 2}
-KERNEL_NAME = {v: k for k, v in KERNEL.items()}
+KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2}
+KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident"}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC"]
@@ -43,7 +43,7 @@ class RunParams(C.Structure):
                 ("noise_mode", C.c_int32), ("kernel", C.c_int32), ("use_target", C.c_int32),
                 ("steps", C.c_int64), ("cadence", C.c_int64), ("trace_stride", C.c_double),
                 ("target_objective", C.c_double), ("first_step", C.c_int64),
-                ("replicas_per_cta", C.c_int32), ("reserved", C.c_int32)]
+                ("replicas_per_cta", C.c_int32), ("variant", C.c_int32)]
 
 
 class RunOutputs(C.Structure):
@@ -71,6 +71,7 @@ SYMBOLS = {
                             C.c_int32, C.c_int32, _P, _P]),
     "oscb_score": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P]),
     "oscb_energy": (C.c_int, [_P, C.c_int64, _P, _P]),
+    "oscb_selftest_sign_state": (C.c_int, [C.c_int, C.POINTER(C.c_uint64)]),
     "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int64), _P, _P, _P, _P]),

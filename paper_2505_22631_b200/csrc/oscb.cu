@@ -657,6 +657,29 @@ int oscb_energy(oscb_graph *g, int64_t R, const double *phi, double *energy)
     });
 }
 
+int oscb_selftest_sign_state(int device, uint64_t *mismatches)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(mismatches != nullptr, "NULL argument");
+        int count = 0;
+        cudaError_t e = cudaGetDeviceCount(&count);
+        if (e != cudaSuccess || count == 0) {
+            set_error("no usable CUDA device (%s); liboscb has no CPU fallback", cudaGetErrorString(e));
+            return OSCB_ECUDA;
+        }
+        OSCB_REQUIRE(device >= 0 && device < count, "device %d out of range (have %d)", device, count);
+        OSCB_CUDA(cudaSetDevice(device));
+        DevBuf<unsigned long long> d(1);
+        OSCB_CUDA(cudaMemset(d.p, 0, sizeof(unsigned long long)));
+        k_selftest_sign_state<<<148 * 8, 256>>>(d.p);
+        check_launch("oscb_selftest_sign_state");
+        unsigned long long h = 0;
+        OSCB_CUDA(cudaMemcpy(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost));
+        *mismatches = h;
+        return OSCB_OK;
+    });
+}
+
 int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t replicas_per_cta,
                             int32_t max_threads, int32_t pair_bytes, int32_t keep_order, int32_t *warps,
                             int32_t *rounds, int64_t *group_rows, int64_t *bank_conflicts, int32_t *warp_start,

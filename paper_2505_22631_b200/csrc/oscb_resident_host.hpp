@@ -4,11 +4,13 @@
 #pragma once
 #include "oscb_host.hpp"
 #include "oscb_resident.cuh"
+#include "oscb_resident_fast.cuh"
 
 #include <algorithm>
 #include <cmath>
 #include <limits>
 #include <numeric>
+#include <type_traits>
 
 namespace oscb {
 
@@ -19,7 +21,7 @@ struct ResidentPlan {
     double fill = 1.0;          // real neighbours / stream entries
     double bank_conflicts = 0;  // stream positions whose slots collide on a bank class / all positions
     DevBuf<int> warp_start;
-    DevBuf<uint16_t> rows;
+    DevBuf<uint16_t> rows, deg;
     DevBuf<uint32_t> ginfo;
     DevBuf<uint2> stream;
     DevBuf<float> w32;
@@ -43,6 +45,7 @@ static void tile_shape(int64_t n, int RT, int max_threads, int *W, int *T)
 struct ResidentStreamHost {
     std::vector<int> warp_start;
     std::vector<uint16_t> rows;     // [W*T*4*C] own row * RT, n*RT when the slot has none
+    std::vector<uint16_t> deg;      // [W*T*4*C] real degree of that row
     std::vector<uint32_t> ginfo;    // [W*T]
     std::vector<uint2> stream;      // [(n_group_rows + 1) * C] ids * RT; >= n*RT: zero padding rows
     std::vector<double> weights;    // [(n_group_rows + 1) * C * 4]
@@ -82,6 +85,7 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
 
     out->warp_start.assign(W, 0);
     out->rows.assign((size_t)W * T * 4 * C, (uint16_t)(n * RT));
+    out->deg.assign((size_t)W * T * 4 * C, 0);
     out->ginfo.assign((size_t)W * T, 0);
     out->stream.clear();
     out->weights.clear();
@@ -113,7 +117,11 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
                 std::vector<std::vector<Item>> laid(C, std::vector<Item>(P, Item{-1, 0.0}));
                 for (int c = 0; c < C; ++c) {
                     const int i = rows[c][kk];
-                    if (i >= 0) out->rows[(((size_t)w * T + t) * 4 + kk) * C + c] = (uint16_t)(i * RT);
+                    const size_t at = (((size_t)w * T + t) * 4 + kk) * C + c;
+                    if (i >= 0) {
+                        out->rows[at] = (uint16_t)(i * RT);
+                        out->deg[at] = (uint16_t)deg(i);
+                    }
                 }
                 for (int c0 = 0; c0 < C; c0 += H) {
                     // remaining items of each slot of this wavefront group, bucketed by bank class
@@ -216,6 +224,7 @@ static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, 
     cudaStream_t s = g->stream;
     plan->warp_start.alloc(W);                plan->warp_start.upload(h.warp_start.data(), W, s);
     plan->rows.alloc(h.rows.size());          plan->rows.upload(h.rows.data(), h.rows.size(), s);
+    plan->deg.alloc(h.deg.size());            plan->deg.upload(h.deg.data(), h.deg.size(), s);
     plan->ginfo.alloc(h.ginfo.size());        plan->ginfo.upload(h.ginfo.data(), h.ginfo.size(), s);
     plan->stream.alloc(h.stream.size());      plan->stream.upload(h.stream.data(), h.stream.size(), s);
     std::vector<float> wf(h.weights.begin(), h.weights.end());
@@ -315,7 +324,70 @@ static void launch_resident(oscb_graph *g, const ResidentArgs &args, int tiles, 
     }
 }
 
-template <typename T, int MAXT, bool STRICT>
+// smem plan of the float32 production kernel: phases first, then the stream
+struct FastFit {
+    bool phi_smem = false, idx_smem = false, piggy = false, states = false;
+    FastSmem lay;
+    size_t smem = 0;
+};
+static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT, int W, int T, int n_group_rows)
+{
+    const bool weighted = !g->unit_weights;
+    FastFit f;
+    f.states = n_states != 2;
+    f.piggy = n_states == 2 && !weighted && objective == OSCB_OBJ_MAXCUT;
+    auto lay = [&](bool phi, bool idx) {
+        return FastSmem::make((int)g->n, RT, 32 / RT, T, W, n_group_rows, f.states, f.piggy, phi, idx, weighted);
+    };
+    const size_t cap = (size_t)g->smem_optin;
+    if (lay(false, false).total > cap && f.piggy) f.piggy = false;   // drop the degree table before giving up
+    if (lay(true, false).total <= cap) f.phi_smem = true;
+    if (lay(f.phi_smem, true).total <= cap) f.idx_smem = true;
+    f.lay = lay(f.phi_smem, f.idx_smem);
+    f.smem = f.lay.total;
+    return f;
+}
+
+static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const ResidentPlan &plan, int n_states,
+                                 const FastFit &f, int tiles)
+{
+    FastArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = ra.n; a.RT = ra.RT; a.LRT = ra.log2RT; a.nRT = ra.n * ra.RT; a.C = ra.C; a.W = ra.W; a.n_rows = 4 * ra.T;
+    a.R_real = ra.R_real; a.n_group_rows = ra.n_group_rows; a.piggy = f.piggy ? 1 : 0;
+    a.off_cs = (uint32_t)f.lay.cs; a.off_phi = (uint32_t)f.lay.phi; a.off_st = (uint32_t)f.lay.st;
+    a.off_rows = (uint32_t)f.lay.rows; a.off_g = (uint32_t)f.lay.g; a.off_deg = (uint32_t)f.lay.deg;
+    a.off_part = (uint32_t)f.lay.part; a.off_misc = (uint32_t)f.lay.misc; a.off_stream = (uint32_t)f.lay.stream;
+    a.off_w = (uint32_t)f.lay.wstream; a.smem_total = (uint32_t)f.lay.total;
+    a.hK = (float)(ra.h * ra.K); a.knsh = (float)ra.kn_sqrt_h;
+    a.h = ra.h; a.ks_max = ra.ks_max; a.ks_period = ra.ks_period; a.ks_scale = ra.h * (n_states == 2 ? 2.0 : 1.0);
+    a.tc = ra.tc;
+    a.noise_on = ra.noise_mode == OSCB_NOISE_DEVICE; a.maximize = ra.maximize; a.use_target = ra.use_target;
+    a.initial_sample = ra.initial_sample; a.n_sample_steps = ra.n_sample_steps; a.sample_offset = ra.sample_offset;
+    a.step_begin = ra.step_begin; a.step_end = ra.step_end; a.cadence = ra.cadence; a.trace_stride = ra.trace_stride;
+    a.target = ra.target;
+    a.warp_start = ra.warp_start; a.rows = ra.rows; a.ginfo = ra.ginfo; a.deg = plan.deg.p; a.stream = ra.stream;
+    a.wstream = reinterpret_cast<const float *>(ra.wstream);
+    a.phi = reinterpret_cast<float *>(ra.phi); a.seeds = ra.seeds; a.sample_steps = ra.sample_steps;
+    a.best_obj = ra.best_obj; a.energy = ra.energy; a.best_trace = ra.best_trace; a.best_states = ra.best_states;
+    a.first_hit = ra.first_hit; a.nonfinite = ra.nonfinite;
+    auto go = [&](auto kernel) {
+        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem));
+        kernel<<<tiles, plan.W * 32, f.smem, g->stream>>>(a);
+    };
+    auto by_mem = [&](auto nm, auto wt) {
+        constexpr int NM = decltype(nm)::value;
+        constexpr bool WT = decltype(wt)::value;
+        if (f.idx_smem) { if (f.phi_smem) go(k_resident_fast<NM, WT, true, true>); else go(k_resident_fast<NM, WT, true, false>); }
+        else            { if (f.phi_smem) go(k_resident_fast<NM, WT, false, true>); else go(k_resident_fast<NM, WT, false, false>); }
+    };
+    using two = std::integral_constant<int, 2>;
+    using any = std::integral_constant<int, 0>;
+    if (n_states == 2) { if (plan.weighted) by_mem(two{}, std::true_type{}); else by_mem(two{}, std::false_type{}); }
+    else               { if (plan.weighted) by_mem(any{}, std::true_type{}); else by_mem(any{}, std::false_type{}); }
+}
+
+template <typename T, int MAXT, bool STRICT, bool FAST>
 static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const ResidentConfig &cfg, int64_t steps,
                               int64_t cadence, const std::vector<long long> &sample_steps, const uint64_t *seeds,
                               int64_t R64, const double *phi0, const double *noise, oscb_run_outputs *out)
@@ -329,6 +401,11 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     if (smem > (size_t)g->smem_optin) {
         idx_smem = false;
         smem = resident_smem_bytes(g, p->precision, p->n_states, RT, plan->W, plan->T, plan->n_group_rows, false);
+    }
+    FastFit fast;
+    if (FAST) {
+        fast = fit_fast(g, p->n_states, p->objective, RT, plan->W, plan->T, plan->n_group_rows);
+        smem = fast.smem;
     }
     OSCB_REQUIRE(smem <= (size_t)g->smem_optin, "resident kernel does not fit in shared memory (%zu bytes)", smem);
     const int maximize = p->objective == OSCB_OBJ_MAXCUT;
@@ -386,7 +463,8 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     OSCB_CUDA(cudaEventCreate(&ev0));
     OSCB_CUDA(cudaEventCreate(&ev1));
     OSCB_CUDA(cudaEventRecord(ev0, s));
-    launch_resident<T, MAXT, STRICT>(g, a, tiles, plan->W * 32, smem, idx_smem, plan->weighted);
+    if (FAST) launch_resident_fast(g, a, *plan, p->n_states, fast, tiles);
+    else launch_resident<T, MAXT, STRICT>(g, a, tiles, plan->W * 32, smem, idx_smem, plan->weighted);
     OSCB_CUDA(cudaEventRecord(ev1, s));
     {
         cudaError_t e = cudaGetLastError();
@@ -442,9 +520,11 @@ static void run_resident(oscb_graph *g, const oscb_run_params *p, int64_t steps,
                  "the resident kernel cannot hold this problem (n = %lld, max degree %lld); use the streaming kernel",
                  (long long)g->n, (long long)g->max_degree);
     if (p->precision == OSCB_PREC_F64)
-        run_resident_impl<double, 512, true>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
+        run_resident_impl<double, 512, true, false>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
+    else if (p->noise_mode == OSCB_NOISE_HOST || p->variant == 1)   // injected noise / variant 1: the generic kernel
+        run_resident_impl<float, 1024, false, false>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
     else
-        run_resident_impl<float, 1024, false>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
+        run_resident_impl<float, 1024, false, true>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
 }
 
 } // namespace oscb

@@ -425,6 +425,7 @@ def run_batch(J: CouplingMatrix, params: SolverParams, objective: str, seeds: Se
     if kernel not in nat.KERNEL:
         raise ValueError(f"kernel must be one of {sorted(nat.KERNEL)}")
     p.kernel = nat.KERNEL[kernel]
+    p.variant = 1 if kernel == "resident-generic" else 0
     p.use_target = int(target is not None)
     p.target_objective = 0.0 if target is None else float(target)
     p.steps = nsteps if steps is not None else 0
