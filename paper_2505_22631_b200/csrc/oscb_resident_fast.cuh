@@ -86,6 +86,7 @@ struct FastArgs {
     int n, nRT, RT, LRT, C, W, n_rows /* 4 * rounds */, R_real;
     int n_group_rows;
     int piggy;                         // N = 2, unit weights, max-cut: score during the next gather
+    int deg_smem;                      // the degree table of the piggyback is staged in shared memory
     uint32_t off_cs, off_phi, off_st, off_rows, off_g, off_deg, off_part, off_misc, off_stream, off_w, smem_total;
     float hK, knsh;
     double h, ks_max, ks_period, ks_scale /* h (x2 for N = 2) */;
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     const uint32_t st32 = smem32 + a.off_st + r;
     const uint32_t rows32 = smem32 + a.off_rows + ((warp * a.n_rows) * a.C + c) * 2;   // own rows, stride C*2
     const uint32_t g32 = smem32 + a.off_g + warp * a.n_rows;                           // G per row position
-    const uint32_t deg32 = smem32 + a.off_deg + ((warp * a.n_rows) * a.C + c) * 2;
+    const uint16_t *deg_lane = (a.deg_smem ? reinterpret_cast<const uint16_t *>(smem_raw + a.off_deg) : a.deg) + (warp * a.n_rows) * a.C + c;
     double *part = reinterpret_cast<double *>(smem_raw + a.off_part);
     double *best_s = reinterpret_cast<double *>(smem_raw + a.off_misc);
     int *improved_s = reinterpret_cast<int *>(smem_raw + a.off_misc + a.RT * 8);
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         const int total_rows = a.W * a.n_rows;
         for (int q = tid; q < total_rows * a.C; q += NT) {
             rows[q] = a.rows[q];
-            if (a.piggy) degs[q] = a.deg[q];
+            if (a.deg_smem) degs[q] = a.deg[q];
         }
         for (int q = tid; q < total_rows; q += NT) gs[q] = (uint8_t)((a.ginfo[q >> 2] >> (8 * (q & 3))) & 0xFFu);
         if (IDX_SMEM) {
@@ -374,14 +375,30 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         int twice_cut = 0;
 
         // pass A ------------------------------------------------------------------------------
-        int g = 0;
-        uint2 pk = group_at(0);
+        // The stream of a warp is contiguous: a running pointer walks it and the next group is
+        // always loaded one group ahead of its use (the pad row covers the last one).
+        uint32_t sp32 = stream32, wp32 = w32;
+        const uint2 *spg = stream_g;
+        const float *wpg = w_g;
+        auto next_group = [&]() -> uint2 {
+            if (IDX_SMEM) { sp32 += (uint32_t)a.C * 8; return lds_u64(sp32); }
+            spg += a.C;
+            return *spg;
+        };
+        auto next_weights = [&]() -> float4 {       // weights of the group consumed now, then advance
+            float4 w4;
+            if (IDX_SMEM) { w4 = lds_f4(wp32); wp32 += (uint32_t)a.C * 16; }
+            else { w4 = *reinterpret_cast<const float4 *>(wpg); wpg += a.C * 4; }
+            return w4;
+        };
+        uint2 pk = IDX_SMEM ? lds_u64(sp32) : *spg;
         float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
 #pragma unroll 1
         for (int row = 0; row < a.n_rows; ++row) {
             const uint32_t iRT = row_at(row);
             const int G = (int)lds_u8(g32 + row);
             const bool valid = iRT < (uint32_t)a.nRT;
+            const float p = load_phi(iRT);              // issued a whole gather ahead of its use
             if ((row & 3) == 0 && a.noise_on && valid)
                 normals4_fast(philox4x32_10(make_uint4((iRT >> a.LRT) >> 2, (uint32_t)step, (uint32_t)(step >> 32), 0x6F736362u), key),
                               z0, z1, z2, z3);
@@ -391,8 +408,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                 // scoring step: the sign bit of every gathered cosine is the neighbour's lattice state
 #pragma unroll 2
                 for (int gg = 0; gg < G; ++gg) {
-                    ++g;
-                    const uint2 nx = group_at(g);
+                    const uint2 nx = next_group();
                     const float2 v0 = pair_at(pk.x & 0xffffu), v1 = pair_at(pk.x >> 16);
                     const float2 v2 = pair_at(pk.y & 0xffffu), v3 = pair_at(pk.y >> 16);
                     sum = __fadd2_rn(sum, __fadd2_rn(__fadd2_rn(v0, v1), __fadd2_rn(v2, v3)));
@@ -403,12 +419,11 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             } else {
 #pragma unroll 2
                 for (int gg = 0; gg < G; ++gg) {
-                    ++g;
-                    const uint2 nx = group_at(g);
+                    const uint2 nx = next_group();
                     const float2 v0 = pair_at(pk.x & 0xffffu), v1 = pair_at(pk.x >> 16);
                     const float2 v2 = pair_at(pk.y & 0xffffu), v3 = pair_at(pk.y >> 16);
                     if (WEIGHTED) {
-                        const float4 w4 = weights_at(g - 1);
+                        const float4 w4 = next_weights();
                         sum = __ffma2_rn(make_float2(w4.x, w4.x), v0, sum);
                         sum = __ffma2_rn(make_float2(w4.y, w4.y), v1, sum);
                         sum = __ffma2_rn(make_float2(w4.z, w4.z), v2, sum);
@@ -423,8 +438,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                 const float2 own = pair_at(iRT);
                 const float ci = own.x, si = own.y;
                 if (NMODE == 2 && !WEIGHTED && count_now)   // differing neighbours: deg - neg if the row itself is in state 1
-                    twice_cut += (ci < 0.f) ? (int)lds_u16(deg32 + (uint32_t)(row * a.C) * 2) - neg : neg;
-                const float p = load_phi(iRT);
+                    twice_cut += (ci < 0.f) ? (int)deg_lane[row * a.C] - neg : neg;
                 const float acc = si * sum.x - ci * sum.y;
                 float shil;
                 if (NMODE == 2) shil = si * ci;                                  // hks holds 2 h ks

@@ -7,6 +7,7 @@
 #include "oscb_resident_fast.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <limits>
 #include <numeric>
@@ -326,7 +327,7 @@ static void launch_resident(oscb_graph *g, const ResidentArgs &args, int tiles, 
 
 // smem plan of the float32 production kernel: phases first, then the stream
 struct FastFit {
-    bool phi_smem = false, idx_smem = false, piggy = false, states = false;
+    bool phi_smem = false, idx_smem = false, piggy = false, deg_smem = false, states = false;
     FastSmem lay;
     size_t smem = 0;
 };
@@ -337,12 +338,26 @@ static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT
     f.states = n_states != 2;
     f.piggy = n_states == 2 && !weighted && objective == OSCB_OBJ_MAXCUT;
     auto lay = [&](bool phi, bool idx) {
-        return FastSmem::make((int)g->n, RT, 32 / RT, T, W, n_group_rows, f.states, f.piggy, phi, idx, weighted);
+        return FastSmem::make((int)g->n, RT, 32 / RT, T, W, n_group_rows, f.states, f.deg_smem, phi, idx, weighted);
     };
     const size_t cap = (size_t)g->smem_optin;
-    if (lay(false, false).total > cap && f.piggy) f.piggy = false;   // drop the degree table before giving up
-    if (lay(true, false).total <= cap) f.phi_smem = true;
-    if (lay(f.phi_smem, true).total <= cap) f.idx_smem = true;
+    // The neighbour stream is on the critical path of every gather (a phase is touched three
+    // times per row and its load can be issued a whole row early), so the stream gets the
+    // shared memory first; OSCB_FAST_PREFER=phi reverses the order (experiments).  The degree
+    // table is read on scoring steps only and goes to shared memory last.
+    const char *pref = getenv("OSCB_FAST_PREFER");
+    const bool phi_first = pref && pref[0] == 'p';
+    if (phi_first) {
+        if (lay(true, false).total <= cap) f.phi_smem = true;
+        if (lay(f.phi_smem, true).total <= cap) f.idx_smem = true;
+    } else {
+        if (lay(false, true).total <= cap) f.idx_smem = true;
+        if (lay(true, f.idx_smem).total <= cap) f.phi_smem = true;
+    }
+    if (f.piggy) {
+        f.deg_smem = true;
+        if (lay(f.phi_smem, f.idx_smem).total > cap) f.deg_smem = false;
+    }
     f.lay = lay(f.phi_smem, f.idx_smem);
     f.smem = f.lay.total;
     return f;
@@ -354,7 +369,7 @@ static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const Re
     FastArgs a;
     memset(&a, 0, sizeof(a));
     a.n = ra.n; a.RT = ra.RT; a.LRT = ra.log2RT; a.nRT = ra.n * ra.RT; a.C = ra.C; a.W = ra.W; a.n_rows = 4 * ra.T;
-    a.R_real = ra.R_real; a.n_group_rows = ra.n_group_rows; a.piggy = f.piggy ? 1 : 0;
+    a.R_real = ra.R_real; a.n_group_rows = ra.n_group_rows; a.piggy = f.piggy ? 1 : 0; a.deg_smem = f.deg_smem ? 1 : 0;
     a.off_cs = (uint32_t)f.lay.cs; a.off_phi = (uint32_t)f.lay.phi; a.off_st = (uint32_t)f.lay.st;
     a.off_rows = (uint32_t)f.lay.rows; a.off_g = (uint32_t)f.lay.g; a.off_deg = (uint32_t)f.lay.deg;
     a.off_part = (uint32_t)f.lay.part; a.off_misc = (uint32_t)f.lay.misc; a.off_stream = (uint32_t)f.lay.stream;
@@ -412,7 +427,7 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     const int64_t S = 1 + (int64_t)sample_steps.size();
     const size_t tot = (size_t)n * R, tot_pad = (size_t)n * R_pad;
 
-    DevBuf<T> d_phi(tot_pad);
+    DevBuf<T> d_phi(tot_pad + 64);   // + one padding row: invalid rows load (never store) row n
     DevBuf<double> d_io(tot);
     std::vector<uint64_t> h_seeds(R_pad, 0);
     std::copy(seeds, seeds + R, h_seeds.begin());
