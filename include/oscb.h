@@ -154,10 +154,11 @@ int oscb_selftest_sign_state(int device, uint64_t *mismatches);
  * replicas, CTAs of at most `max_threads` threads and (cos, sin) pairs of `pair_bytes` bytes.
  * keep_order != 0 keeps every row in CSR order (float64 parity mode).  Call once with
  * ids == NULL for the sizes, then with buffers: warp_start [warps], rows [warps*rounds*4*C],
- * ginfo [warps*rounds], ids [4*(group_rows+1)*C] with C = 32/replicas_per_cta.  Row and
+ * ginfo [warps*rounds], ids [4*(group_rows+1)*C] with C = 32/(replicas_per_cta/replicas_per_lane)
+ * slots per warp (a lane of the float32 kernel may own 2 adjacent replicas).  Row and
  * neighbour ids are pre-multiplied by replicas_per_cta; values >= n*replicas_per_cta are padding. */
 int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices,
-                            int32_t replicas_per_cta, int32_t max_threads, int32_t pair_bytes,
+                            int32_t replicas_per_cta, int32_t replicas_per_lane, int32_t max_threads, int32_t pair_bytes,
                             int32_t keep_order, int32_t *warps, int32_t *rounds, int64_t *group_rows,
                             int64_t *bank_conflicts, int32_t *warp_start, uint16_t *rows,
                             uint32_t *ginfo, uint16_t *ids);

@@ -72,7 +72,7 @@ SYMBOLS = {
     "oscb_score": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P]),
     "oscb_energy": (C.c_int, [_P, C.c_int64, _P, _P]),
     "oscb_selftest_sign_state": (C.c_int, [C.c_int, C.POINTER(C.c_uint64)]),
-    "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+    "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int64), _P, _P, _P, _P]),
     "oscb_run": (C.c_int, [_P, C.POINTER(RunParams), _P, C.c_int64, _P, _P, C.POINTER(RunOutputs)]),

@@ -681,7 +681,7 @@ int oscb_selftest_sign_state(int device, uint64_t *mismatches)
 }
 
 int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, int32_t replicas_per_cta,
-                            int32_t max_threads, int32_t pair_bytes, int32_t keep_order, int32_t *warps,
+                            int32_t replicas_per_lane, int32_t max_threads, int32_t pair_bytes, int32_t keep_order, int32_t *warps,
                             int32_t *rounds, int64_t *group_rows, int64_t *bank_conflicts, int32_t *warp_start,
                             uint16_t *rows, uint32_t *ginfo, uint16_t *ids)
 {
@@ -690,15 +690,17 @@ int oscb_resident_plan_host(int64_t n, const int64_t *indptr, const int64_t *ind
         const int RT = replicas_per_cta;
         OSCB_REQUIRE(RT >= 1 && RT <= 32 && (RT & (RT - 1)) == 0, "replicas_per_cta must be a power of two <= 32");
         OSCB_REQUIRE(max_threads >= 32 && max_threads <= 1024 && max_threads % 32 == 0, "bad max_threads");
+        OSCB_REQUIRE((replicas_per_lane == 1 || replicas_per_lane == 2) && replicas_per_lane <= RT, "replicas_per_lane must be 1 or 2 (<= replicas_per_cta)");
+        const int LPS = RT / replicas_per_lane;
         OSCB_REQUIRE(pair_bytes == 8 || pair_bytes == 16, "pair_bytes must be 8 or 16");
         const int64_t nnz = indptr[n];
         std::vector<int> ip(n + 1), ix(nnz);
         for (int64_t i = 0; i <= n; ++i) ip[i] = (int)indptr[i];
         for (int64_t e = 0; e < nnz; ++e) ix[e] = (int)indices[e];
         int W, T;
-        tile_shape(n, RT, max_threads, &W, &T);
+        tile_shape(n, LPS, max_threads, &W, &T);
         ResidentStreamHost h;
-        compile_resident_stream((int)n, ip.data(), ix.data(), nullptr, RT, W, T, pair_bytes, keep_order != 0, &h);
+        compile_resident_stream((int)n, ip.data(), ix.data(), nullptr, RT, LPS, W, T, pair_bytes, keep_order != 0, &h);
         *warps = W;
         *rounds = T;
         *group_rows = h.n_group_rows;

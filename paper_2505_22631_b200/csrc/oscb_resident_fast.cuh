@@ -17,6 +17,9 @@
 //     state; the tile sum is twice the cut.  Trace samples and the first/last state still go
 //     through the explicit scoring pass;
 //   * other N (NMODE == 0): lattice states as bytes in shared memory, explicit scoring pass;
+//   * RPL replicas per lane (1 or 2): with RPL = 2 a lane owns two adjacent replicas, so one
+//     LDS.128 fetches both (cos, sin) pairs of a neighbour and the index unpacking / address
+//     arithmetic of a gather is shared by two updates;
 //   * Box-Muller on the MUFU unit (lg2 / sin / cos / sqrt approximations, |err| ~ 1e-6 on a
 //     unit normal), noise off is a uniform branch.
 //
@@ -83,7 +86,7 @@ __device__ __forceinline__ void normals4_fast(uint4 x, float &z0, float &z1, flo
 // Everything the kernel needs, precomputed on the host so that the hot loops read constants
 // straight from the parameter bank instead of re-deriving them under register pressure.
 struct FastArgs {
-    int n, nRT, RT, LRT, C, W, n_rows /* 4 * rounds */, R_real;
+    int n, nRT, RT, LRT, LPS, LLPS /* lanes per slot = RT / RPL and its log2 */, C, W, n_rows /* 4 * rounds */, R_real;
     int n_group_rows;
     int piggy;                         // N = 2, unit weights, max-cut: score during the next gather
     int deg_smem;                      // the degree table of the piggyback is staged in shared memory
@@ -100,7 +103,7 @@ struct FastArgs {
     const uint16_t *deg;               // [W * n_rows * C]
     const uint2 *stream;               // [(n_group_rows + 1) * C]
     const float *wstream;              // [(n_group_rows + 1) * C * 4]
-    float *phi;                        // [tiles][n][RT]
+    float *phi;                        // [tiles][n][RT] (+ one padding row at the very end)
     const uint64_t *seeds;
     const long long *sample_steps;
     double *best_obj, *energy, *best_trace;
@@ -109,7 +112,6 @@ struct FastArgs {
     unsigned long long *nonfinite;
 };
 
-// shared-memory layout of the float32 kernel; filled into FastArgs by the host
 // Self-test of the N = 2 scoring shortcut: for EVERY float32 phase p in [0, 1) the sign bit of
 // cospi(2p) + 0 (what pass B stores) must equal the reference threshold of p (dynamics.py:203-213).
 __global__ void k_selftest_sign_state(unsigned long long *mismatches)
@@ -127,6 +129,7 @@ __global__ void k_selftest_sign_state(unsigned long long *mismatches)
     if (bad) atomicAdd(mismatches, bad);
 }
 
+// shared-memory layout of the float32 kernel; filled into FastArgs by the host
 struct FastSmem {
     size_t cs, phi, st, rows, g, deg, part, misc, stream, wstream, total;
     __host__ static FastSmem make(int n, int RT, int C, int T, int W, int n_group_rows, bool need_states, bool need_deg,
@@ -136,7 +139,7 @@ struct FastSmem {
         size_t o = 0;
         auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~(size_t)15; return at; };
         s.cs = take((size_t)(n + OSCB_PAD_ROWS) * RT * 8);
-        s.phi = take(phi_smem ? (size_t)n * RT * 4 : 0);
+        s.phi = take(phi_smem ? (size_t)(n + 1) * RT * 4 : 0);
         s.st = take(need_states ? (size_t)(n + OSCB_PAD_ROWS) * RT : 0);
         s.rows = take((size_t)W * T * 4 * C * 2);
         s.g = take((size_t)W * T * 4);
@@ -166,25 +169,70 @@ __device__ __forceinline__ void sts_u8(uint32_t addr, uint32_t v)
 {
     asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+__device__ __forceinline__ float2 lds_f2(uint32_t addr)
+{
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+
+// (cos, sin) pairs of RPL adjacent replicas of one row: one LDS.64 or one LDS.128
+template <int RPL> struct PairPack;
+template <> struct PairPack<1> {
+    float2 v[1];
+    __device__ __forceinline__ void load(uint32_t addr) { v[0] = lds_f2(addr); }
+};
+template <> struct PairPack<2> {
+    float2 v[2];
+    __device__ __forceinline__ void load(uint32_t addr)
+    {
+        const float4 t = lds_f4(addr);
+        v[0] = make_float2(t.x, t.y);
+        v[1] = make_float2(t.z, t.w);
+    }
+};
+
+// Sum RPL per-lane values over all lanes of the CTA that hold the same replicas (same lane-in-slot
+// q), in a fixed order.  Replica q*RPL + e ends up in part2[...]; result for replica `tid` valid
+// in threads tid < RT.  Two barriers inside.
+template <int RPL>
+__device__ __forceinline__ double tile_reduce_rpl(const double (&v)[RPL], int RT, int LPS, double *part, int tid, int nwarps)
+{
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+        double x = v[e];
+        for (int off = 16; off >= LPS; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+        if (lane < LPS) part[warp * RT + lane * RPL + e] = x;
+    }
+    __syncthreads();
+    double tot = 0.0;
+    if (tid < RT)
+        for (int w = 0; w < nwarps; ++w) tot += part[w * RT + tid];
+    __syncthreads();
+    return tot;
+}
 
 // NMODE: 2 = two lattice states (state = sign of the cosine); 0 = any N, state bytes.
-template <int NMODE, bool WEIGHTED, bool IDX_SMEM, bool PHI_SMEM>
+// RPL:   replicas per lane.
+template <int NMODE, bool WEIGHTED, bool IDX_SMEM, bool PHI_SMEM, int RPL>
 __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool PIGGY = NMODE == 2 && !WEIGHTED;
     const int tid = threadIdx.x, NT = blockDim.x;
     const uint32_t smem32 = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const int lane = tid & 31, warp = tid >> 5;
-    const int r = lane & (a.RT - 1), c = lane >> a.LRT;
+    const int q = lane & (a.LPS - 1), c = lane >> a.LLPS;
+    const int r0 = q * RPL;                                 // first replica (inside the tile) of this lane
     const int tile = blockIdx.x;
-    const int rg = tile * a.RT + r;
-    const bool live = rg < a.R_real;
-    float *phi_g = a.phi + (size_t)tile * a.nRT + r;                        // the tile's slab (global), + row*RT
+    const int rg0 = tile * a.RT + r0;
+    float *phi_g = a.phi + (size_t)tile * a.nRT + r0;       // the tile's slab (global), + row*RT
 
     // lane-resident shared addresses (+ row*RT scaled by the element size)
-    const uint32_t cs32 = smem32 + a.off_cs + r * 8;
-    const uint32_t phi32 = smem32 + a.off_phi + r * 4;
-    const uint32_t st32 = smem32 + a.off_st + r;
+    const uint32_t cs32 = smem32 + a.off_cs + r0 * 8;
+    const uint32_t phi32 = smem32 + a.off_phi + r0 * 4;
+    const uint32_t st32 = smem32 + a.off_st + r0;
     const uint32_t rows32 = smem32 + a.off_rows + ((warp * a.n_rows) * a.C + c) * 2;   // own rows, stride C*2
     const uint32_t g32 = smem32 + a.off_g + warp * a.n_rows;                           // G per row position
     const uint16_t *deg_lane = (a.deg_smem ? reinterpret_cast<const uint16_t *>(smem_raw + a.off_deg) : a.deg) + (warp * a.n_rows) * a.C + c;
@@ -199,41 +247,48 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         uint8_t *gs = smem_raw + a.off_g;
         uint16_t *degs = reinterpret_cast<uint16_t *>(smem_raw + a.off_deg);
         const int total_rows = a.W * a.n_rows;
-        for (int q = tid; q < total_rows * a.C; q += NT) {
-            rows[q] = a.rows[q];
-            if (a.deg_smem) degs[q] = a.deg[q];
+        for (int i = tid; i < total_rows * a.C; i += NT) {
+            rows[i] = a.rows[i];
+            if (a.deg_smem) degs[i] = a.deg[i];
         }
-        for (int q = tid; q < total_rows; q += NT) gs[q] = (uint8_t)((a.ginfo[q >> 2] >> (8 * (q & 3))) & 0xFFu);
+        for (int i = tid; i < total_rows; i += NT) gs[i] = (uint8_t)((a.ginfo[i >> 2] >> (8 * (i & 3))) & 0xFFu);
         if (IDX_SMEM) {
             uint2 *dst = reinterpret_cast<uint2 *>(smem_raw + a.off_stream);
-            for (int q = tid; q < (a.n_group_rows + 1) * a.C; q += NT) dst[q] = a.stream[q];
+            for (int i = tid; i < (a.n_group_rows + 1) * a.C; i += NT) dst[i] = a.stream[i];
             if (WEIGHTED) {
                 float *wd = reinterpret_cast<float *>(smem_raw + a.off_w);
-                for (int q = tid; q < (a.n_group_rows + 1) * a.C * 4; q += NT) wd[q] = a.wstream[q];
+                for (int i = tid; i < (a.n_group_rows + 1) * a.C * 4; i += NT) wd[i] = a.wstream[i];
             }
         }
         float2 *cs = reinterpret_cast<float2 *>(smem_raw + a.off_cs);
         float *phis = reinterpret_cast<float *>(smem_raw + a.off_phi);
         const float *slab = a.phi + (size_t)tile * a.nRT;
-        for (int q = tid; q < a.nRT; q += NT) {
-            const float p = slab[q];
+        for (int i = tid; i < a.nRT; i += NT) {
+            const float p = slab[i];
             float s, co;
             sincospif(2.0f * p, &s, &co);
-            cs[q] = make_float2(co + 0.0f, s);
-            if (PHI_SMEM) phis[q] = p;
+            cs[i] = make_float2(co + 0.0f, s);
+            if (PHI_SMEM) phis[i] = p;
         }
-        for (int q = tid; q < OSCB_PAD_ROWS * a.RT; q += NT) {
-            cs[a.nRT + q] = make_float2(0.0f, 0.0f);
-            if (NMODE != 2) (smem_raw + a.off_st)[a.nRT + q] = 255;
+        for (int i = tid; i < OSCB_PAD_ROWS * a.RT; i += NT) {
+            cs[a.nRT + i] = make_float2(0.0f, 0.0f);
+            if (NMODE != 2) (smem_raw + a.off_st)[a.nRT + i] = 255;
         }
+        if (PHI_SMEM && tid < a.RT) phis[a.nRT + tid] = 0.0f;   // the row invalid slots load
         if (tid < a.RT) {
             best_s[tid] = a.best_obj[tile * a.RT + tid];
             improved_s[tid] = 0;
         }
         if (tid == 0) ks_s[a.step_begin & 1] = (float)(a.ks_scale * ks_value(a.ks_max, a.ks_period, (double)a.step_begin * a.h));
     }
-    const uint64_t seed = a.seeds[rg];
-    const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    uint2 key[RPL];
+    bool live[RPL];
+#pragma unroll
+    for (int e = 0; e < RPL; ++e) {
+        const uint64_t seed = a.seeds[rg0 + e];
+        key[e] = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+        live[e] = rg0 + e < a.R_real;
+    }
     const int gp0 = a.warp_start[warp];
     const uint2 *stream_g = a.stream + (size_t)gp0 * a.C + c;               // this lane's slot, stride C
     const uint32_t stream32 = smem32 + a.off_stream + (uint32_t)(gp0 * a.C + c) * 8;
@@ -241,34 +296,82 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     const uint32_t w32 = smem32 + a.off_w + (uint32_t)(gp0 * a.C + c) * 16;
     __syncthreads();
 
-    auto load_phi = [&](uint32_t iRT) -> float { return PHI_SMEM ? lds_f32(phi32 + iRT * 4) : phi_g[iRT]; };
-    auto store_phi = [&](uint32_t iRT, float v) {
-        if (PHI_SMEM) sts_f32(phi32 + iRT * 4, v);
-        else phi_g[iRT] = v;
+    auto load_phi = [&](uint32_t iRT, float (&p)[RPL]) {
+        if (RPL == 2) {
+            float2 t;
+            if (PHI_SMEM) t = lds_f2(phi32 + iRT * 4);
+            else t = *reinterpret_cast<const float2 *>(phi_g + iRT);
+            p[0] = t.x; p[RPL - 1] = t.y;
+        } else {
+            p[0] = PHI_SMEM ? lds_f32(phi32 + iRT * 4) : phi_g[iRT];
+        }
     };
-    auto pair_at = [&](uint32_t idRT) -> float2 { float2 v; lds_pair(pair_addr<3>(idRT, cs32), v); return v; };
+    auto store_phi = [&](uint32_t iRT, const float (&p)[RPL]) {
+        if (RPL == 2) {
+            if (PHI_SMEM) sts_pair(phi32 + iRT * 4, p[0], p[RPL - 1]);
+            else *reinterpret_cast<float2 *>(phi_g + iRT) = make_float2(p[0], p[RPL - 1]);
+        } else {
+            if (PHI_SMEM) sts_f32(phi32 + iRT * 4, p[0]);
+            else phi_g[iRT] = p[0];
+        }
+    };
+    auto pairs_at = [&](uint32_t idRT) -> PairPack<RPL> { PairPack<RPL> pp; pp.load(pair_addr<3>(idRT, cs32)); return pp; };
     auto group_at = [&](int g) -> uint2 { return IDX_SMEM ? lds_u64(stream32 + (uint32_t)(g * a.C) * 8) : stream_g[g * a.C]; };
     auto weights_at = [&](int g) -> float4 {
         return IDX_SMEM ? lds_f4(w32 + (uint32_t)(g * a.C) * 16) : *reinterpret_cast<const float4 *>(w_g + (size_t)(g * a.C) * 4);
     };
     auto row_at = [&](int row) -> uint32_t { return lds_u16(rows32 + (uint32_t)(row * a.C) * 2); };
-    auto state_of = [&](uint32_t idRT) -> uint32_t {
-        if (NMODE == 2) return __float_as_uint(pair_at(idRT).x) >> 31;
-        return lds_u8(st32 + idRT);
+    auto states_of = [&](uint32_t idRT, uint32_t (&st)[RPL]) {
+        if (NMODE == 2) {
+            const PairPack<RPL> pp = pairs_at(idRT);
+#pragma unroll
+            for (int e = 0; e < RPL; ++e) st[e] = __float_as_uint(pp.v[e].x) >> 31;
+        } else {
+#pragma unroll
+            for (int e = 0; e < RPL; ++e) st[e] = lds_u8(st32 + idRT + e);
+        }
+    };
+    auto publish_states = [&]() {              // best_states rows of the replicas that just improved
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) {
+            if (improved_s[r0 + e] && live[e]) {
+                uint8_t *dst = a.best_states + (size_t)(rg0 + e) * a.n;
+                for (int row = 0; row < a.n_rows; ++row) {
+                    const uint32_t iRT = row_at(row);
+                    if (iRT < (uint32_t)a.nRT) {
+                        uint32_t st[RPL];
+                        states_of(iRT, st);
+                        dst[iRT >> a.LRT] = (uint8_t)st[e];
+                    }
+                }
+            }
+        }
+    };
+    auto record_best = [&](double obj, long long step_label) {     // threads tid < RT: strict improvement
+        const double b = best_s[tid];
+        const bool better = a.maximize ? (obj > b) : (obj < b);
+        improved_s[tid] = better ? 1 : 0;
+        if (better) {
+            best_s[tid] = obj;
+            const int gi = tile * a.RT + tid;
+            if (a.use_target && a.first_hit[gi] < 0 && (a.maximize ? (obj >= a.target) : (obj <= a.target)))
+                a.first_hit[gi] = step_label;
+        }
     };
 
     // explicit scoring pass over the state in cs (/ state bytes); sample_col >= 0 also records the trace column
     auto score_current = [&](long long step_label, int sample_col) {
-        double obj_part = 0.0, en_part = 0.0;
+        double obj_part[RPL], en_part[RPL];
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) { obj_part[e] = 0.0; en_part[e] = 0.0; }
         int g = 0;
         for (int row = 0; row < a.n_rows; ++row) {
             const uint32_t iRT = row_at(row);
             const int G = (int)lds_u8(g32 + row);
             if (iRT < (uint32_t)a.nRT) {
-                const uint32_t si = state_of(iRT);
-                const float2 own = pair_at(iRT);
-                int count = 0;
-                double wsum = 0.0;
+                uint32_t si[RPL];
+                states_of(iRT, si);
+                const PairPack<RPL> own = pairs_at(iRT);
                 for (int gg = 0; gg < G; ++gg) {
                     const uint2 pk = group_at(g + gg);
                     float4 w4 = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -279,43 +382,29 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     for (int u = 0; u < 4; ++u) {
                         const uint32_t jRT = jj[u];
                         if (jRT > iRT && jRT < (uint32_t)a.nRT) {          // canonical pairs i < j only
-                            const bool same = state_of(jRT) == si;
-                            const bool hit = a.maximize ? !same : same;
-                            if (WEIGHTED) { if (hit) wsum += a.maximize ? (double)ww[u] : 1.0; }
-                            else count += hit ? 1 : 0;
-                            if (sample_col >= 0) {
-                                const float2 v = pair_at(jRT);
-                                en_part += (double)ww[u] * ((double)own.x * (double)v.x + (double)own.y * (double)v.y);
+                            uint32_t sj[RPL];
+                            states_of(jRT, sj);
+                            const PairPack<RPL> v = pairs_at(jRT);
+#pragma unroll
+                            for (int e = 0; e < RPL; ++e) {
+                                const bool same = sj[e] == si[e];
+                                const bool hit = a.maximize ? !same : same;
+                                if (hit) obj_part[e] += (WEIGHTED && a.maximize) ? (double)ww[u] : 1.0;
+                                if (sample_col >= 0)
+                                    en_part[e] += (double)ww[u] * ((double)own.v[e].x * (double)v.v[e].x + (double)own.v[e].y * (double)v.v[e].y);
                             }
                         }
                     }
                 }
-                obj_part += WEIGHTED ? wsum : (double)count;
             }
             g += G;
         }
-        const double obj = tile_reduce(obj_part, a.RT, part, tid, a.W);
-        if (tid < a.RT) {
-            const double b = best_s[tid];
-            const bool better = a.maximize ? (obj > b) : (obj < b);
-            improved_s[tid] = better ? 1 : 0;
-            if (better) {
-                best_s[tid] = obj;
-                const int gi = tile * a.RT + tid;
-                if (a.use_target && a.first_hit[gi] < 0 && (a.maximize ? (obj >= a.target) : (obj <= a.target)))
-                    a.first_hit[gi] = step_label;
-            }
-        }
+        const double obj = tile_reduce_rpl<RPL>(obj_part, a.RT, a.LPS, part, tid, a.W);
+        if (tid < a.RT) record_best(obj, step_label);
         __syncthreads();
-        if (improved_s[r] && live) {
-            uint8_t *dst = a.best_states + (size_t)rg * a.n;
-            for (int row = 0; row < a.n_rows; ++row) {
-                const uint32_t iRT = row_at(row);
-                if (iRT < (uint32_t)a.nRT) dst[iRT >> a.LRT] = (uint8_t)state_of(iRT);
-            }
-        }
+        publish_states();
         if (sample_col >= 0) {
-            const double en = tile_reduce(en_part, a.RT, part, tid, a.W);
+            const double en = tile_reduce_rpl<RPL>(en_part, a.RT, a.LPS, part, tid, a.W);
             if (tid < a.RT) {
                 const size_t gi = (size_t)(tile * a.RT + tid);
                 a.energy[gi * a.trace_stride + sample_col] = en;
@@ -325,29 +414,6 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         __syncthreads();
     };
 
-    // N = 2: `twice_cut` was counted during the gather of step `step_label + 1`
-    auto finish_piggyback = [&](int twice_cut, long long step_label) {
-        const double obj = 0.5 * tile_reduce((double)twice_cut, a.RT, part, tid, a.W);
-        if (tid < a.RT) {
-            const double b = best_s[tid];
-            const bool better = obj > b;
-            improved_s[tid] = better ? 1 : 0;
-            if (better) {
-                best_s[tid] = obj;
-                const int gi = tile * a.RT + tid;
-                if (a.use_target && a.first_hit[gi] < 0 && obj >= a.target) a.first_hit[gi] = step_label;
-            }
-        }
-        __syncthreads();
-        if (improved_s[r] && live) {               // cs still holds the scored state (pass B comes later)
-            uint8_t *dst = a.best_states + (size_t)rg * a.n;
-            for (int row = 0; row < a.n_rows; ++row) {
-                const uint32_t iRT = row_at(row);
-                if (iRT < (uint32_t)a.nRT) dst[iRT >> a.LRT] = (uint8_t)(__float_as_uint(pair_at(iRT).x) >> 31);
-            }
-        }
-    };
-
     int sample_cur = 0;
     while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < a.step_begin) ++sample_cur;
 
@@ -355,7 +421,12 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         if (NMODE != 2) {
             for (int row = 0; row < a.n_rows; ++row) {
                 const uint32_t iRT = row_at(row);
-                if (iRT < (uint32_t)a.nRT) sts_u8(st32 + iRT, (uint32_t)threshold_state((double)load_phi(iRT), a.tc.n_states));
+                if (iRT < (uint32_t)a.nRT) {
+                    float p[RPL];
+                    load_phi(iRT, p);
+#pragma unroll
+                    for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, (uint32_t)threshold_state((double)p[e], a.tc.n_states));
+                }
             }
             __syncthreads();
         }
@@ -371,8 +442,10 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         const float hks = ks_s[step & 1];           // h*ks, or 2*h*ks for N = 2
         const bool is_sample = sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] == step;
         const bool cadence_hit = a.cadence > 0 && step % a.cadence == 0;
-        const bool count_now = NMODE == 2 && !WEIGHTED && pending;
-        int twice_cut = 0;
+        const bool count_now = PIGGY && pending;
+        int twice_cut[RPL];
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) twice_cut[e] = 0;
 
         // pass A ------------------------------------------------------------------------------
         // The stream of a warp is contiguous: a running pointer walks it and the next group is
@@ -392,69 +465,99 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             return w4;
         };
         uint2 pk = IDX_SMEM ? lds_u64(sp32) : *spg;
-        float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+        float z[RPL][4];
+#pragma unroll
+        for (int e = 0; e < RPL; ++e) { z[e][0] = 0.f; z[e][1] = 0.f; z[e][2] = 0.f; z[e][3] = 0.f; }
 #pragma unroll 1
         for (int row = 0; row < a.n_rows; ++row) {
             const uint32_t iRT = row_at(row);
             const int G = (int)lds_u8(g32 + row);
             const bool valid = iRT < (uint32_t)a.nRT;
-            const float p = load_phi(iRT);              // issued a whole gather ahead of its use
-            if ((row & 3) == 0 && a.noise_on && valid)
-                normals4_fast(philox4x32_10(make_uint4((iRT >> a.LRT) >> 2, (uint32_t)step, (uint32_t)(step >> 32), 0x6F736362u), key),
-                              z0, z1, z2, z3);
-            float2 sum = make_float2(0.f, 0.f);
-            int neg = 0;
-            if (NMODE == 2 && !WEIGHTED && count_now) {
+            float p[RPL];
+            load_phi(iRT, p);                           // issued a whole gather ahead of its use
+            if ((row & 3) == 0 && a.noise_on && valid) {
+#pragma unroll
+                for (int e = 0; e < RPL; ++e)
+                    normals4_fast(philox4x32_10(make_uint4((iRT >> a.LRT) >> 2, (uint32_t)step, (uint32_t)(step >> 32), 0x6F736362u), key[e]),
+                                  z[e][0], z[e][1], z[e][2], z[e][3]);
+            }
+            float2 sum[RPL];
+            int neg[RPL];
+#pragma unroll
+            for (int e = 0; e < RPL; ++e) { sum[e] = make_float2(0.f, 0.f); neg[e] = 0; }
+            if (PIGGY && count_now) {
                 // scoring step: the sign bit of every gathered cosine is the neighbour's lattice state
-#pragma unroll 2
+#pragma unroll 1
                 for (int gg = 0; gg < G; ++gg) {
                     const uint2 nx = next_group();
-                    const float2 v0 = pair_at(pk.x & 0xffffu), v1 = pair_at(pk.x >> 16);
-                    const float2 v2 = pair_at(pk.y & 0xffffu), v3 = pair_at(pk.y >> 16);
-                    sum = __fadd2_rn(sum, __fadd2_rn(__fadd2_rn(v0, v1), __fadd2_rn(v2, v3)));
-                    neg += (int)(__float_as_uint(v0.x) >> 31) + (int)(__float_as_uint(v1.x) >> 31);
-                    neg += (int)(__float_as_uint(v2.x) >> 31) + (int)(__float_as_uint(v3.x) >> 31);
+                    const PairPack<RPL> v0 = pairs_at(pk.x & 0xffffu), v1 = pairs_at(pk.x >> 16);
+                    const PairPack<RPL> v2 = pairs_at(pk.y & 0xffffu), v3 = pairs_at(pk.y >> 16);
+#pragma unroll
+                    for (int e = 0; e < RPL; ++e) {
+                        sum[e] = __fadd2_rn(sum[e], __fadd2_rn(__fadd2_rn(v0.v[e], v1.v[e]), __fadd2_rn(v2.v[e], v3.v[e])));
+                        neg[e] += (int)(__float_as_uint(v0.v[e].x) >> 31) + (int)(__float_as_uint(v1.v[e].x) >> 31);
+                        neg[e] += (int)(__float_as_uint(v2.v[e].x) >> 31) + (int)(__float_as_uint(v3.v[e].x) >> 31);
+                    }
                     pk = nx;
                 }
             } else {
 #pragma unroll 2
                 for (int gg = 0; gg < G; ++gg) {
                     const uint2 nx = next_group();
-                    const float2 v0 = pair_at(pk.x & 0xffffu), v1 = pair_at(pk.x >> 16);
-                    const float2 v2 = pair_at(pk.y & 0xffffu), v3 = pair_at(pk.y >> 16);
+                    const PairPack<RPL> v0 = pairs_at(pk.x & 0xffffu), v1 = pairs_at(pk.x >> 16);
+                    const PairPack<RPL> v2 = pairs_at(pk.y & 0xffffu), v3 = pairs_at(pk.y >> 16);
                     if (WEIGHTED) {
                         const float4 w4 = next_weights();
-                        sum = __ffma2_rn(make_float2(w4.x, w4.x), v0, sum);
-                        sum = __ffma2_rn(make_float2(w4.y, w4.y), v1, sum);
-                        sum = __ffma2_rn(make_float2(w4.z, w4.z), v2, sum);
-                        sum = __ffma2_rn(make_float2(w4.w, w4.w), v3, sum);
+#pragma unroll
+                        for (int e = 0; e < RPL; ++e) {
+                            sum[e] = __ffma2_rn(make_float2(w4.x, w4.x), v0.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.y, w4.y), v1.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.z, w4.z), v2.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.w, w4.w), v3.v[e], sum[e]);
+                        }
                     } else {
-                        sum = __fadd2_rn(sum, __fadd2_rn(__fadd2_rn(v0, v1), __fadd2_rn(v2, v3)));
+#pragma unroll
+                        for (int e = 0; e < RPL; ++e)
+                            sum[e] = __fadd2_rn(sum[e], __fadd2_rn(__fadd2_rn(v0.v[e], v1.v[e]), __fadd2_rn(v2.v[e], v3.v[e])));
                     }
                     pk = nx;
                 }
             }
             if (valid) {
-                const float2 own = pair_at(iRT);
-                const float ci = own.x, si = own.y;
-                if (NMODE == 2 && !WEIGHTED && count_now)   // differing neighbours: deg - neg if the row itself is in state 1
-                    twice_cut += (ci < 0.f) ? (int)deg_lane[row * a.C] - neg : neg;
-                const float acc = si * sum.x - ci * sum.y;
-                float shil;
-                if (NMODE == 2) shil = si * ci;                                  // hks holds 2 h ks
-                else shil = shil_term(p, si, ci, a.tc);
+                const PairPack<RPL> own = pairs_at(iRT);
                 const uint32_t k = (iRT >> a.LRT) & 3u;
-                const float kick = (k & 2u) ? ((k & 1u) ? z3 : z2) : ((k & 1u) ? z1 : z0);
-                const float x = fmaf(a.hK, acc, fmaf(-hks, shil, fmaf(a.knsh, kick, p)));
-                float y = x - floorf(x);
-                y = (y >= 1.0f) ? 0.0f : y;
-                if (!(fabsf(x) < INFINITY) && live) flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)rg, iRT >> a.LRT);
+                int deg = 0;
+                if (PIGGY && count_now) deg = (int)deg_lane[row * a.C];
+                float y[RPL];
+#pragma unroll
+                for (int e = 0; e < RPL; ++e) {
+                    const float ci = own.v[e].x, si = own.v[e].y;
+                    if (PIGGY && count_now)   // differing neighbours: deg - neg if the row itself is in state 1
+                        twice_cut[e] += (ci < 0.f) ? deg - neg[e] : neg[e];
+                    const float acc = si * sum[e].x - ci * sum[e].y;
+                    float shil;
+                    if (NMODE == 2) shil = si * ci;                              // hks holds 2 h ks
+                    else shil = shil_term(p[e], si, ci, a.tc);
+                    const float kick = (k & 2u) ? ((k & 1u) ? z[e][3] : z[e][2]) : ((k & 1u) ? z[e][1] : z[e][0]);
+                    const float x = fmaf(a.hK, acc, fmaf(-hks, shil, fmaf(a.knsh, kick, p[e])));
+                    float w = x - floorf(x);
+                    y[e] = (w >= 1.0f) ? 0.0f : w;
+                    if (!(fabsf(x) < INFINITY) && live[e])
+                        flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)(rg0 + e), iRT >> a.LRT);
+                }
                 store_phi(iRT, y);
             }
         }
         if (tid == 0) ks_s[(step + 1) & 1] = (float)(a.ks_scale * ks_value(a.ks_max, a.ks_period, (double)(step + 1) * a.h));
         if (count_now) {
-            finish_piggyback(twice_cut, pending_label);
+            // `twice_cut` counted the state after step `pending_label`; cs still holds that state
+            double tc[RPL];
+#pragma unroll
+            for (int e = 0; e < RPL; ++e) tc[e] = (double)twice_cut[e];
+            const double obj = 0.5 * tile_reduce_rpl<RPL>(tc, a.RT, a.LPS, part, tid, a.W);
+            if (tid < a.RT) record_best(obj, pending_label);
+            __syncthreads();
+            publish_states();
             pending = false;
         }
         __syncthreads();
@@ -465,11 +568,23 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         for (int row = 0; row < a.n_rows; ++row) {
             const uint32_t iRT = row_at(row);
             if (iRT < (uint32_t)a.nRT) {
-                const float p = load_phi(iRT);
-                float s, co;
-                sincospif(2.0f * p, &s, &co);
-                sts_pair(pair_addr<3>(iRT, cs32), co + 0.0f, s);
-                if (NMODE != 2 && score_after) sts_u8(st32 + iRT, (uint32_t)threshold_state((double)p, a.tc.n_states));
+                float p[RPL];
+                load_phi(iRT, p);
+                float s[RPL], co[RPL];
+#pragma unroll
+                for (int e = 0; e < RPL; ++e) {
+                    sincospif(2.0f * p[e], &s[e], &co[e]);
+                    co[e] += 0.0f;
+                }
+                if (RPL == 2)
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pair_addr<3>(iRT, cs32)), "f"(co[0]), "f"(s[0]),
+                                 "f"(co[RPL - 1]), "f"(s[RPL - 1]) : "memory");
+                else
+                    sts_pair(pair_addr<3>(iRT, cs32), co[0], s[0]);
+                if (NMODE != 2 && score_after) {
+#pragma unroll
+                    for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, (uint32_t)threshold_state((double)p[e], a.tc.n_states));
+                }
             }
         }
         __syncthreads();
@@ -478,7 +593,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             score_current(step, a.sample_offset + sample_cur);
             ++sample_cur;
         } else if (cadence_hit) {
-            if (NMODE == 2 && !WEIGHTED && a.piggy && step + 1 < a.step_end) {
+            if (PIGGY && a.piggy && step + 1 < a.step_end) {
                 pending = true;
                 pending_label = step;
             } else {
@@ -492,7 +607,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     {
         const float *phis = reinterpret_cast<const float *>(smem_raw + a.off_phi);
         float *slab = a.phi + (size_t)tile * a.nRT;
-        for (int q = tid; q < a.nRT; q += NT) slab[q] = phis[q];
+        for (int i = tid; i < a.nRT; i += NT) slab[i] = phis[i];
     }
 }
 

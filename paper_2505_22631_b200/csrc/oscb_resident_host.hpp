@@ -16,7 +16,7 @@
 namespace oscb {
 
 struct ResidentPlan {
-    int RT = 1, log2RT = 0, C = 32, T = 1, W = 1;
+    int RT = 1, log2RT = 0, LPS = 1, C = 32, T = 1, W = 1;   // LPS: lanes per slot (RT / replicas per lane)
     int n_group_rows = 0;
     bool weighted = false;
     double fill = 1.0;          // real neighbours / stream entries
@@ -31,9 +31,9 @@ struct ResidentPlan {
 
 // warps per CTA for a tile of RT replicas: as many slots as there are quads to hand out, in
 // the fewest rounds the thread limit allows
-static void tile_shape(int64_t n, int RT, int max_threads, int *W, int *T)
+static void tile_shape(int64_t n, int LPS, int max_threads, int *W, int *T)
 {
-    const int C = 32 / RT;
+    const int C = 32 / LPS;
     const int64_t Q = (n + 3) / 4;
     const int64_t s_max = (int64_t)(max_threads / 32) * C;
     const int64_t rounds = std::max<int64_t>(1, (Q + s_max - 1) / s_max);
@@ -54,15 +54,16 @@ struct ResidentStreamHost {
     int64_t real = 0, positions = 0, conflicts = 0;
 };
 
-// `pair_bytes` (8: float2, 16: double2) fixes which slots share a shared-memory wavefront:
-// 128 bytes = 16 (8) lanes = H = max(1, 16 (8) / RT) consecutive slots, and row j sits in bank
-// class j mod H of that wavefront.  `keep_order` (parity mode) keeps every row in CSR order and
+// A slot is LPS lanes wide (RT replicas / replicas per lane) and reads RT * pair_bytes contiguous
+// bytes per neighbour.  `pair_bytes` (8: float2, 16: double2) fixes which slots share a 128-byte
+// shared-memory wavefront: H = max(1, 128 / (RT * pair_bytes)) consecutive slots, and row j sits
+// in bank class j mod H of that wavefront.  `keep_order` (parity mode) keeps every row in CSR order and
 // only picks conflict-free padding rows; otherwise each row's neighbours are also reordered so
 // that the H slots of a wavefront hit H different classes wherever the lists allow it.
-static void compile_resident_stream(int n, const int *indptr, const int *indices, const double *wts, int RT, int W,
-                                    int T, int pair_bytes, bool keep_order, ResidentStreamHost *out)
+static void compile_resident_stream(int n, const int *indptr, const int *indices, const double *wts, int RT, int LPS,
+                                    int W, int T, int pair_bytes, bool keep_order, ResidentStreamHost *out)
 {
-    const int C = 32 / RT, S = W * C;
+    const int C = 32 / LPS, S = W * C;
     const int Q = (n + 3) / 4;
     const int H = std::max(1, std::min(C, (128 / pair_bytes) / RT));
     OSCB_REQUIRE((int64_t)(n + OSCB_PAD_ROWS) * RT <= 65535, "n * replicas_per_cta too large for 16-bit stream ids");
@@ -205,19 +206,21 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
     }
 }
 
-static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, int W, int T, int pair_bytes, bool keep_order)
+static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, int LPS, int W, int T, int pair_bytes,
+                                                         bool keep_order)
 {
     auto plan = std::make_shared<ResidentPlan>();
     plan->RT = RT;
     plan->log2RT = 0;
     while ((1 << plan->log2RT) < RT) ++plan->log2RT;
-    plan->C = 32 / RT;
+    plan->LPS = LPS;
+    plan->C = 32 / LPS;
     plan->W = W;
     plan->T = T;
     plan->weighted = !g->unit_weights;
     ResidentStreamHost h;
-    compile_resident_stream((int)g->n, g->h_indptr.data(), g->h_indices.data(), g->h_w.data(), RT, W, T, pair_bytes,
-                            keep_order, &h);
+    compile_resident_stream((int)g->n, g->h_indptr.data(), g->h_indices.data(), g->h_w.data(), RT, LPS, W, T,
+                            pair_bytes, keep_order, &h);
     OSCB_REQUIRE(h.real == g->nnz, "internal: resident plan lost neighbours (%lld of %lld)", (long long)h.real, (long long)g->nnz);
     plan->n_group_rows = h.n_group_rows;
     plan->fill = h.n_group_rows == 0 ? 1.0 : (double)h.real / (4.0 * (double)h.n_group_rows * plan->C);
@@ -237,23 +240,38 @@ static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, 
     return plan;
 }
 
-static std::shared_ptr<ResidentPlan> get_resident_plan(oscb_graph *g, int RT, int W, int T, int pair_bytes, bool keep_order)
+static std::shared_ptr<ResidentPlan> get_resident_plan(oscb_graph *g, int RT, int LPS, int W, int T, int pair_bytes,
+                                                       bool keep_order)
 {
-    const uint64_t key = ((uint64_t)RT << 40) | ((uint64_t)W << 20) | ((uint64_t)T << 8) | ((uint64_t)pair_bytes << 1) |
-                         (keep_order ? 1u : 0u);
+    const uint64_t key = ((uint64_t)RT << 48) | ((uint64_t)LPS << 40) | ((uint64_t)W << 24) | ((uint64_t)T << 8) |
+                         ((uint64_t)pair_bytes << 1) | (keep_order ? 1u : 0u);
     auto it = g->plans.find(key);
     if (it != g->plans.end()) return it->second;
-    auto plan = build_resident_plan(g, RT, W, T, pair_bytes, keep_order);
+    auto plan = build_resident_plan(g, RT, LPS, W, T, pair_bytes, keep_order);
     g->plans[key] = plan;
     return plan;
 }
 
 struct ResidentConfig {
-    int RT = 0, W = 0, T = 0, max_threads = 1024;
+    int RT = 0, LPS = 0, W = 0, T = 0, max_threads = 1024;
     size_t smem_min = 0; // without the stream staged in shared memory
 };
 
 static inline int max_threads_for(int precision) { return precision == OSCB_PREC_F64 ? 512 : 1024; }
+
+// the specialised float32 kernel applies unless the float64 parity mode, injected noise or the
+// generic variant was asked for
+static inline bool wants_fast(const oscb_run_params *p)
+{
+    return p->precision == OSCB_PREC_F32 && p->noise_mode != OSCB_NOISE_HOST && p->variant != 1;
+}
+// replicas per lane of the float32 kernel: two whenever a tile has two (OSCB_FAST_RPL=1 disables)
+static inline int fast_rpl(int RT)
+{
+    const char *e = getenv("OSCB_FAST_RPL");
+    if (e && e[0] == '1') return 1;
+    return RT >= 2 ? 2 : 1;
+}
 
 static size_t resident_smem_bytes(const oscb_graph *g, int precision, int n_states, int RT, int W, int T,
                                   int n_group_rows, bool idx_smem)
@@ -265,7 +283,7 @@ static size_t resident_smem_bytes(const oscb_graph *g, int precision, int n_stat
 
 // tile width: the candidate with the lowest estimated time
 static bool choose_resident_config(const oscb_graph *g, int precision, int n_states, int64_t R, int requested_rt,
-                                   ResidentConfig *out)
+                                   bool fast, ResidentConfig *out)
 {
     if (g->n > 60000 || g->max_degree > 1020 || n_states > 254) return false;
     static const double eff[6] = {0.35, 0.5, 0.7, 0.85, 1.0, 1.0}; // gather efficiency by log2(RT)
@@ -277,9 +295,12 @@ static bool choose_resident_config(const oscb_graph *g, int precision, int n_sta
         if (requested_rt > 0 && RT != requested_rt) continue;
         if (requested_rt <= 0 && RT > 1 && RT / 2 >= R) continue; // do not pad a tile more than 2x
         int W, T;
-        tile_shape(g->n, RT, max_threads, &W, &T);
+        const int LPS = fast ? RT / fast_rpl(RT) : RT;
+        tile_shape(g->n, LPS, max_threads, &W, &T);
         if ((g->n + OSCB_PAD_ROWS) * RT > 65535) continue;
-        const size_t need = resident_smem_bytes(g, precision, n_states, RT, W, T, 0, false);
+        const size_t need = fast ? FastSmem::make((int)g->n, RT, 32 / LPS, T, W, 0, n_states != 2, false, false, false,
+                                                  !g->unit_weights).total
+                                 : resident_smem_bytes(g, precision, n_states, RT, W, T, 0, false);
         if (need > (size_t)g->smem_optin) continue;
         const int64_t tiles = (R + RT - 1) / RT;
         const int by_smem = (int)std::max<size_t>(1, (size_t)(g->smem_optin + 1024) / (need + 1024));
@@ -292,6 +313,7 @@ static bool choose_resident_config(const oscb_graph *g, int precision, int n_sta
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
             out->RT = RT;
+            out->LPS = LPS;
             out->W = W;
             out->T = T;
             out->max_threads = max_threads;
@@ -305,7 +327,7 @@ static bool choose_resident_config(const oscb_graph *g, int precision, int n_sta
 static bool resident_fits(const oscb_graph *g, const oscb_run_params *p, int64_t R)
 {
     ResidentConfig cfg;
-    return choose_resident_config(g, p->precision, p->n_states, R, p->replicas_per_cta, &cfg);
+    return choose_resident_config(g, p->precision, p->n_states, R, p->replicas_per_cta, wants_fast(p), &cfg);
 }
 
 template <typename T, int MAXT, bool STRICT>
@@ -331,29 +353,22 @@ struct FastFit {
     FastSmem lay;
     size_t smem = 0;
 };
-static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT, int W, int T, int n_group_rows)
+static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT, int C, int W, int T, int n_group_rows)
 {
     const bool weighted = !g->unit_weights;
     FastFit f;
     f.states = n_states != 2;
     f.piggy = n_states == 2 && !weighted && objective == OSCB_OBJ_MAXCUT;
     auto lay = [&](bool phi, bool idx) {
-        return FastSmem::make((int)g->n, RT, 32 / RT, T, W, n_group_rows, f.states, f.deg_smem, phi, idx, weighted);
+        return FastSmem::make((int)g->n, RT, C, T, W, n_group_rows, f.states, f.deg_smem, phi, idx, weighted);
     };
     const size_t cap = (size_t)g->smem_optin;
     // The neighbour stream is on the critical path of every gather (a phase is touched three
     // times per row and its load can be issued a whole row early), so the stream gets the
-    // shared memory first; OSCB_FAST_PREFER=phi reverses the order (experiments).  The degree
-    // table is read on scoring steps only and goes to shared memory last.
-    const char *pref = getenv("OSCB_FAST_PREFER");
-    const bool phi_first = pref && pref[0] == 'p';
-    if (phi_first) {
-        if (lay(true, false).total <= cap) f.phi_smem = true;
-        if (lay(f.phi_smem, true).total <= cap) f.idx_smem = true;
-    } else {
-        if (lay(false, true).total <= cap) f.idx_smem = true;
-        if (lay(true, f.idx_smem).total <= cap) f.phi_smem = true;
-    }
+    // shared memory first, the phases second.  The degree table is read on scoring steps only
+    // and goes to shared memory last.
+    if (lay(false, true).total <= cap) f.idx_smem = true;
+    if (f.idx_smem && lay(true, true).total <= cap) f.phi_smem = true;
     if (f.piggy) {
         f.deg_smem = true;
         if (lay(f.phi_smem, f.idx_smem).total > cap) f.deg_smem = false;
@@ -369,6 +384,9 @@ static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const Re
     FastArgs a;
     memset(&a, 0, sizeof(a));
     a.n = ra.n; a.RT = ra.RT; a.LRT = ra.log2RT; a.nRT = ra.n * ra.RT; a.C = ra.C; a.W = ra.W; a.n_rows = 4 * ra.T;
+    a.LPS = plan.LPS; a.LLPS = 0;
+    while ((1 << a.LLPS) < a.LPS) ++a.LLPS;
+    const int rpl = ra.RT / plan.LPS;
     a.R_real = ra.R_real; a.n_group_rows = ra.n_group_rows; a.piggy = f.piggy ? 1 : 0; a.deg_smem = f.deg_smem ? 1 : 0;
     a.off_cs = (uint32_t)f.lay.cs; a.off_phi = (uint32_t)f.lay.phi; a.off_st = (uint32_t)f.lay.st;
     a.off_rows = (uint32_t)f.lay.rows; a.off_g = (uint32_t)f.lay.g; a.off_deg = (uint32_t)f.lay.deg;
@@ -393,8 +411,13 @@ static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const Re
     auto by_mem = [&](auto nm, auto wt) {
         constexpr int NM = decltype(nm)::value;
         constexpr bool WT = decltype(wt)::value;
-        if (f.idx_smem) { if (f.phi_smem) go(k_resident_fast<NM, WT, true, true>); else go(k_resident_fast<NM, WT, true, false>); }
-        else            { if (f.phi_smem) go(k_resident_fast<NM, WT, false, true>); else go(k_resident_fast<NM, WT, false, false>); }
+        if (rpl == 2) {
+            if (f.idx_smem) { if (f.phi_smem) go(k_resident_fast<NM, WT, true, true, 2>); else go(k_resident_fast<NM, WT, true, false, 2>); }
+            else go(k_resident_fast<NM, WT, false, false, 2>);
+        } else {
+            if (f.idx_smem) { if (f.phi_smem) go(k_resident_fast<NM, WT, true, true, 1>); else go(k_resident_fast<NM, WT, true, false, 1>); }
+            else go(k_resident_fast<NM, WT, false, false, 1>);
+        }
     };
     using two = std::integral_constant<int, 2>;
     using any = std::integral_constant<int, 0>;
@@ -409,7 +432,7 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
 {
     cudaStream_t s = g->stream;
     const int n = (int)g->n, R = (int)R64;
-    auto plan = get_resident_plan(g, cfg.RT, cfg.W, cfg.T, (int)(2 * sizeof(T)), STRICT);
+    auto plan = get_resident_plan(g, cfg.RT, cfg.LPS, cfg.W, cfg.T, (int)(2 * sizeof(T)), STRICT);
     const int RT = plan->RT, tiles = (R + RT - 1) / RT, R_pad = tiles * RT;
     bool idx_smem = true;
     size_t smem = resident_smem_bytes(g, p->precision, p->n_states, RT, plan->W, plan->T, plan->n_group_rows, true);
@@ -419,7 +442,7 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     }
     FastFit fast;
     if (FAST) {
-        fast = fit_fast(g, p->n_states, p->objective, RT, plan->W, plan->T, plan->n_group_rows);
+        fast = fit_fast(g, p->n_states, p->objective, RT, plan->C, plan->W, plan->T, plan->n_group_rows);
         smem = fast.smem;
     }
     OSCB_REQUIRE(smem <= (size_t)g->smem_optin, "resident kernel does not fit in shared memory (%zu bytes)", smem);
@@ -531,12 +554,12 @@ static void run_resident(oscb_graph *g, const oscb_run_params *p, int64_t steps,
                          const double *phi0, const double *noise, oscb_run_outputs *out)
 {
     ResidentConfig cfg;
-    OSCB_REQUIRE(choose_resident_config(g, p->precision, p->n_states, R, p->replicas_per_cta, &cfg),
+    OSCB_REQUIRE(choose_resident_config(g, p->precision, p->n_states, R, p->replicas_per_cta, wants_fast(p), &cfg),
                  "the resident kernel cannot hold this problem (n = %lld, max degree %lld); use the streaming kernel",
                  (long long)g->n, (long long)g->max_degree);
     if (p->precision == OSCB_PREC_F64)
         run_resident_impl<double, 512, true, false>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
-    else if (p->noise_mode == OSCB_NOISE_HOST || p->variant == 1)   // injected noise / variant 1: the generic kernel
+    else if (!wants_fast(p))   // injected noise / variant 1: the generic kernel
         run_resident_impl<float, 1024, false, false>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
     else
         run_resident_impl<float, 1024, false, true>(g, p, cfg, steps, cadence, sample_steps, seeds, R, phi0, noise, out);
