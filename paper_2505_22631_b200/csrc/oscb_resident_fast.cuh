@@ -104,6 +104,7 @@ struct FastArgs {
     const uint2 *stream;               // [(n_group_rows + 1) * C]
     const float *wstream;              // [(n_group_rows + 1) * C * 4]
     float *phi;                        // [tiles][n][RT] (+ one padding row at the very end)
+    float2 *cs_next;                   // [tiles][n][RT] next-step (cos, sin) pairs, L2-resident staging (N = 2 kernels)
     const uint64_t *seeds;
     const long long *sample_steps;
     double *best_obj, *energy, *best_trace;
@@ -228,6 +229,10 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     const int tile = blockIdx.x;
     const int rg0 = tile * a.RT + r0;
     float *phi_g = a.phi + (size_t)tile * a.nRT + r0;       // the tile's slab (global), + row*RT
+    float2 *stage_g = a.cs_next + (size_t)tile * a.nRT + r0; // next-step pairs of this lane's replicas, + row*RT
+    // N = 2: the trig of the new phase is done right in the row epilogue of pass A (where it overlaps
+    // other warps' gathers) and parked in an L2-resident staging slab; pass B is then a plain copy.
+    constexpr bool STAGED = NMODE == 2;
 
     // lane-resident shared addresses (+ row*RT scaled by the element size)
     const uint32_t cs32 = smem32 + a.off_cs + r0 * 8;
@@ -546,6 +551,16 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                         flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)(rg0 + e), iRT >> a.LRT);
                 }
                 store_phi(iRT, y);
+                if (STAGED) {
+                    float s2[RPL], c2[RPL];
+#pragma unroll
+                    for (int e = 0; e < RPL; ++e) {
+                        sincospif(2.0f * y[e], &s2[e], &c2[e]);
+                        c2[e] += 0.0f;
+                    }
+                    if (RPL == 2) *reinterpret_cast<float4 *>(stage_g + iRT) = make_float4(c2[0], s2[0], c2[RPL - 1], s2[RPL - 1]);
+                    else stage_g[iRT] = make_float2(c2[0], s2[0]);
+                }
             }
         }
         if (tid == 0) ks_s[(step + 1) & 1] = (float)(a.ks_scale * ks_value(a.ks_max, a.ks_period, (double)(step + 1) * a.h));
@@ -564,26 +579,44 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
 
         // pass B: pairs (and state bytes) of the new phases -------------------------------------
         const bool score_after = is_sample || cadence_hit;
-#pragma unroll 1
-        for (int row = 0; row < a.n_rows; ++row) {
-            const uint32_t iRT = row_at(row);
-            if (iRT < (uint32_t)a.nRT) {
-                float p[RPL];
-                load_phi(iRT, p);
-                float s[RPL], co[RPL];
-#pragma unroll
-                for (int e = 0; e < RPL; ++e) {
-                    sincospif(2.0f * p[e], &s[e], &co[e]);
-                    co[e] += 0.0f;
+        if (STAGED) {
+            // each lane copies back the pairs it staged itself (same thread wrote them: no fence needed)
+#pragma unroll 4
+            for (int row = 0; row < a.n_rows; ++row) {
+                const uint32_t iRT = row_at(row);
+                if (iRT < (uint32_t)a.nRT) {
+                    if (RPL == 2) {
+                        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(pair_addr<3>(iRT, cs32)), "l"(stage_g + iRT) : "memory");
+                    } else {
+                        float2 v;
+                        asm volatile("ld.global.cg.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(stage_g + iRT) : "memory");
+                        sts_pair(pair_addr<3>(iRT, cs32), v.x, v.y);
+                    }
                 }
-                if (RPL == 2)
-                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pair_addr<3>(iRT, cs32)), "f"(co[0]), "f"(s[0]),
-                                 "f"(co[RPL - 1]), "f"(s[RPL - 1]) : "memory");
-                else
-                    sts_pair(pair_addr<3>(iRT, cs32), co[0], s[0]);
-                if (NMODE != 2 && score_after) {
+            }
+            if (RPL == 2) asm volatile("cp.async.wait_all;" ::: "memory");
+        } else {
+#pragma unroll 1
+            for (int row = 0; row < a.n_rows; ++row) {
+                const uint32_t iRT = row_at(row);
+                if (iRT < (uint32_t)a.nRT) {
+                    float p[RPL];
+                    load_phi(iRT, p);
+                    float s[RPL], co[RPL];
 #pragma unroll
-                    for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, (uint32_t)threshold_state((double)p[e], a.tc.n_states));
+                    for (int e = 0; e < RPL; ++e) {
+                        sincospif(2.0f * p[e], &s[e], &co[e]);
+                        co[e] += 0.0f;
+                    }
+                    if (RPL == 2)
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pair_addr<3>(iRT, cs32)), "f"(co[0]), "f"(s[0]),
+                                     "f"(co[RPL - 1]), "f"(s[RPL - 1]) : "memory");
+                    else
+                        sts_pair(pair_addr<3>(iRT, cs32), co[0], s[0]);
+                    if (score_after) {
+#pragma unroll
+                        for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, (uint32_t)threshold_state((double)p[e], a.tc.n_states));
+                    }
                 }
             }
         }
