@@ -144,6 +144,36 @@ int oscb_run(oscb_graph *g, const oscb_run_params *params, const uint64_t *seeds
              const double *noise /* [steps, R, n] when noise_mode == OSCB_NOISE_HOST */,
              oscb_run_outputs *out);
 
+/* ---- one oversized dense graph, row-sharded over several GPUs ------------------
+ * Every rank creates its shard with oscb_graph_create_dense(device, n, J_rows, row_begin, row_end)
+ * and owns the phases of those rows.  Per Euler step each rank calls oscb_dense_shard_step on the
+ * FULL phase array (all n oscillators, device memory, layout [n][R] replica-minor, float32 or
+ * float64 by `precision`) and gets the new phases of ITS rows ([rows][R]); the host side then
+ * all-gathers the slices (NCCL through torch.distributed) into the next full array.  These calls
+ * take DEVICE pointers and enqueue on `stream` (a cudaStream_t; NULL = the handle's own stream)
+ * without synchronising, so they compose with the collective on the same stream.
+ *   oscb_dense_shard_step       trig precompute + _step_* for the shard's rows  dynamics.py:393-401
+ *   oscb_dense_shard_objective  this shard's part of _score_kernel's sum        dynamics.py:214-223
+ *                               (sum over ranks = the objective; all-reduce it)
+ *   oscb_dense_shard_energy     this shard's part of the sample() energy        dynamics.py:380
+ *   oscb_graph_nonfinite        first non-finite (replica, oscillator, step) seen by the handle */
+typedef struct oscb_shard_step_params {
+    double K, ks, h, kn_sqrt_h;
+    int32_t n_states, precision, noise_on, reserved;
+    int64_t step;                       /* global step index (noise counter, non-finite report) */
+} oscb_shard_step_params;
+
+int oscb_dense_shard_step(oscb_graph *g, int64_t R, const oscb_shard_step_params *p,
+                          const void *phi_full_dev, void *phi_rows_out_dev,
+                          const uint64_t *seeds_dev /* [R] */, void *stream);
+int oscb_dense_shard_objective(oscb_graph *g, int64_t R, int32_t precision, const void *phi_full_dev,
+                               int32_t n_states, int32_t maximize, double *partial_dev /* [R] */,
+                               void *stream);
+int oscb_dense_shard_energy(oscb_graph *g, int64_t R, int32_t precision, const void *phi_full_dev,
+                            double *partial_dev /* [R] */, void *stream);
+int oscb_graph_nonfinite(oscb_graph *g, int64_t where[3] /* replica, oscillator, step; -1 if none */,
+                         int32_t reset);
+
 /* Device self-test behind the N = 2 scoring shortcut of the float32 kernel: counts the float32
  * phases in [0, 1) (all 2^30-ish of them) whose sign-of-cosine state differs from the reference
  * threshold (dynamics.py:203-213).  Must return 0 mismatches. */

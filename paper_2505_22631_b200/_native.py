@@ -55,6 +55,12 @@ class RunOutputs(C.Structure):
                 ("replicas_per_cta", C.c_int32), ("smem_bytes", C.c_int64)]
 
 
+class ShardStepParams(C.Structure):
+    _fields_ = [("K", C.c_double), ("ks", C.c_double), ("h", C.c_double), ("kn_sqrt_h", C.c_double),
+                ("n_states", C.c_int32), ("precision", C.c_int32), ("noise_on", C.c_int32), ("reserved", C.c_int32),
+                ("step", C.c_int64)]
+
+
 # every symbol include/oscb.h declares: name -> (restype, argtypes)
 _P = C.c_void_p
 SYMBOLS = {
@@ -71,6 +77,10 @@ SYMBOLS = {
                             C.c_int32, C.c_int32, _P, _P]),
     "oscb_score": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, _P, _P]),
     "oscb_energy": (C.c_int, [_P, C.c_int64, _P, _P]),
+    "oscb_dense_shard_step": (C.c_int, [_P, C.c_int64, C.POINTER(ShardStepParams), _P, _P, _P, _P]),
+    "oscb_dense_shard_objective": (C.c_int, [_P, C.c_int64, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P]),
+    "oscb_dense_shard_energy": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P, _P]),
+    "oscb_graph_nonfinite": (C.c_int, [_P, _P, C.c_int32]),
     "oscb_selftest_sign_state": (C.c_int, [C.c_int, C.POINTER(C.c_uint64)]),
     "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),

@@ -12,6 +12,7 @@
 #include "oscb_stream.cuh"
 #include "oscb_resident_host.hpp"
 #include "oscb_dense_host.hpp"
+#include <type_traits>
 
 #include <algorithm>
 #include <cmath>
@@ -161,7 +162,7 @@ template <typename T> struct StreamWork {
     DevBuf<T2> cs[2];
     DevBuf<double> io;          // [R, n] float64 staging in the host layout
     DevBuf<uint8_t> states;     // [n, R]
-    DevBuf<double> partial, obj;
+    DevBuf<double> partial, obj, dense_partial;
     int P = 1, chunk = 1;
     int cur = 0;
 
@@ -177,6 +178,7 @@ template <typename T> struct StreamWork {
         if (chunk < 1) chunk = 1;
         partial.alloc((size_t)P * R);
         obj.alloc(R);
+        if (g->is_dense) dense_partial.alloc((size_t)n * R);
     }
     // host-layout float64 phases already in `io` -> device layout + trig
     void load_from_io(cudaStream_t s)
@@ -198,9 +200,13 @@ static void launch_stream_step(const oscb_graph *g, StreamWork<T> &wk, const uin
 {
     const long long threads = (long long)((g->n + 3) / 4) * wk.R;
     const int nxt = wk.cur ^ 1;
-    k_stream_step<T, STRICT><<<blocks_for(threads, 256), 256, 0, g->stream>>>(
-        csr_view(g), wk.R, wk.phi[wk.cur].p, wk.cs[wk.cur].p, wk.phi[nxt].p, wk.cs[nxt].p, d_seeds,
-        d_noise, sc, g->d_nonfinite.p);
+    if (g->is_dense)
+        launch_dense_step<T>(g, g->stream, wk.R, wk.phi[wk.cur].p, wk.cs[wk.cur].p, wk.phi[nxt].p, wk.cs[nxt].p, d_seeds,
+                             d_noise, sc);
+    else
+        k_stream_step<T, STRICT><<<blocks_for(threads, 256), 256, 0, g->stream>>>(
+            csr_view(g), wk.R, wk.phi[wk.cur].p, wk.cs[wk.cur].p, wk.phi[nxt].p, wk.cs[nxt].p, d_seeds,
+            d_noise, sc, g->d_nonfinite.p);
     wk.cur = nxt;
 }
 
@@ -217,7 +223,11 @@ static int launch_stream_score(const oscb_graph *g, StreamWork<T> &wk, int n_sta
     k_threshold<T><<<blocks_for(tot, 256), 256, 0, s>>>(wk.phi[wk.cur].p, wk.states.p, tot, n_states);
     ++launches;
     int P = wk.P;
-    if (sequential) {
+    if (g->is_dense) {
+        launch_dense_pairs<T>(g, s, wk.R, maximize ? 0 : 1, wk.states.p, nullptr, wk.dense_partial.p, wk.partial.p, 1);
+        P = 1;
+        ++launches;
+    } else if (sequential) {
         k_objective_seq<<<blocks_for(wk.R, 64), 64, 0, s>>>(wk.states.p, wk.R, g->d_iu.p, g->d_jv.p,
                                                             g->d_pw.p, (int)g->pairs, maximize, wk.partial.p);
         P = 1;
@@ -352,8 +362,11 @@ static void run_stream(oscb_graph *g, const oscb_run_params *p, const RunPlan &r
     };
     auto sample = [&](long long step_label, int64_t col) {
         score(step_label);
-        k_energy<T><<<R, 256, 0, s>>>(wk.phi[wk.cur].p, R, g->d_iu.p, g->d_jv.p, g->d_pw.p, (int)g->pairs,
-                                      d_energy.p + col, S);
+        if (g->is_dense)
+            launch_dense_pairs<T>(g, s, R, 2, nullptr, wk.cs[wk.cur].p, wk.dense_partial.p, d_energy.p + col, S);
+        else
+            k_energy<T><<<R, 256, 0, s>>>(wk.phi[wk.cur].p, R, g->d_iu.p, g->d_jv.p, g->d_pw.p, (int)g->pairs,
+                                          d_energy.p + col, S);
         k_record_best<<<blocks_for(R, 128), 128, 0, s>>>(d_best.p, d_btrace.p + col, S, R);
         launches += 2;
     };
@@ -423,6 +436,70 @@ static void run_stream(oscb_graph *g, const oscb_run_params *p, const RunPlan &r
         set_error("non-finite phase for oscillator %lld (replica row %lld) after step %lld; parameters are numerically unstable",
                   (long long)out->nonfinite[1], (long long)out->nonfinite[0], (long long)out->nonfinite[2]);
         throw OscbFail{OSCB_ENONFINITE};
+    }
+}
+
+// workspace of the row-sharded dense driver: pairs and states of all n oscillators, row partials
+struct ShardWork {
+    int R = 0, precision = 0;
+    DevBuf<unsigned char> cs;      // [n][R] pairs in the call's precision
+    DevBuf<uint8_t> states;        // [n][R]
+    DevBuf<double> partial;        // [rows][R]
+    bool flag_armed = false;
+};
+
+static ShardWork &shard_work(oscb_graph *g, int R, int precision)
+{
+    if (!g->shard_work || g->shard_work->R != R || g->shard_work->precision != precision) {
+        auto w = std::make_shared<ShardWork>();
+        w->R = R;
+        w->precision = precision;
+        const size_t tot = (size_t)g->n * R;
+        w->cs.alloc(tot * (precision == OSCB_PREC_F64 ? 16 : 8));
+        w->states.alloc(tot);
+        w->partial.alloc((size_t)(g->row_end - g->row_begin) * R);
+        g->shard_work = w;
+    }
+    if (!g->shard_work->flag_armed) {
+        const unsigned long long none = ~0ull;
+        OSCB_CUDA(cudaMemcpy(g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice));
+        g->shard_work->flag_armed = true;
+    }
+    return *g->shard_work;
+}
+
+template <typename T>
+static void shard_step_impl(oscb_graph *g, int R, const oscb_shard_step_params *p, const void *phi_full, void *phi_rows,
+                            const uint64_t *seeds_dev, cudaStream_t s)
+{
+    using T2 = typename Vec2<T>::type;
+    ShardWork &w = shard_work(g, R, p->precision);
+    const long long tot = (long long)g->n * R;
+    T2 *cs = reinterpret_cast<T2 *>(w.cs.p);
+    k_trig<T><<<blocks_for(tot, 256), 256, 0, s>>>(reinterpret_cast<const T *>(phi_full), cs, tot);
+    StepScalars sc;
+    sc.K = p->K; sc.ks = p->ks; sc.h = p->h; sc.kn_sqrt_h = p->kn_sqrt_h;
+    sc.tc = make_trig_const(p->n_states);
+    sc.step = (uint64_t)p->step;
+    sc.noise_mode = p->noise_on ? OSCB_NOISE_DEVICE : OSCB_NOISE_NONE;
+    launch_dense_step<T>(g, s, R, reinterpret_cast<const T *>(phi_full), cs, reinterpret_cast<T *>(phi_rows),
+                         (T2 *)nullptr, seeds_dev, nullptr, sc);
+}
+
+template <typename T>
+static void shard_pairs_impl(oscb_graph *g, int R, int precision, const void *phi_full, int mode, int n_states,
+                             double *partial_dev, cudaStream_t s)
+{
+    using T2 = typename Vec2<T>::type;
+    ShardWork &w = shard_work(g, R, precision);
+    const long long tot = (long long)g->n * R;
+    if (mode == 2) {
+        T2 *cs = reinterpret_cast<T2 *>(w.cs.p);
+        k_trig<T><<<blocks_for(tot, 256), 256, 0, s>>>(reinterpret_cast<const T *>(phi_full), cs, tot);
+        launch_dense_pairs<T>(g, s, R, 2, nullptr, cs, w.partial.p, partial_dev, 1);
+    } else {
+        k_threshold<T><<<blocks_for(tot, 256), 256, 0, s>>>(reinterpret_cast<const T *>(phi_full), w.states.p, tot, n_states);
+        launch_dense_pairs<T>(g, s, R, mode, w.states.p, (const T2 *)nullptr, w.partial.p, partial_dev, 1);
     }
 }
 
@@ -519,6 +596,7 @@ int oscb_graph_destroy(oscb_graph *g)
     }
     g->plans.clear();
     g->dense.reset();
+    g->shard_work.reset();
     cudaStream_t s = g->stream;
     delete g;
     if (s) cudaStreamDestroy(s);
@@ -596,10 +674,6 @@ int oscb_step(oscb_graph *g, int64_t R, const double *phi_in, const double *nois
         OSCB_REQUIRE(precision == OSCB_PREC_F32 || precision == OSCB_PREC_F64, "unknown precision %d", precision);
         OSCB_REQUIRE(g->row_begin == 0 && g->row_end == g->n, "oscb_step needs the whole graph, not a row shard");
         bind_device(g);
-        if (g->is_dense && g->dense) {
-            dense_step(g, R, phi_in, noise, K, ks, h, kn_sqrt_h, n_states, precision, phi_out, nonfinite);
-            return OSCB_OK;
-        }
         if (precision == OSCB_PREC_F64)
             step_impl<double, true>(g, R, phi_in, noise, K, ks, h, kn_sqrt_h, n_states, phi_out, nonfinite);
         else
@@ -649,10 +723,92 @@ int oscb_energy(oscb_graph *g, int64_t R, const double *phi, double *energy)
         DevBuf<double> io(tot), dev(tot), en(R);
         io.upload(phi, tot, s);
         k_to_dev_layout<double><<<blocks_for((long long)tot, 256), 256, 0, s>>>(io.p, dev.p, (int)g->n, (int)R);
+        if (g->is_dense) {
+            DevBuf<double2> cs(tot);
+            DevBuf<double> partial(tot);
+            k_trig<double><<<blocks_for((long long)tot, 256), 256, 0, s>>>(dev.p, cs.p, (long long)tot);
+            launch_dense_pairs<double>(g, s, (int)R, 2, nullptr, cs.p, partial.p, en.p, 1);
+            check_launch("oscb_energy");
+            en.download(energy, R, s);
+            OSCB_CUDA(cudaStreamSynchronize(s));
+            return OSCB_OK;
+        }
         k_energy<double><<<(unsigned)R, 256, 0, s>>>(dev.p, (int)R, g->d_iu.p, g->d_jv.p, g->d_pw.p, (int)g->pairs, en.p, 1);
         check_launch("oscb_energy");
         en.download(energy, R, s);
         OSCB_CUDA(cudaStreamSynchronize(s));
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_shard_step(oscb_graph *g, int64_t R, const oscb_shard_step_params *p, const void *phi_full_dev,
+                          void *phi_rows_out_dev, const uint64_t *seeds_dev, void *stream)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(g && p && phi_full_dev && phi_rows_out_dev, "NULL argument");
+        OSCB_REQUIRE(g->is_dense && g->dense, "oscb_dense_shard_step needs a dense (row shard) handle");
+        OSCB_REQUIRE(R >= 1 && R <= 65536, "replicas must be in [1, 65536]");
+        OSCB_REQUIRE(p->precision == OSCB_PREC_F32 || p->precision == OSCB_PREC_F64, "unknown precision %d", p->precision);
+        OSCB_REQUIRE(p->n_states >= 2 && p->n_states <= 255, "n_states must be in [2, 255]");
+        OSCB_REQUIRE(!p->noise_on || seeds_dev != nullptr, "noise needs the seeds");
+        bind_device(g);
+        cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
+        if (p->precision == OSCB_PREC_F64) shard_step_impl<double>(g, (int)R, p, phi_full_dev, phi_rows_out_dev, seeds_dev, s);
+        else shard_step_impl<float>(g, (int)R, p, phi_full_dev, phi_rows_out_dev, seeds_dev, s);
+        check_launch("oscb_dense_shard_step");
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_shard_objective(oscb_graph *g, int64_t R, int32_t precision, const void *phi_full_dev, int32_t n_states,
+                               int32_t maximize, double *partial_dev, void *stream)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(g && phi_full_dev && partial_dev, "NULL argument");
+        OSCB_REQUIRE(g->is_dense && g->dense, "oscb_dense_shard_objective needs a dense (row shard) handle");
+        OSCB_REQUIRE(R >= 1 && R <= 65536, "replicas must be in [1, 65536]");
+        OSCB_REQUIRE(precision == OSCB_PREC_F32 || precision == OSCB_PREC_F64, "unknown precision %d", precision);
+        OSCB_REQUIRE(n_states >= 2 && n_states <= 255, "n_states must be in [2, 255]");
+        bind_device(g);
+        cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
+        if (precision == OSCB_PREC_F64) shard_pairs_impl<double>(g, (int)R, precision, phi_full_dev, maximize ? 0 : 1, n_states, partial_dev, s);
+        else shard_pairs_impl<float>(g, (int)R, precision, phi_full_dev, maximize ? 0 : 1, n_states, partial_dev, s);
+        check_launch("oscb_dense_shard_objective");
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_shard_energy(oscb_graph *g, int64_t R, int32_t precision, const void *phi_full_dev, double *partial_dev,
+                            void *stream)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(g && phi_full_dev && partial_dev, "NULL argument");
+        OSCB_REQUIRE(g->is_dense && g->dense, "oscb_dense_shard_energy needs a dense (row shard) handle");
+        OSCB_REQUIRE(R >= 1 && R <= 65536, "replicas must be in [1, 65536]");
+        OSCB_REQUIRE(precision == OSCB_PREC_F32 || precision == OSCB_PREC_F64, "unknown precision %d", precision);
+        bind_device(g);
+        cudaStream_t s = stream ? (cudaStream_t)stream : g->stream;
+        if (precision == OSCB_PREC_F64) shard_pairs_impl<double>(g, (int)R, precision, phi_full_dev, 2, 2, partial_dev, s);
+        else shard_pairs_impl<float>(g, (int)R, precision, phi_full_dev, 2, 2, partial_dev, s);
+        check_launch("oscb_dense_shard_energy");
+        return OSCB_OK;
+    });
+}
+
+int oscb_graph_nonfinite(oscb_graph *g, int64_t where[3], int32_t reset)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(g && where, "NULL argument");
+        bind_device(g);
+        OSCB_CUDA(cudaDeviceSynchronize());
+        unsigned long long flag = ~0ull;
+        OSCB_CUDA(cudaMemcpy(&flag, g->d_nonfinite.p, sizeof(flag), cudaMemcpyDeviceToHost));
+        where[0] = where[1] = where[2] = -1;
+        if (flag != ~0ull) decode_nonfinite(flag, where);
+        if (reset) {
+            const unsigned long long none = ~0ull;
+            OSCB_CUDA(cudaMemcpy(g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice));
+        }
         return OSCB_OK;
     });
 }
@@ -755,11 +911,11 @@ int oscb_run(oscb_graph *g, const oscb_run_params *p, const uint64_t *seeds, int
             if (out->trace_ks) out->trace_ks[k] = ks_value(p->ks_max, p->ks_period, t);
         }
 
-        if (g->is_dense && g->dense) {
-            run_dense(g, p, rp.steps, rp.cadence, rp.sample_steps, seeds, R, phi0, noise, out);
-            return OSCB_OK;
-        }
         int kernel = p->kernel;
+        if (g->is_dense) {
+            OSCB_REQUIRE(kernel != OSCB_KERNEL_RESIDENT, "dense couplings run on the streaming loop (no resident kernel)");
+            kernel = OSCB_KERNEL_STREAM;
+        }
         if (kernel == OSCB_KERNEL_AUTO)
             kernel = resident_fits(g, p, R) ? OSCB_KERNEL_RESIDENT : OSCB_KERNEL_STREAM;
         if (kernel == OSCB_KERNEL_RESIDENT) {

@@ -1,55 +1,123 @@
-// oscb_dense_host.hpp -- dense all-to-all couplings (north_star subsystem 2, dense branch).
+// oscb_dense_host.hpp -- host side of the dense path: upload of a row shard of J and the
+// launch helpers the generic entry points (oscb_step / oscb_score / oscb_energy / oscb_run)
+// and the sharded driver (oscb_dense_shard_*) share.
 #pragma once
 #include "oscb_host.hpp"
+#include "oscb_dense.cuh"
 #include <cmath>
 
 namespace oscb {
 
+enum DenseKind { DENSE_I8 = 0, DENSE_F = 1 };
+
 struct DensePlan {
-    int dummy = 0;
+    int kind = DENSE_F;
+    int n_pad = 0;
+    DevBuf<int8_t> J8;
+    DevBuf<float> J32;
+    DevBuf<double> J64;
 };
 
-static void finish_csr(oscb_graph *g);
-
 // J: rows [row_begin, row_end) of the full symmetric matrix, row-major, n columns each.
-// Round-1 first cut: the couplings are compacted to the canonical CSR so every entry point works
-// on dense inputs through the sparse kernels; the dedicated dense kernel replaces this.
 static void build_dense(oscb_graph *g, const double *J)
 {
-    const int64_t n = g->n;
-    OSCB_REQUIRE(g->row_begin == 0 && g->row_end == n, "row-sharded dense graphs need the dense kernel (not built yet)");
-    g->h_indptr.assign(n + 1, 0);
-    g->h_indices.clear();
-    g->h_w.clear();
-    for (int64_t i = 0; i < n; ++i) {
+    const int64_t n = g->n, rows = g->row_end - g->row_begin;
+    const int n_pad = (int)((n + 3) / 4 * 4);
+    bool unit = true, integral = true, small = true;
+    int64_t nnz = 0, pairs = 0, maxdeg = 0;
+    for (int64_t q = 0; q < rows; ++q) {
+        const int64_t i = g->row_begin + q;
+        int64_t d = 0;
         for (int64_t j = 0; j < n; ++j) {
-            const double v = J[i * n + j];
+            const double v = J[q * n + j];
             OSCB_REQUIRE(std::isfinite(v), "non-finite coupling at (%lld, %lld)", (long long)i, (long long)j);
             OSCB_REQUIRE(i != j || v == 0.0, "coupling diagonal must be zero");
             if (v != 0.0) {
-                g->h_indices.push_back((int)j);
-                g->h_w.push_back(v);
+                ++d;
+                if (j > i) ++pairs;
+                if (v != 1.0) unit = false;
+                if (v != std::nearbyint(v)) integral = false;
+                if (std::fabs(v) > 127.0) small = false;
             }
         }
-        OSCB_REQUIRE(g->h_indices.size() < (size_t)1 << 31, "too many couplings");
-        g->h_indptr[i + 1] = (int)g->h_indices.size();
+        nnz += d;
+        maxdeg = std::max(maxdeg, d);
     }
-    g->nnz = (int64_t)g->h_indices.size();
-    finish_csr(g);
+    g->nnz = nnz;
+    g->pairs = pairs;
+    g->max_degree = maxdeg;
+    g->unit_weights = unit;
+    g->int_weights = integral;
+    auto plan = std::make_shared<DensePlan>();
+    plan->n_pad = n_pad;
+    cudaStream_t s = g->stream;
+    const size_t elems = (size_t)rows * n_pad;
+    if (integral && small) {
+        plan->kind = DENSE_I8;
+        std::vector<int8_t> h(elems, 0);
+        for (int64_t q = 0; q < rows; ++q)
+            for (int64_t j = 0; j < n; ++j) h[(size_t)q * n_pad + j] = (int8_t)J[q * n + j];
+        plan->J8.alloc(elems);
+        plan->J8.upload(h.data(), elems, s);
+        OSCB_CUDA(cudaStreamSynchronize(s));
+    } else {
+        plan->kind = DENSE_F;
+        std::vector<double> h64(elems, 0.0);
+        std::vector<float> h32(elems, 0.f);
+        for (int64_t q = 0; q < rows; ++q)
+            for (int64_t j = 0; j < n; ++j) {
+                h64[(size_t)q * n_pad + j] = J[q * n + j];
+                h32[(size_t)q * n_pad + j] = (float)J[q * n + j];
+            }
+        plan->J64.alloc(elems);
+        plan->J64.upload(h64.data(), elems, s);
+        plan->J32.alloc(elems);
+        plan->J32.upload(h32.data(), elems, s);
+        OSCB_CUDA(cudaStreamSynchronize(s));
+    }
+    g->dense = plan;
 }
 
-static void dense_step(oscb_graph *, int64_t, const double *, const double *, double, double, double, double,
-                       int, int, double *, int64_t *)
+// One dense Euler step of the handle's rows on stream `s`.
+template <typename T>
+static void launch_dense_step(const oscb_graph *g, cudaStream_t s, int R, const T *phi_in,
+                              const typename Vec2<T>::type *cs_in, T *phi_out, typename Vec2<T>::type *cs_out,
+                              const uint64_t *d_seeds, const double *d_noise, const StepScalars &sc)
 {
-    set_error("dense kernel not built");
-    throw OscbFail{OSCB_ECUDA};
+    const DensePlan &pl = *g->dense;
+    DenseStepArgs a;
+    a.n = (int)g->n; a.n_pad = pl.n_pad; a.row_begin = (int)g->row_begin; a.rows = (int)(g->row_end - g->row_begin);
+    a.R = R; a.sc = sc;
+    const unsigned bx = (unsigned)((a.rows + 7) / 8);
+    auto go = [&](auto jptr) {
+        using JT = std::remove_cv_t<std::remove_pointer_t<decltype(jptr)>>;
+        if (R == 1) k_dense_step<T, JT, 1><<<dim3(bx, 1), 256, 0, s>>>(a, jptr, phi_in, cs_in, phi_out, cs_out, d_seeds, d_noise, g->d_nonfinite.p);
+        else k_dense_step<T, JT, 8><<<dim3(bx, (unsigned)((R + 7) / 8)), 256, 0, s>>>(a, jptr, phi_in, cs_in, phi_out, cs_out, d_seeds, d_noise, g->d_nonfinite.p);
+    };
+    if (pl.kind == DENSE_I8) go((const int8_t *)pl.J8.p);
+    else if (sizeof(T) == 8) go((const double *)pl.J64.p);
+    else go((const float *)pl.J32.p);
 }
 
-static void run_dense(oscb_graph *, const oscb_run_params *, int64_t, int64_t, const std::vector<long long> &,
-                      const uint64_t *, int64_t, const double *, const double *, oscb_run_outputs *)
+// Row partials of the objective (mode 0 cut / 1 conflicts) or the energy (mode 2) into `partial`
+// [rows][R], then their in-order sum into out[r * out_stride].
+template <typename T>
+static void launch_dense_pairs(const oscb_graph *g, cudaStream_t s, int R, int mode, const uint8_t *states,
+                               const typename Vec2<T>::type *cs, double *partial, double *out, long long out_stride)
 {
-    set_error("dense kernel not built");
-    throw OscbFail{OSCB_ECUDA};
+    const DensePlan &pl = *g->dense;
+    const int n = (int)g->n, rb = (int)g->row_begin, rows = (int)(g->row_end - g->row_begin);
+    const dim3 grid((unsigned)((rows + 7) / 8), (unsigned)R);
+    auto go = [&](auto jptr) {
+        using JT = std::remove_cv_t<std::remove_pointer_t<decltype(jptr)>>;
+        if (mode == 0) k_dense_pairs<T, JT, 0><<<grid, 256, 0, s>>>(n, pl.n_pad, rb, rows, R, jptr, states, cs, partial);
+        else if (mode == 1) k_dense_pairs<T, JT, 1><<<grid, 256, 0, s>>>(n, pl.n_pad, rb, rows, R, jptr, states, cs, partial);
+        else k_dense_pairs<T, JT, 2><<<grid, 256, 0, s>>>(n, pl.n_pad, rb, rows, R, jptr, states, cs, partial);
+    };
+    if (pl.kind == DENSE_I8) go((const int8_t *)pl.J8.p);
+    else if (sizeof(T) == 8) go((const double *)pl.J64.p);
+    else go((const float *)pl.J32.p);
+    k_dense_reduce<<<(unsigned)((R + 127) / 128), 128, 0, s>>>(partial, rows, R, out, out_stride);
 }
 
 } // namespace oscb

@@ -78,6 +78,7 @@ template <typename T> struct DevBuf {
 
 struct ResidentPlan; // oscb_resident_host.hpp
 struct DensePlan;    // oscb_dense_host.hpp
+struct ShardWork;    // oscb.cu: workspace of the row-sharded dense driver
 
 } // namespace oscb
 
@@ -104,4 +105,5 @@ struct oscb_graph {
     // resident-kernel plans keyed by (precision, replicas_per_cta, threads)
     std::map<uint64_t, std::shared_ptr<oscb::ResidentPlan>> plans;
     std::shared_ptr<oscb::DensePlan> dense;
+    std::shared_ptr<oscb::ShardWork> shard_work;
 };

@@ -392,6 +392,24 @@ class BatchResult:
     wall_time: float
 
 
+def _objective_cadence_for(n: int, pair_count: int) -> int:
+    """Steps between best-of objective checks (dynamics.py:325-330)."""
+    return max(1, min(10, round(pair_count / max(n, 1))))
+
+
+def _sample_steps(steps: int, h: float, stride: float) -> List[int]:
+    """Steps after which the reference takes a trace sample (dynamics.py:385, :404-408), with the
+    same float arithmetic."""
+    out, next_sample = [], stride
+    for step in range(steps):
+        t_next = (step + 1) * h
+        if t_next >= next_sample or step == steps - 1:
+            while next_sample <= t_next:
+                next_sample += stride
+            out.append(step)
+    return out
+
+
 def _sample_capacity(steps: int, h: float, stride: float) -> int:
     return int(min(steps + 2, steps * h / stride + 8))
 
