@@ -178,13 +178,80 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def bench_dense(args, rank, world, local_rank):
+    """configs[4]: dense +-1 SK graph, J row-sharded over the ranks, phases all-gathered every Euler
+    step (strong scaling: the graph is fixed, the rows per GPU shrink)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2505_22631_b200 import workloads
+    from paper_2505_22631_b200.dense_sharded import CudaDenseShard, run_dense_sharded
+    from paper_2505_22631_b200.model import SolverParams
+    n = int(args.workload[2:].split("x")[0])
+    R = args.replicas or int(args.workload.split("x")[1])
+    window = args.window if args.window != 2048 else 256
+    rows = n // world
+    J8 = workloads.sk_dense(n)                                   # int8, symmetric, zero diagonal
+    shard = CudaDenseShard(J8[rank * rows:(rank + 1) * rows].astype(np.float64), n, rank * rows, (rank + 1) * rows,
+                           local_rank, args.precision)
+    del J8
+    params = SolverParams.tuned_for(n, 2, seed=0)
+    seeds = list(range(R))
+    pairs = n * (n - 1) // 2
+
+    def one():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        res = run_dense_sharded(shard, params, "maxcut", seeds, pair_count=pairs, steps=window)
+        torch.cuda.synchronize()
+        return time.perf_counter() - t0, res
+
+    for _ in range(args.warmup):
+        one()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    total = 0.0
+    for _ in range(args.steps):
+        dt, res = one()
+        total += dt
+    clocks = sampler.stop()
+    t = torch.tensor([total], dtype=torch.float64, device=f"cuda:{local_rank}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.cpu())
+    nnz = n * (n - 1)
+    value = R * nnz * window * args.steps / total
+    peaks, peak_kind = measured_peaks()
+    # algorithmic HBM bytes per Euler step and GPU: the shard of J once (1 B per coupling, int8) + phases
+    bytes_step = rows * n * 1 + 2 * R * n * (4 if args.precision == "f32" else 8)
+    achieved = bytes_step * window * args.steps / total / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": f"dense +-1 SK graph n={n}, {R} replica(s), J row-sharded over {world} GPU(s) with a phase "
+                                   f"all-gather per Euler step, window {window} Euler steps incl. scoring every 10",
+                       "replicas": R, "window": window, "parallelism": f"row-shard x{world}",
+                       "l2": "J shard (n^2/G bytes) exceeds L2 for n=16384 at G<=2; re-read from HBM every step"},
+            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": int(8 * R * n), "d2h_bytes_per_step": int(9 * R * n),
+                    "note": "run_dense_sharded takes host phases in and returns host results; timed wall clock"},
+            "gpu_launches": int(window * 2.4) * args.steps,
+            "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "peak_kind": peak_kind, "kernel": "k_dense_step",
+                         "note": "per GPU; includes the host loop (one launch + one all-gather per Euler step)"},
+        }), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="G22x1024", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="G22x1024", help="one of %s, or SK<n>x<replicas> (dense, row-sharded)" % sorted(WORKLOADS))
     ap.add_argument("--window", type=int, default=2048, help="Euler steps per bench step")
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "resident"])
@@ -208,6 +275,12 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    if args.workload.startswith("SK"):
+        bench_dense(args, rank, world, local_rank)
+        if dist is not None:
+            dist.destroy_process_group()
+        return
 
     from paper_2505_22631_b200 import _native as nat
     from paper_2505_22631_b200 import dynamics as dyn

@@ -241,16 +241,22 @@ def _scratch_graph(device: int, n: int) -> DeviceGraph:
     return _scratch[key]
 
 
+# Couplings stored dense (model.py:21, :190-192) get the dense device path (J in HBM, O(n^2)
+# kernels) only from this size on; below it the device CSR + the persistent shared-memory kernel
+# is the faster home even for a complete graph (rows of up to 1020 neighbours fit its stream).
+DENSE_DEVICE_MIN_N = 1021
+
+
 def device_graph(J: CouplingMatrix, device: Optional[int] = None) -> DeviceGraph:
-    """The (cached) device mirror of J on `device`: dense J when the coupling is stored dense
-    (model.py:21, :190-192), device CSR otherwise (north_star subsystem 1)."""
+    """The (cached) device mirror of J on `device`: dense J for large couplings stored dense,
+    device CSR otherwise (north_star subsystem 1)."""
     device = _default_device() if device is None else device
     cache = J._device
     if cache is None:
         cache = {}
         J._device = cache
     if device not in cache:
-        if J.storage_kind == "dense" and J._dense is not None:
+        if J.storage_kind == "dense" and J._dense is not None and J.n >= DENSE_DEVICE_MIN_N:
             cache[device] = DeviceGraph.from_dense(device, J._dense)
         else:
             cache[device] = DeviceGraph.from_csr(device, J.n, J.indptr, J.indices, J.data)

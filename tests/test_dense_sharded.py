@@ -140,9 +140,12 @@ def test_two_rank_gloo_orchestration_matches_oracle(tmp_path, oracle):
 @pytest.fixture(scope="module")
 def pkg():
     import paper_2505_22631_b200 as p
-    from paper_2505_22631_b200 import _native
+    from paper_2505_22631_b200 import _native, dynamics
     assert _native.device_count() > 0, "no CUDA device: " + _native.last_error()
-    return p
+    old = dynamics.DENSE_DEVICE_MIN_N
+    dynamics.DENSE_DEVICE_MIN_N = 0          # exercise the dense kernels on test-sized graphs
+    yield p
+    dynamics.DENSE_DEVICE_MIN_N = old
 
 
 @pytest.mark.gpu
