@@ -114,6 +114,9 @@ typedef struct oscb_run_outputs {
 const char *oscb_last_error(void);
 int oscb_version(void);
 int oscb_device_count(int *count);
+/* Device workspaces are recycled through a size-keyed pool between calls; this frees the parked
+ * blocks (cudaFree).  Never needed for correctness. */
+int oscb_pool_trim(void);
 
 int oscb_graph_create_csr(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
                           const double *data, oscb_graph **out);

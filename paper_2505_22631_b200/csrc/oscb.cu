@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <mutex>
+#include <utility>
 
 namespace oscb {
 
@@ -31,6 +33,67 @@ void set_error(const char *fmt, ...)
     vsnprintf(buf, sizeof(buf), fmt, ap);
     va_end(ap);
     g_last_error = buf;
+}
+
+// ---- device block pool -------------------------------------------------------------------
+static std::mutex g_pool_mutex;
+static std::map<std::pair<int, size_t>, std::vector<void *>> g_pool;
+static size_t g_pool_bytes = 0;
+static const size_t kPoolCap = (size_t)8 << 30;     // parked bytes above which frees go straight to cudaFree
+
+void *pool_alloc(size_t bytes)
+{
+    int dev = 0;
+    OSCB_CUDA(cudaGetDevice(&dev));
+    bytes = (bytes + 255) & ~(size_t)255;
+    {
+        std::lock_guard<std::mutex> lock(g_pool_mutex);
+        auto it = g_pool.find({dev, bytes});
+        if (it != g_pool.end() && !it->second.empty()) {
+            void *p = it->second.back();
+            it->second.pop_back();
+            g_pool_bytes -= bytes;
+            return p;
+        }
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {            // give the parked blocks back and retry once
+        cudaGetLastError();
+        pool_trim();
+        e = cudaMalloc(&p, bytes);
+    }
+    if (e != cudaSuccess) {
+        set_error("cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+        throw OscbFail{e == cudaErrorMemoryAllocation ? OSCB_ENOMEM : OSCB_ECUDA};
+    }
+    return p;
+}
+
+void pool_free(void *p, size_t bytes)
+{
+    if (!p) return;
+    bytes = (bytes + 255) & ~(size_t)255;
+    cudaPointerAttributes attr;
+    int dev = 0;
+    if (cudaPointerGetAttributes(&attr, p) == cudaSuccess) dev = attr.device;
+    else cudaGetLastError();
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    if (g_pool_bytes + bytes > kPoolCap) {
+        cudaFree(p);
+        return;
+    }
+    g_pool[{dev, bytes}].push_back(p);
+    g_pool_bytes += bytes;
+}
+
+void pool_trim()
+{
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    for (auto &kv : g_pool)
+        for (void *p : kv.second) cudaFree(p);
+    g_pool.clear();
+    g_pool_bytes = 0;
 }
 
 template <typename F> static int guarded(F &&f)
@@ -512,6 +575,14 @@ extern "C" {
 
 const char *oscb_last_error(void) { return g_last_error.c_str(); }
 int oscb_version(void) { return 100; }
+
+int oscb_pool_trim(void)
+{
+    return guarded([&]() -> int {
+        pool_trim();
+        return OSCB_OK;
+    });
+}
 
 int oscb_device_count(int *count)
 {

@@ -37,7 +37,15 @@ struct OscbFail {
         }                                                                                      \
     } while (0)
 
-// device buffer that frees itself; sized in elements of T
+// Size-keyed pool of device blocks: oscb_run allocates a dozen workspaces per call and
+// cudaMalloc / cudaFree cost about a millisecond each (and synchronise the device), which is as
+// much as a whole short integrate window.  Freed blocks are parked per (device, bytes) and handed
+// back to the next request of the same size; oscb_pool_trim() really frees them.
+void *pool_alloc(size_t bytes);
+void pool_free(void *p, size_t bytes);
+void pool_trim();
+
+// device buffer that returns its block to the pool; sized in elements of T
 template <typename T> struct DevBuf {
     T *p = nullptr;
     size_t count = 0;
@@ -54,7 +62,7 @@ template <typename T> struct DevBuf {
     ~DevBuf() { release(); }
     void release()
     {
-        if (p) cudaFree(p);
+        if (p) pool_free(p, count * sizeof(T));
         p = nullptr;
         count = 0;
     }
@@ -62,7 +70,7 @@ template <typename T> struct DevBuf {
     {
         release();
         if (n == 0) n = 1;
-        OSCB_CUDA(cudaMalloc((void **)&p, n * sizeof(T)));
+        p = static_cast<T *>(pool_alloc(n * sizeof(T)));
         count = n;
     }
     void upload(const T *src, size_t n, cudaStream_t s)

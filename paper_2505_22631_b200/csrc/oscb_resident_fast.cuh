@@ -480,12 +480,17 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             const bool valid = iRT < (uint32_t)a.nRT;
             float p[RPL];
             load_phi(iRT, p);                           // issued a whole gather ahead of its use
-            if ((row & 3) == 0 && a.noise_on && valid) {
+            // One Philox block per quad and replica.  Even warps draw it before the quad's first
+            // gather, odd warps after it, so that at any time half of the SM's warps are on the
+            // ALU/MUFU pipes while the other half keep the shared-memory pipe busy.
+            const bool draw = (row & 3) == 0 && a.noise_on && valid;
+            auto draw_noise = [&]() {
 #pragma unroll
                 for (int e = 0; e < RPL; ++e)
                     normals4_fast(philox4x32_10(make_uint4((iRT >> a.LRT) >> 2, (uint32_t)step, (uint32_t)(step >> 32), 0x6F736362u), key[e]),
                                   z[e][0], z[e][1], z[e][2], z[e][3]);
-            }
+            };
+            if (draw && !(warp & 1)) draw_noise();
             float2 sum[RPL];
             int neg[RPL];
 #pragma unroll
@@ -528,6 +533,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     pk = nx;
                 }
             }
+            if (draw && (warp & 1)) draw_noise();
             if (valid) {
                 const PairPack<RPL> own = pairs_at(iRT);
                 const uint32_t k = (iRT >> a.LRT) & 3u;
