@@ -100,7 +100,8 @@ struct FastArgs {
     const int *warp_start;             // [W]
     const uint16_t *rows;              // [W * n_rows * C] own row * RT (>= nRT: none)
     const uint32_t *ginfo;             // [W * rounds]
-    const uint16_t *deg;               // [W * n_rows * C]
+    const uint16_t *deg;               // [W * n_rows * C]  row degrees (unit weights)
+    const float *rowsum;               // [W * n_rows * C]  row weight sums (integer-valued weights)
     const uint2 *stream;               // [(n_group_rows + 1) * C]
     const float *wstream;              // [(n_group_rows + 1) * C * 4]
     float *phi;                        // [tiles][n][RT] (+ one padding row at the very end)
@@ -220,7 +221,7 @@ template <int NMODE, bool WEIGHTED, bool IDX_SMEM, bool PHI_SMEM, int RPL>
 __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr bool PIGGY = NMODE == 2 && !WEIGHTED;
+    constexpr bool PIGGY = NMODE == 2;    // max-cut with integer couplings: score during the next gather
     const int tid = threadIdx.x, NT = blockDim.x;
     const uint32_t smem32 = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const int lane = tid & 31, warp = tid >> 5;
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     const uint32_t rows32 = smem32 + a.off_rows + ((warp * a.n_rows) * a.C + c) * 2;   // own rows, stride C*2
     const uint32_t g32 = smem32 + a.off_g + warp * a.n_rows;                           // G per row position
     const uint16_t *deg_lane = (a.deg_smem ? reinterpret_cast<const uint16_t *>(smem_raw + a.off_deg) : a.deg) + (warp * a.n_rows) * a.C + c;
+    const float *rowsum_lane = a.rowsum + (warp * a.n_rows) * a.C + c;
     double *part = reinterpret_cast<double *>(smem_raw + a.off_part);
     double *best_s = reinterpret_cast<double *>(smem_raw + a.off_misc);
     int *improved_s = reinterpret_cast<int *>(smem_raw + a.off_misc + a.RT * 8);
@@ -448,9 +450,10 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         const bool is_sample = sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] == step;
         const bool cadence_hit = a.cadence > 0 && step % a.cadence == 0;
         const bool count_now = PIGGY && pending;
-        int twice_cut[RPL];
+        int twice_cut[RPL];            // unit weights: exact integer count
+        float twice_cut_w[RPL];        // integer-valued weights: exact in float32 below 2^24
 #pragma unroll
-        for (int e = 0; e < RPL; ++e) twice_cut[e] = 0;
+        for (int e = 0; e < RPL; ++e) { twice_cut[e] = 0; twice_cut_w[e] = 0.f; }
 
         // pass A ------------------------------------------------------------------------------
         // The stream of a warp is contiguous: a running pointer walks it and the next group is
@@ -493,8 +496,9 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             if (draw && !(warp & 1)) draw_noise();
             float2 sum[RPL];
             int neg[RPL];
+            float negw[RPL];
 #pragma unroll
-            for (int e = 0; e < RPL; ++e) { sum[e] = make_float2(0.f, 0.f); neg[e] = 0; }
+            for (int e = 0; e < RPL; ++e) { sum[e] = make_float2(0.f, 0.f); neg[e] = 0; negw[e] = 0.f; }
             if (PIGGY && count_now) {
                 // scoring step: the sign bit of every gathered cosine is the neighbour's lattice state
 #pragma unroll 1
@@ -502,11 +506,24 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     const uint2 nx = next_group();
                     const PairPack<RPL> v0 = pairs_at(pk.x & 0xffffu), v1 = pairs_at(pk.x >> 16);
                     const PairPack<RPL> v2 = pairs_at(pk.y & 0xffffu), v3 = pairs_at(pk.y >> 16);
+                    if (WEIGHTED) {
+                        const float4 w4 = next_weights();
 #pragma unroll
-                    for (int e = 0; e < RPL; ++e) {
-                        sum[e] = __fadd2_rn(sum[e], __fadd2_rn(__fadd2_rn(v0.v[e], v1.v[e]), __fadd2_rn(v2.v[e], v3.v[e])));
-                        neg[e] += (int)(__float_as_uint(v0.v[e].x) >> 31) + (int)(__float_as_uint(v1.v[e].x) >> 31);
-                        neg[e] += (int)(__float_as_uint(v2.v[e].x) >> 31) + (int)(__float_as_uint(v3.v[e].x) >> 31);
+                        for (int e = 0; e < RPL; ++e) {
+                            sum[e] = __ffma2_rn(make_float2(w4.x, w4.x), v0.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.y, w4.y), v1.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.z, w4.z), v2.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.w, w4.w), v3.v[e], sum[e]);
+                            negw[e] += (v0.v[e].x < 0.f ? w4.x : 0.f) + (v1.v[e].x < 0.f ? w4.y : 0.f);
+                            negw[e] += (v2.v[e].x < 0.f ? w4.z : 0.f) + (v3.v[e].x < 0.f ? w4.w : 0.f);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < RPL; ++e) {
+                            sum[e] = __fadd2_rn(sum[e], __fadd2_rn(__fadd2_rn(v0.v[e], v1.v[e]), __fadd2_rn(v2.v[e], v3.v[e])));
+                            neg[e] += (int)(__float_as_uint(v0.v[e].x) >> 31) + (int)(__float_as_uint(v1.v[e].x) >> 31);
+                            neg[e] += (int)(__float_as_uint(v2.v[e].x) >> 31) + (int)(__float_as_uint(v3.v[e].x) >> 31);
+                        }
                     }
                     pk = nx;
                 }
@@ -538,13 +555,19 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                 const PairPack<RPL> own = pairs_at(iRT);
                 const uint32_t k = (iRT >> a.LRT) & 3u;
                 int deg = 0;
-                if (PIGGY && count_now) deg = (int)deg_lane[row * a.C];
+                float wrow = 0.f;
+                if (PIGGY && count_now) {
+                    if (WEIGHTED) wrow = rowsum_lane[row * a.C];
+                    else deg = (int)deg_lane[row * a.C];
+                }
                 float y[RPL];
 #pragma unroll
                 for (int e = 0; e < RPL; ++e) {
                     const float ci = own.v[e].x, si = own.v[e].y;
-                    if (PIGGY && count_now)   // differing neighbours: deg - neg if the row itself is in state 1
-                        twice_cut[e] += (ci < 0.f) ? deg - neg[e] : neg[e];
+                    if (PIGGY && count_now) {   // differing neighbours: deg - neg if the row itself is in state 1
+                        if (WEIGHTED) twice_cut_w[e] += (ci < 0.f) ? wrow - negw[e] : negw[e];
+                        else twice_cut[e] += (ci < 0.f) ? deg - neg[e] : neg[e];
+                    }
                     const float acc = si * sum[e].x - ci * sum[e].y;
                     float shil;
                     if (NMODE == 2) shil = si * ci;                              // hks holds 2 h ks
@@ -574,7 +597,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             // `twice_cut` counted the state after step `pending_label`; cs still holds that state
             double tc[RPL];
 #pragma unroll
-            for (int e = 0; e < RPL; ++e) tc[e] = (double)twice_cut[e];
+            for (int e = 0; e < RPL; ++e) tc[e] = WEIGHTED ? (double)twice_cut_w[e] : (double)twice_cut[e];
             const double obj = 0.5 * tile_reduce_rpl<RPL>(tc, a.RT, a.LPS, part, tid, a.W);
             if (tid < a.RT) record_best(obj, pending_label);
             __syncthreads();

@@ -22,8 +22,10 @@ struct ResidentPlan {
     bool weighted = false;
     double fill = 1.0;          // real neighbours / stream entries
     double bank_conflicts = 0;  // stream positions whose slots collide on a bank class / all positions
+    bool exact_f32_cut = false; // integer couplings small enough that float32 sums of them stay exact
     DevBuf<int> warp_start;
     DevBuf<uint16_t> rows, deg;
+    DevBuf<float> rowsum;
     DevBuf<uint32_t> ginfo;
     DevBuf<uint2> stream;
     DevBuf<float> w32;
@@ -48,6 +50,8 @@ struct ResidentStreamHost {
     std::vector<int> warp_start;
     std::vector<uint16_t> rows;     // [W*T*4*C] own row * RT, n*RT when the slot has none
     std::vector<uint16_t> deg;      // [W*T*4*C] real degree of that row
+    std::vector<float> rowsum;      // [W*T*4*C] sum of that row's couplings
+    double max_abs_rowsum = 0.0;
     std::vector<uint32_t> ginfo;    // [W*T]
     std::vector<uint2> stream;      // [(n_group_rows + 1) * C] ids * RT; >= n*RT: zero padding rows
     std::vector<double> weights;    // [(n_group_rows + 1) * C * 4]
@@ -116,6 +120,8 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
     out->warp_start.assign(W, 0);
     out->rows.assign((size_t)W * T * 4 * C, (uint16_t)(n * RT));
     out->deg.assign((size_t)W * T * 4 * C, 0);
+    out->rowsum.assign((size_t)W * T * 4 * C, 0.f);
+    out->max_abs_rowsum = 0.0;
     out->ginfo.assign((size_t)W * T, 0);
     out->stream.clear();
     out->weights.clear();
@@ -151,6 +157,10 @@ static void compile_resident_stream(int n, const int *indptr, const int *indices
                     if (i >= 0) {
                         out->rows[at] = (uint16_t)(i * RT);
                         out->deg[at] = (uint16_t)deg(i);
+                        double rs = 0.0, ra = 0.0;
+                        for (int e = indptr[i]; e < indptr[i + 1]; ++e) { rs += wts ? wts[e] : 1.0; ra += std::fabs(wts ? wts[e] : 1.0); }
+                        out->rowsum[at] = (float)rs;
+                        out->max_abs_rowsum = std::max(out->max_abs_rowsum, ra);
                     }
                 }
                 for (int c0 = 0; c0 < C; c0 += H) {
@@ -257,6 +267,8 @@ static std::shared_ptr<ResidentPlan> build_resident_plan(oscb_graph *g, int RT, 
     plan->warp_start.alloc(W);                plan->warp_start.upload(h.warp_start.data(), W, s);
     plan->rows.alloc(h.rows.size());          plan->rows.upload(h.rows.data(), h.rows.size(), s);
     plan->deg.alloc(h.deg.size());            plan->deg.upload(h.deg.data(), h.deg.size(), s);
+    plan->rowsum.alloc(h.rowsum.size());      plan->rowsum.upload(h.rowsum.data(), h.rowsum.size(), s);
+    plan->exact_f32_cut = g->int_weights && h.max_abs_rowsum * (double)g->n < 16777216.0;
     plan->ginfo.alloc(h.ginfo.size());        plan->ginfo.upload(h.ginfo.data(), h.ginfo.size(), s);
     plan->stream.alloc(h.stream.size());      plan->stream.upload(h.stream.data(), h.stream.size(), s);
     std::vector<float> wf(h.weights.begin(), h.weights.end());
@@ -381,12 +393,13 @@ struct FastFit {
     FastSmem lay;
     size_t smem = 0;
 };
-static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT, int C, int W, int T, int n_group_rows)
+static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT, int C, int W, int T, int n_group_rows,
+                        bool exact_f32_cut)
 {
     const bool weighted = !g->unit_weights;
     FastFit f;
     f.states = n_states != 2;
-    f.piggy = n_states == 2 && !weighted && objective == OSCB_OBJ_MAXCUT;
+    f.piggy = n_states == 2 && objective == OSCB_OBJ_MAXCUT && (!weighted || exact_f32_cut);
     auto lay = [&](bool phi, bool idx) {
         return FastSmem::make((int)g->n, RT, C, T, W, n_group_rows, f.states, f.deg_smem, phi, idx, weighted);
     };
@@ -397,7 +410,7 @@ static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT
     // and goes to shared memory last.
     if (lay(false, true).total <= cap) f.idx_smem = true;
     if (f.idx_smem && lay(true, true).total <= cap) f.phi_smem = true;
-    if (f.piggy) {
+    if (f.piggy && !weighted) {
         f.deg_smem = true;
         if (lay(f.phi_smem, f.idx_smem).total > cap) f.deg_smem = false;
     }
@@ -427,7 +440,8 @@ static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const Re
     a.initial_sample = ra.initial_sample; a.n_sample_steps = ra.n_sample_steps; a.sample_offset = ra.sample_offset;
     a.step_begin = ra.step_begin; a.step_end = ra.step_end; a.cadence = ra.cadence; a.trace_stride = ra.trace_stride;
     a.target = ra.target;
-    a.warp_start = ra.warp_start; a.rows = ra.rows; a.ginfo = ra.ginfo; a.deg = plan.deg.p; a.stream = ra.stream;
+    a.warp_start = ra.warp_start; a.rows = ra.rows; a.ginfo = ra.ginfo; a.deg = plan.deg.p; a.rowsum = plan.rowsum.p;
+    a.stream = ra.stream;
     a.wstream = reinterpret_cast<const float *>(ra.wstream);
     a.phi = reinterpret_cast<float *>(ra.phi); a.seeds = ra.seeds; a.sample_steps = ra.sample_steps;
     a.cs_next = cs_next;
@@ -471,7 +485,7 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     }
     FastFit fast;
     if (FAST) {
-        fast = fit_fast(g, p->n_states, p->objective, RT, plan->C, plan->W, plan->T, plan->n_group_rows);
+        fast = fit_fast(g, p->n_states, p->objective, RT, plan->C, plan->W, plan->T, plan->n_group_rows, plan->exact_f32_cut);
         smem = fast.smem;
     }
     OSCB_REQUIRE(smem <= (size_t)g->smem_optin, "resident kernel does not fit in shared memory (%zu bytes)", smem);
