@@ -56,6 +56,7 @@ extern "C" {
 #define OSCB_KERNEL_AUTO 0
 #define OSCB_KERNEL_STREAM 1   /* one launch per step, phases in HBM/L2                   */
 #define OSCB_KERNEL_RESIDENT 2 /* persistent CTA per replica tile, phases' (cos,sin) in smem */
+#define OSCB_KERNEL_DENSE_TC 3 /* dense integer J: persistent tcgen05 int8 GEMM J*[cos|sin] digit planes */
 
 typedef struct oscb_graph oscb_graph;
 

@@ -23,8 +23,8 @@ OK, EINVAL, ECUDA, ENONFINITE, ENOMEM = 0, 1, 2, 3, 4
 OBJ = {"maxcut": 0, "coloring": 1}
 PREC = {"f32": 32, "f64": 64}
 NOISE_DEVICE, NOISE_HOST, NOISE_NONE = 0, 1, 2
-KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2}
-KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident"}
+KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2, "dense-tc": 3}
+KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident", 3: "dense-tc"}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC"]
@@ -103,14 +103,45 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     newest = max(p.stat().st_mtime for p in sources())
     if not force and LIB_PATH.exists() and LIB_PATH.stat().st_mtime >= newest:
         return LIB_PATH
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", str(LIB_PATH), str(CSRC / "oscb.cu")]
+    # one object per translation unit (compiled in parallel, rebuilt only when stale), then one link
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = PKG_DIR / "build"
+    objdir.mkdir(exist_ok=True)
+    units = sorted(CSRC.glob("*.cu"))
+
+    def deps(src, seen=None):
+        """`src` plus the local headers it includes, transitively."""
+        import re
+        seen = set() if seen is None else seen
+        if src in seen or not src.exists():
+            return seen
+        seen.add(src)
+        for inc in re.findall(r'#include\s+"([^"]+)"', src.read_text()):
+            deps((src.parent / inc).resolve(), seen)
+        return seen
+
+    def compile_unit(src):
+        obj = objdir / (src.stem + ".o")
+        stamp = max(p.stat().st_mtime for p in deps(src))
+        if not force and obj.exists() and obj.stat().st_mtime >= stamp:
+            return obj, ""
+        cmd = ["nvcc", *[f for f in NVCC_FLAGS if f != "-shared"], "-c", "-o", str(obj), str(src)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stdout}\n{res.stderr}")
+        return obj, res.stderr
+
+    with ThreadPoolExecutor(max_workers=len(units)) as ex:
+        results = list(ex.map(compile_unit, units))
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+        for _, log in results:
+            print(log)
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", str(LIB_PATH), *[str(o) for o, _ in results]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stdout}\n{res.stderr}")
-    if verbose:
-        print(res.stderr)
+        raise RuntimeError(f"nvcc link failed:\n{res.stdout}\n{res.stderr}")
     return LIB_PATH
 
 

@@ -12,6 +12,7 @@
 #include "oscb_stream.cuh"
 #include "oscb_resident_host.hpp"
 #include "oscb_dense_host.hpp"
+#include "oscb_umma.hpp"
 #include <type_traits>
 
 #include <algorithm>
@@ -502,6 +503,116 @@ static void run_stream(oscb_graph *g, const oscb_run_params *p, const RunPlan &r
     }
 }
 
+// ------------------------------------------------------------------------------------------
+// the integrate loop of a dense integer-coupled max-cut graph on the tensor cores
+// (oscb_umma.cuh): one persistent launch per chunk of <= 28 replicas
+static bool umma_applies(const oscb_graph *g, const oscb_run_params *p)
+{
+    return g->is_dense && g->umma && p->n_states == 2 && p->objective == OSCB_OBJ_MAXCUT &&
+           p->noise_mode != OSCB_NOISE_HOST && p->kernel != OSCB_KERNEL_STREAM;
+}
+
+static void run_umma(oscb_graph *g, const oscb_run_params *p, const RunPlan &rp, const uint64_t *seeds, int64_t R64,
+                     const double *phi0, oscb_run_outputs *out)
+{
+    cudaStream_t s = g->stream;
+    const int R = (int)R64, n = (int)g->n;
+    const size_t tot = (size_t)n * R;
+    const int64_t S = rp.n_samples, steps = rp.steps;
+    // pass q integrates step q and first scores the phases it starts from (= after step q - 1)
+    std::vector<uint8_t> flags((size_t)steps + 1, 0);
+    std::vector<long long> event_step;          // step label of every scored pass (-1: initial sample)
+    std::vector<long long> sample_event;        // event index of every sample
+    flags[0] = 3;
+    {
+        size_t next_sample = 0;
+        event_step.push_back(-1);
+        sample_event.push_back(0);
+        for (int64_t step = 0; step < steps; ++step) {
+            const int64_t gstep = p->first_step + step;
+            if (next_sample < rp.sample_steps.size() && rp.sample_steps[next_sample] == step) {
+                flags[(size_t)step + 1] = 3;
+                sample_event.push_back((long long)event_step.size());
+                event_step.push_back(gstep);
+                ++next_sample;
+            } else if (rp.cadence > 0 && gstep % rp.cadence == 0) {
+                flags[(size_t)step + 1] = 1;
+                event_step.push_back(gstep);
+            }
+        }
+    }
+    const long long E = (long long)event_step.size();
+    DevBuf<double> io(tot);
+    DevBuf<uint64_t> d_seeds(R);
+    d_seeds.upload(seeds, R, s);
+    if (phi0) io.upload(phi0, tot, s);
+    else k_initial_phases<<<blocks_for((long long)((n + 3) / 4) * R, 128), 128, 0, s>>>(d_seeds.p, io.p, n, R);
+    DevBuf<double> d_final(tot);
+    std::vector<uint8_t> h_states;
+    if (out->best_states) h_states.resize(tot);
+    double ms = 0.0;
+    int64_t launches = 0;
+    unsigned long long flag = ~0ull;
+    UmmaSpec last{};
+    for (int r0 = 0; r0 < R; r0 += kUmmaMaxReplicas) {
+        const int Rc = std::min(kUmmaMaxReplicas, R - r0);
+        std::vector<long long> ev((size_t)E * Rc);
+        std::vector<double> en((size_t)S * Rc);
+        UmmaSpec sp{};
+        sp.R = Rc;
+        sp.precision = p->precision;
+        sp.noise_on = (p->noise_mode == OSCB_NOISE_DEVICE && p->kn != 0.0) ? 1 : 0;
+        sp.K = p->K; sp.h = p->h; sp.kn_sqrt_h = p->kn * std::sqrt(p->h); sp.ks_max = p->ks_max; sp.ks_period = p->ks_period;
+        sp.steps = steps; sp.first_step = p->first_step;
+        sp.flags = flags.data();
+        sp.n_events = E; sp.n_samples = S;
+        sp.seeds = seeds + r0;
+        sp.d_phi0 = io.p + (size_t)r0 * n;
+        sp.d_final = d_final.p + (size_t)r0 * n;
+        sp.h_best_states = out->best_states ? h_states.data() + (size_t)r0 * n : nullptr;
+        sp.h_events = ev.data();
+        sp.h_energy = en.data();
+        umma_run(g, *g->umma, sp);
+        ms += sp.ms;
+        launches += 1;
+        flag = std::min(flag, sp.nonfinite == ~0ull ? ~0ull : sp.nonfinite + ((unsigned long long)r0 << 20));
+        last = sp;
+        for (int r = 0; r < Rc; ++r) {
+            double best = -std::numeric_limits<double>::infinity();
+            long long first = -1;
+            size_t k = 0;
+            for (long long e = 0; e < E; ++e) {
+                const double obj = 0.5 * (double)ev[(size_t)e * Rc + r];
+                if (obj > best) {
+                    best = obj;
+                    if (p->use_target && first < 0 && obj >= p->target_objective) first = event_step[(size_t)e];
+                }
+                if (k < sample_event.size() && sample_event[k] == e) {
+                    if (out->best_trace) out->best_trace[(size_t)(r0 + r) * out->max_samples + k] = best;
+                    if (out->energy) out->energy[(size_t)(r0 + r) * out->max_samples + k] = en[k * Rc + r];
+                    ++k;
+                }
+            }
+            if (out->best_objective) out->best_objective[r0 + r] = best;
+            if (out->first_hit_step) out->first_hit_step[r0 + r] = first;
+        }
+    }
+    if (out->final_phases) d_final.download(out->final_phases, tot, s);
+    OSCB_CUDA(cudaStreamSynchronize(s));
+    if (out->best_states) std::memcpy(out->best_states, h_states.data(), tot);
+    out->device_ms = ms;
+    out->kernel_launches = launches;
+    out->kernel_used = OSCB_KERNEL_DENSE_TC;
+    out->replicas_per_cta = std::min(R, kUmmaMaxReplicas);
+    out->smem_bytes = (int64_t)last.smem;
+    if (flag != ~0ull) {
+        decode_nonfinite(flag, out->nonfinite);
+        set_error("non-finite phase for oscillator %lld (replica row %lld) after step %lld; parameters are numerically unstable",
+                  (long long)out->nonfinite[1], (long long)out->nonfinite[0], (long long)out->nonfinite[2]);
+        throw OscbFail{OSCB_ENONFINITE};
+    }
+}
+
 // workspace of the row-sharded dense driver: pairs and states of all n oscillators, row partials
 struct ShardWork {
     int R = 0, precision = 0;
@@ -653,6 +764,9 @@ int oscb_graph_create_dense(int device, int64_t n, const double *J, int64_t row_
         g->row_end = row_end;
         // J holds rows [row_begin, row_end) of the full matrix, row-major, n columns each
         build_dense(g.get(), J);
+        // integer couplings on 128-row aligned shards also get the tile images of the tensor-core kernel
+        if (g->dense->kind == DENSE_I8 && row_begin % 128 == 0 && (row_end % 128 == 0 || row_end == n))
+            g->umma = umma_build_plan(g->dense->J8.p, n, g->dense->n_pad, row_begin, row_end, g->stream);
         *out = g.release();
         return OSCB_OK;
     });
@@ -667,6 +781,7 @@ int oscb_graph_destroy(oscb_graph *g)
     }
     g->plans.clear();
     g->dense.reset();
+    g->umma.reset();
     g->shard_work.reset();
     cudaStream_t s = g->stream;
     delete g;
@@ -984,7 +1099,13 @@ int oscb_run(oscb_graph *g, const oscb_run_params *p, const uint64_t *seeds, int
 
         int kernel = p->kernel;
         if (g->is_dense) {
-            OSCB_REQUIRE(kernel != OSCB_KERNEL_RESIDENT, "dense couplings run on the streaming loop (no resident kernel)");
+            OSCB_REQUIRE(kernel != OSCB_KERNEL_RESIDENT, "dense couplings run on the streaming loop or the tensor-core kernel (no resident kernel)");
+            OSCB_REQUIRE(kernel != OSCB_KERNEL_DENSE_TC || umma_applies(g, p),
+                         "the tensor-core dense kernel needs integer couplings |J| <= 127, N = 2 max-cut and device noise");
+            if (umma_applies(g, p)) {
+                run_umma(g, p, rp, seeds, R, phi0, out);
+                return OSCB_OK;
+            }
             kernel = OSCB_KERNEL_STREAM;
         }
         if (kernel == OSCB_KERNEL_AUTO)

@@ -87,6 +87,7 @@ template <typename T> struct DevBuf {
 struct ResidentPlan; // oscb_resident_host.hpp
 struct DensePlan;    // oscb_dense_host.hpp
 struct ShardWork;    // oscb.cu: workspace of the row-sharded dense driver
+struct UmmaPlan;     // oscb_umma.hpp: tile images of J for the tensor-core dense kernel
 
 } // namespace oscb
 
@@ -114,4 +115,5 @@ struct oscb_graph {
     std::map<uint64_t, std::shared_ptr<oscb::ResidentPlan>> plans;
     std::shared_ptr<oscb::DensePlan> dense;
     std::shared_ptr<oscb::ShardWork> shard_work;
+    std::shared_ptr<oscb::UmmaPlan> umma;
 };

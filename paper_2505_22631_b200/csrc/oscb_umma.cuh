@@ -1,0 +1,500 @@
+// oscb_umma.cuh -- the dense (all-to-all, integer couplings) integrator on the 5th-generation
+// tensor cores: ONE persistent kernel runs every Euler step of a run.
+//
+//   J * [cos Theta | sin Theta]  as an exact integer GEMM
+//     A = J                    int8 [rows x n]        (SK couplings are +-1; any integer |J| <= 127)
+//     B = digit planes of the (cos, sin) pairs:  c = 2^-30 * sum_k 2^(8k) d_k,  d_k signed bytes,
+//         i.e. 4 int8 planes per component, plus one plane of spins sigma = +-1 for the cut
+//     D = A * B^T              int32 in TMEM, tcgen05.mma kind::i8 (UTCIMMA), M = 128, K = 32
+//   Integer accumulation is exact and order independent, so the coupling sums carry only the
+//   2^-31 quantisation of each pair -- tighter than a float32 FMA chain over n = 16384 terms.
+//
+// Roles of the 192 threads of a CTA (one CTA per SM, one 128-row tile of J at a time):
+//   warp 0   producer: cp.async.bulk (UBLKCP) of the 16 KB tile images of A (HBM stream) and
+//            of B (L2 resident) into a ring of shared-memory stages, signalled on mbarriers;
+//   warp 1   one elected lane issues the tcgen05.mma instructions and commits them;
+//   warps 2-5 epilogue: tcgen05.ld of their 32 TMEM lanes, then per (row, replica) the fused
+//            Euler update (SHIL, Philox noise, schedule, wrap; dynamics.py:166-172), the new
+//            (cos, sin) digits written straight into the NEXT step's B image on every rank
+//            (peer pointers: the push all-gather of the row-sharded multi-GPU run), the cut
+//            contribution from the sigma plane (dynamics.py:214-223) and the sample energy
+//            (dynamics.py:380).
+// Steps are separated by one grid-wide (all ranks) arrive/wait on a monotonic counter; only the
+// producer waits on it, and it prefetches the next step's A tiles first, so the HBM stream of J
+// does not stop at a step boundary.
+//
+// Tile images: A and B live in global memory already in the 128-byte-swizzled K-major layout
+// the UMMA shared-memory descriptor expects (byte (r, c) of a [rows x 128 B] tile at
+// r*128 + ((c/16 ^ r%8)*16) + c%16), so a stage is filled by two plain bulk copies.
+#pragma once
+#include "oscb_device.cuh"
+#include <limits.h>
+
+namespace oscb {
+
+constexpr int UMMA_MAXW = 8;          // ranks a row-sharded run may span
+constexpr int UMMA_TILE = 128;        // rows per tile = bytes of K per stage
+constexpr int UMMA_A_STAGE = UMMA_TILE * UMMA_TILE;
+constexpr int UMMA_THREADS = 192;
+constexpr int UMMA_MAXR = 28;         // 9 B rows per replica, N <= 256
+
+struct UmmaArgs {
+    int n;                    // oscillators
+    int tiles;                // ceil(n / 128): row tiles of the whole graph = k-blocks
+    int tile_begin, tile_end; // this rank's row tiles
+    int R;                    // replicas (<= UMMA_MAXR)
+    int NB;                   // rows of B: round_up(9 R, 16) -- the MMA N
+    int stages;
+    int world, rank;
+    int tmem_cols;
+    unsigned int ctas_total;  // CTAs of all ranks (grid barrier target per pass)
+    int cta_offset;           // global index of this rank's CTA 0 (energy partials)
+    long long passes;         // steps + 1 (the last pass only scores)
+    long long first_step;
+    double K, h, kn_sqrt_h, ks_max, ks_period;
+    TrigConst tc;
+    int noise_on;
+    long long ld_phi;         // leading dimension of phi / best_states: local rows padded to tiles
+    const uint8_t *A_img;     // [local tiles][tiles][16384]
+    uint8_t *B_img[2][UMMA_MAXW];  // per buffer and rank: [tiles][NB * 128]
+    void *phi[2];             // [R][ld_phi] in T
+    const int *W;             // [local rows] row sums of J
+    const uint64_t *seeds;    // [R]
+    const uint8_t *flags;     // [passes] bit 0: score the pass's input phases, bit 1: + energy sample
+    unsigned int *bar[UMMA_MAXW];      // monotonic arrival counters, one per rank
+    long long *events[UMMA_MAXW];      // [n_events][R]: sum_i sum_j J_ij [s_i != s_j] = 2 * cut
+    double *en_part[UMMA_MAXW];        // [n_samples][ctas_total][R]
+    uint8_t *best_states;     // [R][ld_phi]
+    unsigned long long *nonfinite;
+};
+
+namespace umma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity)
+{
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate)
+{
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
+                 ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, int &v)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int threads)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+
+// K-major, 128-byte swizzle, rows of 128 bytes, 8-row groups 1024 bytes apart (SM100 descriptor
+// version 1).  Advancing K by 32 bytes inside the swizzle atom adds 2 to the start-address field.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr)
+{
+    return (uint64_t)((addr >> 4) & 0x3FFFu) | (1ull << 16) | (64ull << 32) | (1ull << 46) | (2ull << 61);
+}
+// D = int32, A = B = signed 8-bit, both K-major, M = 128, N = nb
+__host__ __device__ inline uint32_t instr_desc_i8(int nb)
+{
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(UMMA_TILE >> 4) << 24);
+}
+
+// byte offset of (row r, k-byte c) inside a swizzled [rows x 128 B] tile image
+__host__ __device__ inline uint32_t swz(uint32_t r, uint32_t c)
+{
+    return (r >> 3) * 1024u + (r & 7u) * 128u + ((((c >> 4) ^ (r & 7u)) << 4) | (c & 15u));
+}
+
+// c in [-1, 1] -> round(c 2^30) as four signed base-256 digits (d0 least significant)
+template <typename T> __device__ __forceinline__ void pair_digits(T v, int (&d)[4])
+{
+    int q = (sizeof(T) == 8) ? __double2int_rn((double)v * 1073741824.0) : __float2int_rn((float)v * 1073741824.0f);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int lo = ((q & 0xFF) ^ 0x80) - 0x80;
+        d[k] = lo;
+        q = (q - lo) >> 8;
+    }
+    d[3] = q;
+}
+__device__ __forceinline__ long long digits_sum(const int *D)
+{
+    return (long long)D[0] + ((long long)D[1] << 8) + ((long long)D[2] << 16) + ((long long)D[3] << 24);
+}
+
+// write the 8 digit bytes and the spin of oscillator (tile kb, column c) for replica r into one B image
+template <typename T>
+__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state)
+{
+    uint8_t *base = Bimg + (size_t)kb * NB * 128;
+    int dc[4], ds[4];
+    pair_digits<T>(cv, dc);
+    pair_digits<T>(sv, ds);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        base[swz(8 * r + k, c)] = (uint8_t)dc[k];
+        base[swz(8 * r + 4 + k, c)] = (uint8_t)ds[k];
+    }
+    base[swz(8 * R + r, c)] = (uint8_t)(state ? -1 : 1);
+}
+
+__device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p, bool sys)
+{
+    unsigned int v;
+    if (sys) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release(unsigned int *p, bool sys)
+{
+    if (sys) asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+    else asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+} // namespace umma
+
+// phases [R][n] float64 (host layout) -> this rank's rows in T, plus the B image of ALL n
+// oscillators for pass 0 (every rank builds the full image locally).
+template <typename T>
+__global__ void k_umma_init(UmmaArgs a, const double *__restrict__ phi0)
+{
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)a.n * a.R) return;
+    const int r = (int)(q / a.n), j = (int)(q % a.n);
+    const T p = (T)phi0[q];
+    T s, c;
+    phase_trig(p, s, c);
+    umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, threshold_state((double)p, 2));
+    const int row0 = a.tile_begin * UMMA_TILE, row1 = a.tile_end * UMMA_TILE;
+    if (j >= row0 && j < row1) reinterpret_cast<T *>(a.phi[0])[(long long)r * a.ld_phi + (j - row0)] = p;
+}
+
+// this rank's rows back to the host layout [R][n] (only the local columns are written)
+template <typename T>
+__global__ void k_umma_export(UmmaArgs a, const void *phi, double *__restrict__ out)
+{
+    const int rows = min(a.n, a.tile_end * UMMA_TILE) - a.tile_begin * UMMA_TILE;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (long long)rows * a.R) return;
+    const int r = (int)(q / rows), i = (int)(q % rows);
+    out[(long long)r * a.n + a.tile_begin * UMMA_TILE + i] = (double)reinterpret_cast<const T *>(phi)[(long long)r * a.ld_phi + i];
+}
+
+// int8 J rows [rows][n_pad] -> swizzled tile images + row sums
+__global__ void k_umma_build_a(const int8_t *__restrict__ J, int n, int n_pad, int rows, int tiles, uint8_t *__restrict__ A_img,
+                               int *__restrict__ W)
+{
+    // one CTA per (local tile, k-block); 256 threads move 16 KB
+    const int lt = blockIdx.y, kb = blockIdx.x;
+    uint8_t *img = A_img + ((size_t)lt * tiles + kb) * UMMA_A_STAGE;
+    for (int q = threadIdx.x; q < UMMA_A_STAGE / 4; q += blockDim.x) {
+        const int r = q / 32, c = (q % 32) * 4;
+        const int row = lt * UMMA_TILE + r, col = kb * UMMA_TILE + c;
+        uint32_t v = 0;
+        if (row < rows && col < n_pad) v = *reinterpret_cast<const uint32_t *>(J + (size_t)row * n_pad + col); // n_pad % 4 == 0, zero padded
+        *reinterpret_cast<uint32_t *>(img + umma::swz(r, c)) = v;
+    }
+    if (kb == 0) {
+        for (int r = threadIdx.x; r < UMMA_TILE; r += blockDim.x) {
+            const int row = lt * UMMA_TILE + r;
+            int s = 0;
+            if (row < rows)
+                for (int j = 0; j < n; ++j) s += J[(size_t)row * n_pad + j];
+            W[lt * UMMA_TILE + r] = s;
+        }
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a)
+{
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = umma::smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *smem = smem_raw + (base - raw);
+    const int stages = a.stages;
+    const uint32_t b_stage = (uint32_t)a.NB * 128u;
+    const uint32_t sA = base, sB = base + (uint32_t)stages * UMMA_A_STAGE;
+    uint8_t *ctl = smem + (size_t)stages * (UMMA_A_STAGE + b_stage);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ctl);            // full[stages], empty[stages], tmem_full, tmem_empty
+    const uint32_t bar_full = umma::smem_u32(bars), bar_empty = bar_full + 8u * stages;
+    const uint32_t bar_tfull = bar_empty + 8u * stages, bar_tempty = bar_tfull + 8u;
+    long long *best_s = reinterpret_cast<long long *>(ctl + 8 * (2 * 16 + 2));   // [32]
+    double *en_acc = reinterpret_cast<double *>(best_s + 32);                    // [32]
+    double *en_w = en_acc + 32;                                                  // [4][32]
+    int *improved_s = reinterpret_cast<int *>(en_w + 128);                       // [32]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(improved_s + 32);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool sys = a.world > 1;
+    const int my_tiles = (a.tile_end - a.tile_begin - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const long long per_pass = (long long)my_tiles * a.tiles;
+    const uint32_t stage_tx = UMMA_A_STAGE + b_stage;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) { umma::mbar_init(bar_full + 8u * s, 1); umma::mbar_init(bar_empty + 8u * s, 1); }
+        umma::mbar_init(bar_tfull, 1);
+        umma::mbar_init(bar_tempty, 4);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(umma::smem_u32(tmem_slot)), "r"(a.tmem_cols) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x >= 64 && threadIdx.x - 64 < 32) {
+        best_s[threadIdx.x - 64] = LLONG_MIN;
+        en_acc[threadIdx.x - 64] = 0.0;
+        improved_s[threadIdx.x - 64] = 0;
+    }
+    umma::tc_fence_before();
+    __syncthreads();
+    umma::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== producer =====
+        if (lane == 0) {
+            long long it = 0;
+            auto coords = [&](long long q, int &lt, int &kb) {
+                const int tk = (int)(q / a.tiles);
+                kb = (int)(q % a.tiles);
+                lt = (int)blockIdx.x + tk * (int)gridDim.x;
+            };
+            auto issue_a = [&](long long gi, long long q) {
+                const int s = (int)(gi % stages);
+                umma::mbar_wait(bar_empty + 8u * s, (uint32_t)(((gi / stages) & 1) ^ 1));
+                umma::mbar_expect_tx(bar_full + 8u * s, stage_tx);
+                int lt, kb;
+                coords(q, lt, kb);
+                umma::bulk_g2s(sA + (uint32_t)s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + kb) * UMMA_A_STAGE, UMMA_A_STAGE,
+                               bar_full + 8u * s);
+            };
+            auto issue_b = [&](long long gi, long long q, int buf) {
+                const int s = (int)(gi % stages);
+                int lt, kb;
+                coords(q, lt, kb);
+                umma::bulk_g2s(sB + (uint32_t)s * b_stage, a.B_img[buf][a.rank] + (size_t)kb * b_stage, b_stage, bar_full + 8u * s);
+            };
+            for (long long pass = 0; pass < a.passes; ++pass) {
+                const int buf = (int)(pass & 1);
+                long long start = 0;
+                if (pass > 0) {
+                    const long long pre = per_pass < stages ? per_pass : stages;
+                    for (long long j = 0; j < pre; ++j) issue_a(it + j, j);     // J does not depend on the step: run ahead
+                    const unsigned int target = a.ctas_total * (unsigned int)pass;
+                    while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
+                    umma::fence_proxy_async();
+                    for (long long j = 0; j < pre; ++j) issue_b(it + j, j, buf);
+                    start = pre;
+                }
+                for (long long j = start; j < per_pass; ++j) {
+                    issue_a(it + j, j);
+                    issue_b(it + j, j, buf);
+                }
+                it += per_pass;
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            const uint32_t idesc = umma::instr_desc_i8(a.NB);
+            long long it = 0, acc_it = 0;
+            for (long long pass = 0; pass < a.passes; ++pass) {
+                for (int tk = 0; tk < my_tiles; ++tk) {
+                    umma::mbar_wait(bar_tempty, (uint32_t)((acc_it & 1) ^ 1));
+                    umma::tc_fence_after();
+                    for (int kb = 0; kb < a.tiles; ++kb, ++it) {
+                        const int s = (int)(it % stages);
+                        umma::mbar_wait(bar_full + 8u * s, (uint32_t)((it / stages) & 1));
+                        umma::tc_fence_after();
+                        const uint64_t ad = umma::smem_desc(sA + (uint32_t)s * UMMA_A_STAGE);
+                        const uint64_t bd = umma::smem_desc(sB + (uint32_t)s * b_stage);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
+                        umma::tc_commit(bar_empty + 8u * s);
+                    }
+                    umma::tc_commit(bar_tfull);
+                    ++acc_it;
+                }
+            }
+        }
+    } else {
+        // ===== epilogue =====
+        const int et = (int)threadIdx.x - 64;
+        const int ew = warp - 2;
+        const int quad = warp & 3;
+        const int rowt = quad * 32 + lane;
+        const uint32_t tlane = tmem + ((uint32_t)(quad * 32) << 16);
+        const int R = a.R;
+        const T hT = (T)a.h, KT = (T)a.K, knT = (T)a.kn_sqrt_h;
+        long long e_idx = 0, s_idx = 0, acc_it = 0;
+        const int row0 = a.tile_begin * UMMA_TILE;
+        const int cta_global = a.cta_offset + (int)blockIdx.x;
+        for (long long pass = 0; pass < a.passes; ++pass) {
+            const int flags = a.flags[pass];
+            const bool prev_scored = pass > 0 && (a.flags[pass - 1] & 1);
+            const bool last = pass == a.passes - 1;
+            const uint64_t gstep = (uint64_t)(a.first_step + pass);
+            const T ksT = (T)ks_value(a.ks_max, a.ks_period, (double)gstep * a.h);
+            const T *phi_in = reinterpret_cast<const T *>(a.phi[pass & 1]);
+            T *phi_out = reinterpret_cast<T *>(a.phi[(pass + 1) & 1]);
+            bool checked = false;
+            for (int tk = 0; tk < my_tiles; ++tk) {
+                const int lt = (int)blockIdx.x + tk * (int)gridDim.x;
+                const int tile = a.tile_begin + lt;
+                const int rowl = lt * UMMA_TILE + rowt;
+                const int row = row0 + rowl;
+                const bool valid = row < a.n;
+                umma::mbar_wait(bar_tfull, (uint32_t)(acc_it & 1));
+                umma::tc_fence_after();
+                if (!checked) {
+                    // the grid barrier of the previous pass is behind us: its cut totals are complete
+                    if (prev_scored && et < R) {
+                        const long long tot = *reinterpret_cast<volatile long long *>(a.events[a.rank] + (e_idx - 1) * R + et);
+                        const int imp = tot > best_s[et];
+                        improved_s[et] = imp;
+                        if (imp) best_s[et] = tot;
+                    }
+                    umma::named_bar_sync(1, 128);
+                    checked = true;
+                }
+                const int Wi = valid ? a.W[rowl] : 0;
+                for (int r = 0; r < R; ++r) {
+                    int D[8], Dsig = 0;
+                    umma::tmem_ld8(tlane + (uint32_t)(8 * r), D);
+                    if (flags & 1) umma::tmem_ld1(tlane + (uint32_t)(8 * R + r), Dsig);
+                    umma::tmem_ld_wait();
+                    const long long Sx = umma::digits_sum(D), Sy = umma::digits_sum(D + 4);
+                    const long long at = (long long)r * a.ld_phi + rowl;
+                    const T p = valid ? phi_in[at] : T(0);
+                    if (prev_scored && improved_s[r] && valid)
+                        a.best_states[at] = (uint8_t)threshold_state((double)phi_out[at], 2);   // phi_out still holds the scored phases
+                    T si, ci;
+                    phase_trig(p, si, ci);
+                    const int st = threshold_state((double)p, 2);
+                    if (flags & 1) {
+                        long long contrib = valid ? ((long long)Wi - (st ? -(long long)Dsig : (long long)Dsig)) / 2 : 0;
+                        for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
+                        if (lane == 0)
+                            for (int w = 0; w < a.world; ++w) {
+                                unsigned long long *dst = reinterpret_cast<unsigned long long *>(a.events[w] + e_idx * R + r);
+                                if (sys) atomicAdd_system(dst, (unsigned long long)contrib);
+                                else atomicAdd(dst, (unsigned long long)contrib);
+                            }
+                    }
+                    if (flags & 2) {
+                        const double sc = 9.313225746154785e-10; // 2^-30
+                        double e = valid ? 0.5 * ((double)ci * ((double)Sx * sc) + (double)si * ((double)Sy * sc)) : 0.0;
+                        for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+                        if (lane == 0) en_w[ew * 32 + r] = e;
+                    }
+                    if (!last && valid) {
+                        const T scale = (T)9.313225746154785e-10;
+                        const T accv = si * ((T)Sx * scale) - ci * ((T)Sy * scale);
+                        const T shil = shil_term(p, si, ci, a.tc);
+                        T kick = T(0);
+                        if (a.noise_on) {
+                            T z[4];
+                            normals4(noise_block(a.seeds[r], gstep, (uint32_t)(row >> 2)), z);
+                            kick = z[row & 3];
+                        }
+                        const T x = p + hT * (KT * accv - ksT * shil) + knT * kick;
+                        if (!isfinite(x)) flag_nonfinite(a.nonfinite, gstep, (uint32_t)r, (uint32_t)row);
+                        const T y = wrap_unit(x);
+                        phi_out[at] = y;
+                        T s2, c2;
+                        phase_trig(y, s2, c2);
+                        const int st2 = threshold_state((double)y, 2);
+                        for (int w = 0; w < a.world; ++w)
+                            umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2);
+                    }
+                }
+                umma::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) umma::mbar_arrive(bar_tempty);
+                ++acc_it;
+                if (flags & 2) {
+                    umma::named_bar_sync(1, 128);
+                    if (et < R) en_acc[et] += ((en_w[et] + en_w[32 + et]) + en_w[64 + et]) + en_w[96 + et];
+                    umma::named_bar_sync(1, 128);
+                }
+            }
+            if ((flags & 2) && et < R) {
+                for (int w = 0; w < a.world; ++w)
+                    a.en_part[w][((size_t)s_idx * a.ctas_total + cta_global) * R + et] = en_acc[et];
+                en_acc[et] = 0.0;
+            }
+            // publish: every write of this pass (phases' digits on all ranks, cut atomics, energy
+            // partials) before the arrival that lets the next pass start anywhere
+            if (sys) __threadfence_system(); else __threadfence();
+            umma::fence_proxy_async();
+            umma::named_bar_sync(1, 128);
+            if (et == 0)
+                for (int w = 0; w < a.world; ++w) umma::red_release(a.bar[w], sys);
+            if (flags & 1) ++e_idx;
+            if (flags & 2) ++s_idx;
+        }
+        // the last pass scored the final phases: wait for every rank's totals, then keep the states
+        if (et == 0) {
+            const unsigned int target = a.ctas_total * (unsigned int)a.passes;
+            while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
+        }
+        umma::named_bar_sync(1, 128);
+        if ((a.flags[a.passes - 1] & 1) && et < R) {
+            const long long tot = *reinterpret_cast<volatile long long *>(a.events[a.rank] + (e_idx - 1) * R + et);
+            improved_s[et] = tot > best_s[et];
+        }
+        umma::named_bar_sync(1, 128);
+        if (a.flags[a.passes - 1] & 1) {
+            const T *phi_fin = reinterpret_cast<const T *>(a.phi[(a.passes - 1) & 1]);
+            for (int tk = 0; tk < my_tiles; ++tk) {
+                const int rowl = ((int)blockIdx.x + tk * (int)gridDim.x) * UMMA_TILE + rowt;
+                if (row0 + rowl < a.n)
+                    for (int r = 0; r < R; ++r)
+                        if (improved_s[r]) a.best_states[(long long)r * a.ld_phi + rowl] = (uint8_t)threshold_state((double)phi_fin[(long long)r * a.ld_phi + rowl], 2);
+            }
+        }
+    }
+    umma::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+}
+
+} // namespace oscb

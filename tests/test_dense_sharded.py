@@ -180,15 +180,15 @@ def test_dense_handle_matches_oracle(pkg, oracle, weights):
     seeds = [4, 5, 6]
     ref = oracle.simulate(Js.indptr, Js.indices, Js.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period,
                           kn=0.0, h=params.h, t_stop=params.t_stop, n_states=2, seeds=seeds, objective="maxcut")
-    got = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f64")
+    got = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f64", kernel="stream")
     assert got.kernel == "stream"
     assert circ_dist_rad(got.final_phases, ref.final_phases).max() <= 1e-9          # N = 200 steps
     assert np.array_equal(got.best_objective, ref.best_objective)
     assert np.array_equal(got.best_states.astype(np.int64), ref.best_states)
     assert np.array_equal(got.trace_t, ref.trace_t)
     assert np.abs(got.energy - ref.energy).max() <= 1e-8
-    short = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", steps=30)
-    ref30 = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f64", steps=30)
+    short = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", steps=30, kernel="stream")
+    ref30 = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f64", steps=30, kernel="stream")
     assert circ_dist_rad(short.final_phases, ref30.final_phases).max() <= 1e-4       # N = 30 steps
 
 
@@ -240,7 +240,7 @@ def test_sharded_driver_equals_single_handle_run(pkg):
     params = pkg.SolverParams(K=0.05, ks_max=1.0, ks_period=1.0, kn=0.2, h=0.01, t_stop=1.5, seed=30)
     seeds = [30, 31, 32, 33]
     for precision in ("f32", "f64"):
-        want = pkg.run_batch(Jd, params, "maxcut", seeds, precision=precision)
+        want = pkg.run_batch(Jd, params, "maxcut", seeds, precision=precision, kernel="stream")
         shard = CudaDenseShard(J, n, 0, n, 0, precision)
         got = run_dense_sharded(shard, params, "maxcut", seeds, pair_count=n * (n - 1) // 2).batch
         assert np.array_equal(got.final_phases, want.final_phases)

@@ -1,0 +1,107 @@
+"""Tensor-core dense integrator (csrc/oscb_umma.cuh, kernel "dense-tc") against the float64 SIMT
+dense path and the CPU oracle on the same couplings and seeds.
+
+The coupling sums of the tensor-core kernel are exact integer dot products of J with the 2^-30
+fixed-point digits of (cos, sin), so with a float64 epilogue the trajectory differs from the
+reference only by that quantisation: the noise-free bar is 1e-6 rad after N = 200 steps (the
+north-star tolerance is 1e-4 rad); cut values, best states and traces are bit-exact."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def sk_graph(n, seed, weights=(-1.0, 1.0)):
+    rng = np.random.default_rng(seed)
+    U = np.triu(rng.choice(np.asarray(weights, dtype=np.float64), size=(n, n)), 1)
+    return U + U.T
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2505_22631_b200 as p
+    from paper_2505_22631_b200 import _native, dynamics
+    assert _native.device_count() > 0, "no CUDA device: " + _native.last_error()
+    old = dynamics.DENSE_DEVICE_MIN_N
+    dynamics.DENSE_DEVICE_MIN_N = 0
+    yield p
+    dynamics.DENSE_DEVICE_MIN_N = old
+
+
+def circ(a, b):
+    d = np.abs(a - b)
+    return 2 * np.pi * np.minimum(d, 1 - d)
+
+
+@pytest.mark.parametrize("n,R,weights,grid_cap", [
+    (256, 3, (-1.0, 1.0), None),
+    (300, 5, (-1.0, 1.0), None),                     # ragged last tile
+    (200, 2, (-3.0, -1.0, 0.0, 0.0, 1.0, 2.0), None),  # general small integers, zeros
+    (640, 4, (-1.0, 1.0), "2"),                      # 5 row tiles on 2 CTAs: several tiles per CTA
+])
+def test_noise_free_run_matches_float64_stream_and_oracle(pkg, oracle, n, R, weights, grid_cap):
+    J = sk_graph(n, 100 + n, weights)
+    Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
+    Js = pkg.CouplingMatrix.from_dense(J, storage="sparse")
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=1.0, kn=0.0, h=0.01, t_stop=2.0, seed=4)
+    seeds = list(range(4, 4 + R))
+    if grid_cap:
+        os.environ["OSCB_UMMA_MAX_GRID"] = grid_cap
+    try:
+        got = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f64", kernel="dense-tc")
+    finally:
+        os.environ.pop("OSCB_UMMA_MAX_GRID", None)
+    assert got.kernel == "dense-tc" and got.steps == 200
+    want = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f64", kernel="stream")
+    ref = oracle.simulate(Js.indptr, Js.indices, Js.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period,
+                          kn=0.0, h=params.h, t_stop=params.t_stop, n_states=2, seeds=seeds, objective="maxcut")
+    assert circ(got.final_phases, want.final_phases).max() <= 1e-6          # N = 200 steps
+    assert circ(got.final_phases, ref.final_phases).max() <= 1e-6
+    assert np.array_equal(got.best_objective, ref.best_objective)
+    assert np.array_equal(got.best_states.astype(np.int64), ref.best_states)
+    assert np.array_equal(got.trace_t, ref.trace_t) and np.array_equal(got.trace_ks, ref.trace_ks)
+    assert np.array_equal(got.best_trace, ref.best_trace)
+    assert np.abs(got.energy - ref.energy).max() <= 1e-6 * n
+
+
+def test_noisy_f32_run_is_consistent(pkg):
+    """Noise on, float32 epilogue: same (seed, step, oscillator) noise as the SIMT path, so 30 steps
+    agree within 1e-4 rad; the result contract holds; best objective == cut of best states."""
+    n, R = 384, 6
+    J = sk_graph(n, 7)
+    Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=1.0, kn=0.2, h=0.01, t_stop=3.0, seed=11)
+    seeds = list(range(11, 11 + R))
+    a = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", kernel="dense-tc", steps=30)
+    b = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", kernel="stream", steps=30)
+    assert circ(a.final_phases, b.final_phases).max() <= 1e-4                # N = 30 steps
+    full = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32")        # auto -> dense-tc
+    assert full.kernel == "dense-tc" and full.steps == 300
+    assert (full.final_phases >= 0).all() and (full.final_phases < 1).all()
+    iu, jv = np.triu_indices(n, 1)
+    for r in range(R):
+        s = full.best_states[r].astype(np.int64)
+        assert full.best_objective[r] == float((J[iu, jv] * (s[iu] != s[jv])).sum())
+        assert (np.diff(full.best_trace[r]) >= 0).all()
+    again = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32")
+    assert np.array_equal(again.final_phases, full.final_phases)              # deterministic
+    assert np.array_equal(again.energy, full.energy)
+
+
+def test_replica_chunks_equal_single_runs(pkg):
+    """More replicas than one launch takes (28): the chunks reproduce the solo runs bit for bit."""
+    n, R = 256, 31
+    J = sk_graph(n, 3)
+    Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.1, h=0.01, t_stop=0.6, seed=0)
+    seeds = list(range(R))
+    allr = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", target=0.0)
+    for r in (0, 27, 28, 30):
+        solo = pkg.run_batch(Jd, params, "maxcut", [seeds[r]], precision="f32", target=0.0)
+        assert np.array_equal(solo.final_phases[0], allr.final_phases[r])
+        assert np.array_equal(solo.best_states[0], allr.best_states[r])
+        assert solo.best_objective[0] == allr.best_objective[r]
+        assert np.array_equal(solo.energy[0], allr.energy[r])
+        assert solo.first_hit_step[0] == allr.first_hit_step[r]
