@@ -178,30 +178,154 @@ def run_reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def dense_csr(J8):
+    """CSR (int64/float64, the reference's layout) of a dense int8 J with zero diagonal -- the CPU arm's input."""
+    n = J8.shape[0]
+    mask = ~np.eye(n, dtype=bool)
+    indices = np.broadcast_to(np.arange(n, dtype=np.int64), (n, n))[mask]
+    data = J8[mask].astype(np.float64)
+    indptr = np.arange(n + 1, dtype=np.int64) * (n - 1)
+    return indptr, indices, data
+
+
+def dense_cpu_sample(J8, params, steps, threads=None):
+    """The CPU oracle port on the dense graph: R = 1, a few Euler steps (~0.3 s each on 16 cores)."""
+    from oracle import oracle as O
+    O.build()
+    threads = threads or O.max_threads()
+    indptr, indices, data = dense_csr(J8)
+    t0 = time.perf_counter()
+    O.simulate(indptr, indices, data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period, kn=params.kn,
+               h=params.h, t_stop=steps * params.h, n_states=2, seeds=[0], objective="maxcut", threads=threads)
+    dt = time.perf_counter() - t0
+    return len(data) * steps / dt, dt, threads
+
+
 def bench_dense(args, rank, world, local_rank):
-    """configs[4]: dense +-1 SK graph, J row-sharded over the ranks, phases all-gathered every Euler
-    step (strong scaling: the graph is fixed, the rows per GPU shrink)."""
+    """configs[4]: dense +-1 SK graph.  One GPU: the persistent tensor-core kernel (csrc/oscb_umma.cuh)
+    integrates the whole window in ONE launch.  Several GPUs: J row-sharded over the ranks, phases
+    all-gathered every Euler step (strong scaling: the graph is fixed, the rows per GPU shrink)."""
     import torch
     import torch.distributed as dist
     from paper_2505_22631_b200 import workloads
-    from paper_2505_22631_b200.dense_sharded import CudaDenseShard, run_dense_sharded
     from paper_2505_22631_b200.model import SolverParams
     n = int(args.workload[2:].split("x")[0])
     R = args.replicas or int(args.workload.split("x")[1])
-    window = args.window if args.window != 2048 else 256
-    rows = n // world
+    window = args.window if args.window != 2048 else (1024 if world == 1 else 256)
+    params = SolverParams.tuned_for(n, 2, seed=0)
+    seeds = list(range(R))
+    nnz = n * (n - 1)
+    peaks, peak_kind = measured_peaks()
+    s_phi = 4 if args.precision == "f32" else 8
+    label = (f"dense +-1 SK graph n={n} N=2 K={params.K} ks_max={params.ks_max} kn={params.kn} h={params.h}, {R} replica(s), "
+             f"window {window} Euler steps incl. scoring every 10")
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        J8 = workloads.sk_dense(n)
+        steps_cpu = max(2, min(window, int(12.0 * 80e6 * (os.cpu_count() or 1) / nnz)))
+        for _ in range(min(1, args.warmup)):
+            dense_cpu_sample(J8, params, 2)
+        t_all = upd = 0.0
+        threads = 1
+        for _ in range(args.steps):
+            v, dt, threads = dense_cpu_sample(J8, params, steps_cpu)
+            t_all += dt
+            upd += nnz * steps_cpu
+        value = upd / t_all
+        sample = f"1 replica x {steps_cpu} Euler steps per step (of {R} x {window}), linear in replicas and steps"
+        print(json.dumps({
+            "impl": "reference", "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": label, "replicas": R, "window": window, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}, "gpu_launches": 0}), flush=True)
+        return
+
     J8 = workloads.sk_dense(n)                                   # int8, symmetric, zero diagonal
+    if world == 1:
+        from paper_2505_22631_b200 import dynamics as dyn
+        g = dyn.DeviceGraph.from_dense(local_rank, J8.astype(np.float64))
+
+        def device_step():
+            return dyn.run_batch(None, params, "maxcut", seeds, precision=args.precision, device=local_rank, steps=window,
+                                 want_phases=False, want_states=False, want_traces=False, graph=g)
+
+        for _ in range(args.warmup):
+            device_step()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local_rank)
+        sampler.start()
+        dev_ms, launches, last = 0.0, 0, None
+        for _ in range(args.steps):
+            last = device_step()
+            dev_ms += last.device_ms
+            launches += last.kernel_launches
+        torch.cuda.synchronize()
+        clocks = sampler.stop()
+        phi0_pinned = torch.empty((R, n), dtype=torch.float64, pin_memory=True)
+        phi0 = phi0_pinned.numpy()
+        phi0[...] = dyn._initial_phases_host(local_rank, seeds, n)
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(args.steps):
+            b = dyn.run_batch(None, params, "maxcut", seeds, precision=args.precision, device=local_rank, steps=window,
+                              phi0=phi0, graph=g)
+            h2d = phi0.nbytes + 8 * R
+            d2h = b.final_phases.nbytes + b.best_states.nbytes + b.best_objective.nbytes + b.energy.nbytes + b.best_trace.nbytes
+        e2e_s = time.perf_counter() - t0
+        value = R * nnz * window * args.steps / (dev_ms / 1e3)
+        e2e_value = R * nnz * window * args.steps / e2e_s
+        chunks = -(-R // 28)                                      # launches per window (28 replicas per launch)
+        # algorithmic HBM bytes per Euler step: J once (1 B per coupling, int8) per launch + phases read and written
+        bytes_step = chunks * n * n + 2 * R * n * s_phi
+        kernel_ms = dev_ms / args.steps
+        achieved = bytes_step * window / (kernel_ms * 1e-3) / 1e9
+        traffic = None
+        tpath = ROOT / "profiles" / "dram_traffic.json"
+        if tpath.exists():
+            t = json.loads(tpath.read_text()).get(f"{args.workload}:{last.kernel}:{args.precision}:{window}")
+            if t:
+                traffic = t["dram_bytes_per_launch"]
+        # int8 tensor work issued: 2 * 128-row tiles * N columns * n per step (N = 16-padded 9 planes per replica)
+        nb = -(-9 * min(R, 28) // 16) * 16
+        tensor_tops = 2.0 * n * n * nb * chunks * window / (kernel_ms * 1e-3) / 1e12
+        line = {
+            "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.precision + " epilogue, int8 x int8 -> int32 tensor-core sums", "data": "synthetic",
+            "config": {"workload": label, "replicas": R, "window": window, "kernel": last.kernel,
+                       "replicas_per_launch": last.replicas_per_cta, "smem_bytes": last.smem_bytes, "parallelism": "one GPU",
+                       "l2": "J (n^2 bytes = %.0f MB) exceeds the 126 MB L2 and is re-read from HBM every Euler step; no flush needed" % (n * n / 1e6)},
+            "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_kind": peak_kind, "kernel": "k_dense_umma",
+                         "algorithmic_bytes_per_launch": bytes_step * window / chunks, "bytes_per_update": bytes_step / (R * nnz),
+                         "tensor_int8_tops_issued": tensor_tops,
+                         "note": "one persistent launch = the whole window; per Euler step it streams J (int8) once from HBM"},
+        }
+        if not args.no_cpu_baseline:
+            steps_cpu = max(2, min(window, int(12.0 * 80e6 * (os.cpu_count() or 1) / nnz)))
+            v, dt, threads = dense_cpu_sample(J8, params, steps_cpu)
+            line["cpu_baseline"] = {"value": v, "unit": "updates/s", "cores": threads, "kind": "port",
+                                    "sample": f"1 replica x {steps_cpu} Euler steps of the same graph in {dt:.1f} s "
+                                              f"(oracle/ C+OpenMP port of the reference; linear in replicas and steps)"}
+        print(json.dumps(line), flush=True)
+        return
+
+    from paper_2505_22631_b200.dense_sharded import CudaDenseShard, run_dense_sharded
+    rows = n // world
     shard = CudaDenseShard(J8[rank * rows:(rank + 1) * rows].astype(np.float64), n, rank * rows, (rank + 1) * rows,
                            local_rank, args.precision)
     del J8
-    params = SolverParams.tuned_for(n, 2, seed=0)
-    seeds = list(range(R))
     pairs = n * (n - 1) // 2
 
     def one():
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        dist.barrier()
         t0 = time.perf_counter()
         res = run_dense_sharded(shard, params, "maxcut", seeds, pair_count=pairs, steps=window)
         torch.cuda.synchronize()
@@ -217,22 +341,17 @@ def bench_dense(args, rank, world, local_rank):
         total += dt
     clocks = sampler.stop()
     t = torch.tensor([total], dtype=torch.float64, device=f"cuda:{local_rank}")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total = float(t.cpu())
-    nnz = n * (n - 1)
     value = R * nnz * window * args.steps / total
-    peaks, peak_kind = measured_peaks()
-    # algorithmic HBM bytes per Euler step and GPU: the shard of J once (1 B per coupling, int8) + phases
-    bytes_step = rows * n * 1 + 2 * R * n * (4 if args.precision == "f32" else 8)
+    bytes_step = rows * n * 1 + 2 * R * n * s_phi
     achieved = bytes_step * window * args.steps / total / 1e9
     if rank == 0:
         print(json.dumps({
             "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": f"dense +-1 SK graph n={n}, {R} replica(s), J row-sharded over {world} GPU(s) with a phase "
-                                   f"all-gather per Euler step, window {window} Euler steps incl. scoring every 10",
+            "config": {"workload": label + f"; J row-sharded over {world} GPUs with a phase all-gather per Euler step",
                        "replicas": R, "window": window, "parallelism": f"row-shard x{world}",
                        "l2": "J shard (n^2/G bytes) exceeds L2 for n=16384 at G<=2; re-read from HBM every step"},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": int(8 * R * n), "d2h_bytes_per_step": int(9 * R * n),
@@ -264,7 +383,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference_arm(args, rank, world)
+        if args.workload.startswith("SK"):
+            bench_dense(args, rank, world, 0)
+        else:
+            run_reference_arm(args, rank, world)
         return
 
     import torch

@@ -3,6 +3,7 @@
 #include "oscb_umma.cuh"
 #include <algorithm>
 #include <cstdlib>
+#include <cstdio>
 #include <vector>
 
 namespace oscb {
@@ -87,6 +88,13 @@ static void umma_run_t(oscb_graph *g, const UmmaPlan &plan, UmmaSpec &spec)
     a.best_states = d_best.p;
     a.nonfinite = g->d_nonfinite.p;
 
+    DevBuf<long long> d_trace;
+    const char *trace_path = getenv("OSCB_UMMA_TRACE");           // debug: per-CTA timeline of the first passes
+    if (trace_path) {
+        d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * 4);
+        d_trace.zero(s);
+        a.trace = d_trace.p;
+    }
     const long long tot = (long long)n * R;
     k_umma_init<T><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, spec.d_phi0);
     OSCB_CUDA(cudaGetLastError());
@@ -111,6 +119,19 @@ static void umma_run_t(oscb_graph *g, const UmmaPlan &plan, UmmaSpec &spec)
     OSCB_CUDA(cudaMemcpyAsync(&spec.nonfinite, g->d_nonfinite.p, sizeof(none), cudaMemcpyDeviceToHost, s));
     OSCB_CUDA(cudaStreamSynchronize(s));
     OSCB_CUDA(cudaEventElapsedTime(&spec.ms, ev0, ev1));
+    if (trace_path) {
+        std::vector<long long> h((size_t)grid * UMMA_TRACE_PASSES * 4);
+        OSCB_CUDA(cudaMemcpy(h.data(), d_trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        if (FILE *f = fopen(trace_path, "w")) {
+            fprintf(f, "cta,pass,barrier_seen,tmem_full,arrived,barrier_wait_begin\n");
+            for (int c = 0; c < grid; ++c)
+                for (int q = 0; q < UMMA_TRACE_PASSES && q < a.passes; ++q) {
+                    const long long *t = &h[((size_t)c * UMMA_TRACE_PASSES + q) * 4];
+                    fprintf(f, "%d,%d,%lld,%lld,%lld,%lld\n", c, q, t[0], t[1], t[2], t[3]);
+                }
+            fclose(f);
+        }
+    }
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
     if (spec.h_energy)

@@ -9,11 +9,11 @@
 //   Integer accumulation is exact and order independent, so the coupling sums carry only the
 //   2^-31 quantisation of each pair -- tighter than a float32 FMA chain over n = 16384 terms.
 //
-// Roles of the 192 threads of a CTA (one CTA per SM, one 128-row tile of J at a time):
+// Roles of the 576 threads of a CTA (one CTA per SM, one 128-row tile of J at a time):
 //   warp 0   producer: cp.async.bulk (UBLKCP) of the 16 KB tile images of A (HBM stream) and
 //            of B (L2 resident) into a ring of shared-memory stages, signalled on mbarriers;
 //   warp 1   one elected lane issues the tcgen05.mma instructions and commits them;
-//   warps 2-5 epilogue: tcgen05.ld of their 32 TMEM lanes, then per (row, replica) the fused
+//   warps 2-17 epilogue: tcgen05.ld of their 32 TMEM lanes, then per (row, replica) the fused
 //            Euler update (SHIL, Philox noise, schedule, wrap; dynamics.py:166-172), the new
 //            (cos, sin) digits written straight into the NEXT step's B image on every rank
 //            (peer pointers: the push all-gather of the row-sharded multi-GPU run), the cut
@@ -35,8 +35,12 @@ namespace oscb {
 constexpr int UMMA_MAXW = 8;          // ranks a row-sharded run may span
 constexpr int UMMA_TILE = 128;        // rows per tile = bytes of K per stage
 constexpr int UMMA_A_STAGE = UMMA_TILE * UMMA_TILE;
-constexpr int UMMA_THREADS = 192;
+constexpr int UMMA_EPI_WARPS = 16;      // 4 groups x 4 TMEM lane quadrants
+constexpr int UMMA_EPI_THREADS = UMMA_EPI_WARPS * 32;
+constexpr int UMMA_THREADS = 64 + UMMA_EPI_THREADS;
 constexpr int UMMA_MAXR = 28;         // 9 B rows per replica, N <= 256
+constexpr int UMMA_RPG = UMMA_MAXR / 4; // replicas per epilogue group
+constexpr int UMMA_TRACE_PASSES = 64;
 
 struct UmmaArgs {
     int n;                    // oscillators
@@ -66,6 +70,7 @@ struct UmmaArgs {
     double *en_part[UMMA_MAXW];        // [n_samples][ctas_total][R]
     uint8_t *best_states;     // [R][ld_phi]
     unsigned long long *nonfinite;
+    long long *trace;         // debug timeline [cta][UMMA_TRACE_PASSES][4] in SM clocks, or null
 };
 
 namespace umma {
@@ -95,6 +100,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -271,7 +280,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) { umma::mbar_init(bar_full + 8u * s, 1); umma::mbar_init(bar_empty + 8u * s, 1); }
         umma::mbar_init(bar_tfull, 1);
-        umma::mbar_init(bar_tempty, 4);
+        umma::mbar_init(bar_tempty, UMMA_EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -289,66 +298,69 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ===== producer =====
+        // ===== producer =====  (one thread; no divisions on this path: it paces the whole CTA)
         if (lane == 0) {
-            long long it = 0;
-            auto coords = [&](long long q, int &lt, int &kb) {
-                const int tk = (int)(q / a.tiles);
-                kb = (int)(q % a.tiles);
-                lt = (int)blockIdx.x + tk * (int)gridDim.x;
+            struct Cursor {
+                int s; uint32_t ph; int tk, kb;
             };
-            auto issue_a = [&](long long gi, long long q) {
-                const int s = (int)(gi % stages);
-                umma::mbar_wait(bar_empty + 8u * s, (uint32_t)(((gi / stages) & 1) ^ 1));
-                umma::mbar_expect_tx(bar_full + 8u * s, stage_tx);
-                int lt, kb;
-                coords(q, lt, kb);
-                umma::bulk_g2s(sA + (uint32_t)s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + kb) * UMMA_A_STAGE, UMMA_A_STAGE,
-                               bar_full + 8u * s);
+            Cursor ca{0, 0, 0, 0}, cb{0, 0, 0, 0};
+            auto advance = [&](Cursor &c) {
+                if (++c.s == stages) { c.s = 0; c.ph ^= 1u; }
+                if (++c.kb == a.tiles) { c.kb = 0; if (++c.tk == my_tiles) c.tk = 0; }
             };
-            auto issue_b = [&](long long gi, long long q, int buf) {
-                const int s = (int)(gi % stages);
-                int lt, kb;
-                coords(q, lt, kb);
-                umma::bulk_g2s(sB + (uint32_t)s * b_stage, a.B_img[buf][a.rank] + (size_t)kb * b_stage, b_stage, bar_full + 8u * s);
+            auto issue_a = [&](Cursor &c) {
+                umma::mbar_wait(bar_empty + 8u * c.s, c.ph ^ 1u);
+                umma::mbar_expect_tx(bar_full + 8u * c.s, stage_tx);
+                const int lt = (int)blockIdx.x + c.tk * (int)gridDim.x;
+                umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
+                               bar_full + 8u * c.s);
+                advance(c);
             };
+            auto issue_b = [&](Cursor &c, const uint8_t *Bsrc) {
+                umma::bulk_g2s(sB + (uint32_t)c.s * b_stage, Bsrc + (size_t)c.kb * b_stage, b_stage, bar_full + 8u * c.s);
+                advance(c);
+            };
+            const int per_pass_i = (int)per_pass;
+            const int pre = per_pass_i < stages ? per_pass_i : stages;
             for (long long pass = 0; pass < a.passes; ++pass) {
-                const int buf = (int)(pass & 1);
-                long long start = 0;
+                const uint8_t *Bsrc = a.B_img[pass & 1][a.rank];
+                int start = 0;
                 if (pass > 0) {
-                    const long long pre = per_pass < stages ? per_pass : stages;
-                    for (long long j = 0; j < pre; ++j) issue_a(it + j, j);     // J does not depend on the step: run ahead
+                    for (int j = 0; j < pre; ++j) issue_a(ca);                  // J does not depend on the step: run ahead
                     const unsigned int target = a.ctas_total * (unsigned int)pass;
+                    if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 3] = clock64();
                     while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
+                    if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 0] = clock64();
                     umma::fence_proxy_async();
-                    for (long long j = 0; j < pre; ++j) issue_b(it + j, j, buf);
+                    for (int j = 0; j < pre; ++j) issue_b(cb, Bsrc);
                     start = pre;
                 }
-                for (long long j = start; j < per_pass; ++j) {
-                    issue_a(it + j, j);
-                    issue_b(it + j, j, buf);
+                for (int j = start; j < per_pass_i; ++j) {
+                    issue_a(ca);
+                    issue_b(cb, Bsrc);
                 }
-                it += per_pass;
             }
         }
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
             const uint32_t idesc = umma::instr_desc_i8(a.NB);
-            long long it = 0, acc_it = 0;
+            long long acc_it = 0;
+            int s = 0;
+            uint32_t ph = 0;
             for (long long pass = 0; pass < a.passes; ++pass) {
                 for (int tk = 0; tk < my_tiles; ++tk) {
                     umma::mbar_wait(bar_tempty, (uint32_t)((acc_it & 1) ^ 1));
                     umma::tc_fence_after();
-                    for (int kb = 0; kb < a.tiles; ++kb, ++it) {
-                        const int s = (int)(it % stages);
-                        umma::mbar_wait(bar_full + 8u * s, (uint32_t)((it / stages) & 1));
+                    for (int kb = 0; kb < a.tiles; ++kb) {
+                        umma::mbar_wait(bar_full + 8u * s, ph);
                         umma::tc_fence_after();
                         const uint64_t ad = umma::smem_desc(sA + (uint32_t)s * UMMA_A_STAGE);
                         const uint64_t bd = umma::smem_desc(sB + (uint32_t)s * b_stage);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
                         umma::tc_commit(bar_empty + 8u * s);
+                        if (++s == stages) { s = 0; ph ^= 1u; }
                     }
                     umma::tc_commit(bar_tfull);
                     ++acc_it;
@@ -356,10 +368,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             }
         }
     } else {
-        // ===== epilogue =====
+        // ===== epilogue: 16 warps.  Warp w reads TMEM lanes 32 (w % 4) .. +31 (a hardware rule), so the
+        // four warps of "group" g = (w - 2) / 4 cover the 128 rows of the tile; group g owns the
+        // replicas r = g, g + 4, ...  Everything that does not need the coupling sums (own trig,
+        // SHIL, the Philox draw) is computed BEFORE the wait on the accumulator. =====
         const int et = (int)threadIdx.x - 64;
-        const int ew = warp - 2;
         const int quad = warp & 3;
+        const int group = (warp - 2) >> 2;
         const int rowt = quad * 32 + lane;
         const uint32_t tlane = tmem + ((uint32_t)(quad * 32) << 16);
         const int R = a.R;
@@ -382,8 +397,30 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 const int rowl = lt * UMMA_TILE + rowt;
                 const int row = row0 + rowl;
                 const bool valid = row < a.n;
+                // ---- before the sums exist ----
+                T pre_p[UMMA_RPG], pre_s[UMMA_RPG], pre_c[UMMA_RPG], pre_d[UMMA_RPG];   // phase, sin, cos, h*(-ks shil) + kn xi
+                const int Wi = valid ? a.W[rowl] : 0;
+#pragma unroll
+                for (int k = 0; k < UMMA_RPG; ++k) {
+                    const int r = group + 4 * k;
+                    pre_p[k] = pre_s[k] = pre_c[k] = pre_d[k] = T(0);
+                    if (r < R && valid) {
+                        const T p = phi_in[(long long)r * a.ld_phi + rowl];
+                        T si, ci;
+                        phase_trig(p, si, ci);
+                        T kick = T(0);
+                        if (a.noise_on && !last) {
+                            T z[4];
+                            normals4(noise_block(a.seeds[r], gstep, (uint32_t)(row >> 2)), z);
+                            kick = z[row & 3];
+                        }
+                        pre_p[k] = p; pre_s[k] = si; pre_c[k] = ci;
+                        pre_d[k] = kick;
+                    }
+                }
                 umma::mbar_wait(bar_tfull, (uint32_t)(acc_it & 1));
                 umma::tc_fence_after();
+                if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 1] = clock64();
                 if (!checked) {
                     // the grid barrier of the previous pass is behind us: its cut totals are complete
                     if (prev_scored && et < R) {
@@ -392,24 +429,25 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         improved_s[et] = imp;
                         if (imp) best_s[et] = tot;
                     }
-                    umma::named_bar_sync(1, 128);
+                    if (prev_scored) umma::named_bar_sync(1, UMMA_EPI_THREADS);
                     checked = true;
                 }
-                const int Wi = valid ? a.W[rowl] : 0;
-                for (int r = 0; r < R; ++r) {
+#pragma unroll
+                for (int k = 0; k < UMMA_RPG; ++k) {
+                    const int r = group + 4 * k;
+                    if (r >= R) break;                       // warp uniform
                     int D[8], Dsig = 0;
                     umma::tmem_ld8(tlane + (uint32_t)(8 * r), D);
                     if (flags & 1) umma::tmem_ld1(tlane + (uint32_t)(8 * R + r), Dsig);
                     umma::tmem_ld_wait();
+
                     const long long Sx = umma::digits_sum(D), Sy = umma::digits_sum(D + 4);
                     const long long at = (long long)r * a.ld_phi + rowl;
-                    const T p = valid ? phi_in[at] : T(0);
+                    const T p = pre_p[k], si = pre_s[k], ci = pre_c[k];
                     if (prev_scored && improved_s[r] && valid)
                         a.best_states[at] = (uint8_t)threshold_state((double)phi_out[at], 2);   // phi_out still holds the scored phases
-                    T si, ci;
-                    phase_trig(p, si, ci);
-                    const int st = threshold_state((double)p, 2);
                     if (flags & 1) {
+                        const int st = threshold_state((double)p, 2);
                         long long contrib = valid ? ((long long)Wi - (st ? -(long long)Dsig : (long long)Dsig)) / 2 : 0;
                         for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
                         if (lane == 0)
@@ -423,19 +461,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         const double sc = 9.313225746154785e-10; // 2^-30
                         double e = valid ? 0.5 * ((double)ci * ((double)Sx * sc) + (double)si * ((double)Sy * sc)) : 0.0;
                         for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
-                        if (lane == 0) en_w[ew * 32 + r] = e;
+                        if (lane == 0) en_w[quad * 32 + r] = e;
                     }
                     if (!last && valid) {
                         const T scale = (T)9.313225746154785e-10;
                         const T accv = si * ((T)Sx * scale) - ci * ((T)Sy * scale);
                         const T shil = shil_term(p, si, ci, a.tc);
-                        T kick = T(0);
-                        if (a.noise_on) {
-                            T z[4];
-                            normals4(noise_block(a.seeds[r], gstep, (uint32_t)(row >> 2)), z);
-                            kick = z[row & 3];
-                        }
-                        const T x = p + hT * (KT * accv - ksT * shil) + knT * kick;
+                        const T x = p + hT * (KT * accv - ksT * shil) + knT * pre_d[k];
                         if (!isfinite(x)) flag_nonfinite(a.nonfinite, gstep, (uint32_t)r, (uint32_t)row);
                         const T y = wrap_unit(x);
                         phi_out[at] = y;
@@ -451,9 +483,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 if (lane == 0) umma::mbar_arrive(bar_tempty);
                 ++acc_it;
                 if (flags & 2) {
-                    umma::named_bar_sync(1, 128);
+                    umma::named_bar_sync(1, UMMA_EPI_THREADS);
                     if (et < R) en_acc[et] += ((en_w[et] + en_w[32 + et]) + en_w[64 + et]) + en_w[96 + et];
-                    umma::named_bar_sync(1, 128);
+                    umma::named_bar_sync(1, UMMA_EPI_THREADS);
                 }
             }
             if ((flags & 2) && et < R) {
@@ -463,11 +495,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             }
             // publish: every write of this pass (phases' digits on all ranks, cut atomics, energy
             // partials) before the arrival that lets the next pass start anywhere
-            if (sys) __threadfence_system(); else __threadfence();
             umma::fence_proxy_async();
-            umma::named_bar_sync(1, 128);
-            if (et == 0)
+            umma::named_bar_sync(1, UMMA_EPI_THREADS);
+            if (et == 0) {
+                if (sys) __threadfence_system(); else __threadfence();       // cumulative over the CTA barrier above
                 for (int w = 0; w < a.world; ++w) umma::red_release(a.bar[w], sys);
+                if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 2] = clock64();
+            }
             if (flags & 1) ++e_idx;
             if (flags & 2) ++s_idx;
         }
@@ -476,18 +510,18 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             const unsigned int target = a.ctas_total * (unsigned int)a.passes;
             while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
         }
-        umma::named_bar_sync(1, 128);
+        umma::named_bar_sync(1, UMMA_EPI_THREADS);
         if ((a.flags[a.passes - 1] & 1) && et < R) {
             const long long tot = *reinterpret_cast<volatile long long *>(a.events[a.rank] + (e_idx - 1) * R + et);
             improved_s[et] = tot > best_s[et];
         }
-        umma::named_bar_sync(1, 128);
+        umma::named_bar_sync(1, UMMA_EPI_THREADS);
         if (a.flags[a.passes - 1] & 1) {
             const T *phi_fin = reinterpret_cast<const T *>(a.phi[(a.passes - 1) & 1]);
             for (int tk = 0; tk < my_tiles; ++tk) {
                 const int rowl = ((int)blockIdx.x + tk * (int)gridDim.x) * UMMA_TILE + rowt;
                 if (row0 + rowl < a.n)
-                    for (int r = 0; r < R; ++r)
+                    for (int r = group; r < R; r += 4)
                         if (improved_s[r]) a.best_states[(long long)r * a.ld_phi + rowl] = (uint8_t)threshold_state((double)phi_fin[(long long)r * a.ld_phi + rowl], 2);
             }
         }

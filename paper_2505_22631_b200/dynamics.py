@@ -426,13 +426,15 @@ def run_batch(J: CouplingMatrix, params: SolverParams, objective: str, seeds: Se
               cadence: Optional[int] = None, phi0: Optional[np.ndarray] = None,
               noise: Optional[np.ndarray] = None, noise_off: bool = False,
               target: Optional[float] = None, first_step: int = 0, replicas_per_cta: int = 0,
-              want_phases: bool = True, want_states: bool = True, want_traces: bool = True) -> BatchResult:
+              want_phases: bool = True, want_states: bool = True, want_traces: bool = True,
+              graph: Optional[DeviceGraph] = None) -> BatchResult:
     """Advance the replicas `seeds` together on one GPU: the drop-in for `_simulate`
     (dynamics.py:333-431).  `noise` ([steps, R, n]) injects host-supplied normals (parity
-    hook); `noise_off` integrates with kn treated as 0."""
-    g = device_graph(J, device)
+    hook); `noise_off` integrates with kn treated as 0.  `graph` runs on an already uploaded
+    device graph (J may then be None -- e.g. a dense J too large to also hold as CSR)."""
+    g = device_graph(J, device) if graph is None else graph
     prec = _precision(precision)
-    n, R = J.n, len(seeds)
+    n, R = (J.n if graph is None else int(graph.info().n)), len(seeds)
     stride = params.ks_period / 2.0 if trace_stride is None else float(trace_stride)
     if stride <= 0:
         raise ValueError("trace_stride must be > 0")
