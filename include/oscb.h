@@ -178,6 +178,39 @@ int oscb_dense_shard_energy(oscb_graph *g, int64_t R, int32_t precision, const v
 int oscb_graph_nonfinite(oscb_graph *g, int64_t where[3] /* replica, oscillator, step; -1 if none */,
                          int32_t reset);
 
+/* ---- the same row-sharded dense run FUSED: one persistent tensor-core kernel per rank ---------
+ * (csrc/oscb_umma.cuh).  J (integer couplings |J| <= 127, shards aligned to 128 rows) is streamed
+ * as int8 tile images through tcgen05.mma against the int8 digit planes of (cos, sin); the epilogue
+ * of every Euler step writes the new digits of the rank's rows straight into EVERY rank's next-step
+ * image (peer memory over NVLink: the per-step all-gather of oscb_dense_shard_step + NCCL becomes
+ * stores from inside the kernel), adds its part of the cut into every rank's event record
+ * (system-scope atomics) and arrives on every rank's step counter.  No host code runs between
+ * steps.  Replaces, per rank: trig precompute + _step_* + _score_kernel + sample() of
+ * dynamics.py:387-410 for the rank's rows, and the phase exchange between them.
+ *
+ *   create   : schedule (steps, sample steps, scoring cadence from `pair_count` of the WHOLE graph
+ *              when params->cadence == 0) and buffers for R <= 28 replicas
+ *   export   : OSCB_FUSED_MEM_BYTES describing this rank's exchange block (CUDA IPC handle +
+ *              address + grid size); all-gather these blobs over the ranks (any host transport)
+ *   connect  : map every peer's block (cudaIpcOpenMemHandle; plain addresses inside one process)
+ *   prepare  : zero the block, build the pass-0 state from phi0 ([R, n] of the WHOLE graph, or
+ *              NULL for the Philox initial phases).  Host-barrier over the ranks after this call.
+ *   launch   : enqueue the kernel (asynchronous)
+ *   finish   : wait; outputs as oscb_run, except final_phases / best_states hold THIS RANK's rows
+ *              only ([R, rows], rows from oscb_dense_fused_rows); objectives, traces and energies
+ *              are complete on every rank. */
+typedef struct oscb_fused oscb_fused;
+#define OSCB_FUSED_MEM_BYTES 96
+int oscb_dense_fused_create(oscb_graph *shard, const oscb_run_params *params, int64_t R, int64_t pair_count,
+                            int32_t world, int32_t rank, oscb_fused **out);
+int oscb_dense_fused_export(oscb_fused *f, void *mem /* [OSCB_FUSED_MEM_BYTES] */);
+int oscb_dense_fused_connect(oscb_fused *f, const void *all /* [world * OSCB_FUSED_MEM_BYTES], rank order */);
+int oscb_dense_fused_prepare(oscb_fused *f, const uint64_t *seeds /* [R] */, const double *phi0 /* [R, n] or NULL */);
+int oscb_dense_fused_launch(oscb_fused *f);
+int oscb_dense_fused_finish(oscb_fused *f, oscb_run_outputs *out);
+int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows);
+int oscb_dense_fused_destroy(oscb_fused *f);
+
 /* Device self-test behind the N = 2 scoring shortcut of the float32 kernel: counts the float32
  * phases in [0, 1) (all 2^30-ish of them) whose sign-of-cosine state differs from the reference
  * threshold (dynamics.py:203-213).  Must return 0 mismatches. */

@@ -23,6 +23,7 @@ OK, EINVAL, ECUDA, ENONFINITE, ENOMEM = 0, 1, 2, 3, 4
 OBJ = {"maxcut": 0, "coloring": 1}
 PREC = {"f32": 32, "f64": 64}
 NOISE_DEVICE, NOISE_HOST, NOISE_NONE = 0, 1, 2
+FUSED_MEM_BYTES = 96
 KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2, "dense-tc": 3}
 KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident", 3: "dense-tc"}
 
@@ -82,6 +83,14 @@ SYMBOLS = {
     "oscb_dense_shard_objective": (C.c_int, [_P, C.c_int64, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P]),
     "oscb_dense_shard_energy": (C.c_int, [_P, C.c_int64, C.c_int32, _P, _P, _P]),
     "oscb_graph_nonfinite": (C.c_int, [_P, _P, C.c_int32]),
+    "oscb_dense_fused_create": (C.c_int, [_P, C.POINTER(RunParams), C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "oscb_dense_fused_export": (C.c_int, [_P, _P]),
+    "oscb_dense_fused_connect": (C.c_int, [_P, _P]),
+    "oscb_dense_fused_prepare": (C.c_int, [_P, _P, _P]),
+    "oscb_dense_fused_launch": (C.c_int, [_P]),
+    "oscb_dense_fused_finish": (C.c_int, [_P, C.POINTER(RunOutputs)]),
+    "oscb_dense_fused_rows": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "oscb_dense_fused_destroy": (C.c_int, [_P]),
     "oscb_selftest_sign_state": (C.c_int, [C.c_int, C.POINTER(C.c_uint64)]),
     "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),

@@ -512,105 +512,128 @@ static bool umma_applies(const oscb_graph *g, const oscb_run_params *p)
            p->noise_mode != OSCB_NOISE_HOST && p->kernel != OSCB_KERNEL_STREAM;
 }
 
+// which passes score / sample: pass q integrates step q and first scores the phases it starts
+// from (= the reference's score after step q - 1, dynamics.py:404-410)
+struct UmmaSchedule {
+    std::vector<uint8_t> flags;            // [steps + 1]
+    std::vector<long long> event_step;     // step label of every scored pass (-1: initial sample)
+    std::vector<long long> sample_event;   // event index of every sample
+};
+
+static UmmaSchedule umma_schedule(const oscb_run_params *p, const RunPlan &rp)
+{
+    UmmaSchedule sc;
+    sc.flags.assign((size_t)rp.steps + 1, 0);
+    sc.flags[0] = 3;
+    sc.event_step.push_back(-1);
+    sc.sample_event.push_back(0);
+    size_t next_sample = 0;
+    for (int64_t step = 0; step < rp.steps; ++step) {
+        const int64_t gstep = p->first_step + step;
+        if (next_sample < rp.sample_steps.size() && rp.sample_steps[next_sample] == step) {
+            sc.flags[(size_t)step + 1] = 3;
+            sc.sample_event.push_back((long long)sc.event_step.size());
+            sc.event_step.push_back(gstep);
+            ++next_sample;
+        } else if (rp.cadence > 0 && gstep % rp.cadence == 0) {
+            sc.flags[(size_t)step + 1] = 1;
+            sc.event_step.push_back(gstep);
+        }
+    }
+    return sc;
+}
+
+static UmmaSpec umma_spec(const oscb_run_params *p, const RunPlan &rp, const UmmaSchedule &sc, int R)
+{
+    UmmaSpec sp{};
+    sp.R = R;
+    sp.precision = p->precision;
+    sp.noise_on = (p->noise_mode == OSCB_NOISE_DEVICE && p->kn != 0.0) ? 1 : 0;
+    sp.K = p->K; sp.h = p->h; sp.kn_sqrt_h = p->kn * std::sqrt(p->h); sp.ks_max = p->ks_max; sp.ks_period = p->ks_period;
+    sp.steps = rp.steps; sp.first_step = p->first_step;
+    sp.flags = sc.flags.data();
+    sp.n_events = (long long)sc.event_step.size();
+    sp.n_samples = rp.n_samples;
+    return sp;
+}
+
+// the score() / sample() bookkeeping of dynamics.py:370-384 replayed on the recorded cut sums
+// (ev[e][r] = 2 * cut of scored pass e) for replicas [r0, r0 + Rc) of the outputs
+static void umma_bookkeeping(const oscb_run_params *p, const UmmaSchedule &sc, const long long *ev, const double *en, int Rc,
+                             int r0, oscb_run_outputs *out)
+{
+    const long long E = (long long)sc.event_step.size();
+    for (int r = 0; r < Rc; ++r) {
+        double best = -std::numeric_limits<double>::infinity();
+        long long first = -1;
+        size_t k = 0;
+        for (long long e = 0; e < E; ++e) {
+            const double obj = 0.5 * (double)ev[(size_t)e * Rc + r];
+            if (obj > best) {
+                best = obj;
+                if (p->use_target && first < 0 && obj >= p->target_objective) first = sc.event_step[(size_t)e];
+            }
+            if (k < sc.sample_event.size() && sc.sample_event[k] == e) {
+                if (out->best_trace) out->best_trace[(size_t)(r0 + r) * out->max_samples + k] = best;
+                if (out->energy) out->energy[(size_t)(r0 + r) * out->max_samples + k] = en[k * Rc + r];
+                ++k;
+            }
+        }
+        if (out->best_objective) out->best_objective[r0 + r] = best;
+        if (out->first_hit_step) out->first_hit_step[r0 + r] = first;
+    }
+}
+
+static void umma_raise_nonfinite(unsigned long long flag, oscb_run_outputs *out)
+{
+    if (flag == ~0ull) return;
+    decode_nonfinite(flag, out->nonfinite);
+    set_error("non-finite phase for oscillator %lld (replica row %lld) after step %lld; parameters are numerically unstable",
+              (long long)out->nonfinite[1], (long long)out->nonfinite[0], (long long)out->nonfinite[2]);
+    throw OscbFail{OSCB_ENONFINITE};
+}
+
 static void run_umma(oscb_graph *g, const oscb_run_params *p, const RunPlan &rp, const uint64_t *seeds, int64_t R64,
                      const double *phi0, oscb_run_outputs *out)
 {
     cudaStream_t s = g->stream;
     const int R = (int)R64, n = (int)g->n;
     const size_t tot = (size_t)n * R;
-    const int64_t S = rp.n_samples, steps = rp.steps;
-    // pass q integrates step q and first scores the phases it starts from (= after step q - 1)
-    std::vector<uint8_t> flags((size_t)steps + 1, 0);
-    std::vector<long long> event_step;          // step label of every scored pass (-1: initial sample)
-    std::vector<long long> sample_event;        // event index of every sample
-    flags[0] = 3;
-    {
-        size_t next_sample = 0;
-        event_step.push_back(-1);
-        sample_event.push_back(0);
-        for (int64_t step = 0; step < steps; ++step) {
-            const int64_t gstep = p->first_step + step;
-            if (next_sample < rp.sample_steps.size() && rp.sample_steps[next_sample] == step) {
-                flags[(size_t)step + 1] = 3;
-                sample_event.push_back((long long)event_step.size());
-                event_step.push_back(gstep);
-                ++next_sample;
-            } else if (rp.cadence > 0 && gstep % rp.cadence == 0) {
-                flags[(size_t)step + 1] = 1;
-                event_step.push_back(gstep);
-            }
-        }
-    }
-    const long long E = (long long)event_step.size();
+    const int64_t S = rp.n_samples;
+    const UmmaSchedule sc = umma_schedule(p, rp);
+    const long long E = (long long)sc.event_step.size();
     DevBuf<double> io(tot);
     DevBuf<uint64_t> d_seeds(R);
     d_seeds.upload(seeds, R, s);
     if (phi0) io.upload(phi0, tot, s);
     else k_initial_phases<<<blocks_for((long long)((n + 3) / 4) * R, 128), 128, 0, s>>>(d_seeds.p, io.p, n, R);
     DevBuf<double> d_final(tot);
-    std::vector<uint8_t> h_states;
-    if (out->best_states) h_states.resize(tot);
     double ms = 0.0;
-    int64_t launches = 0;
+    int64_t launches = 0, smem = 0;
     unsigned long long flag = ~0ull;
-    UmmaSpec last{};
     for (int r0 = 0; r0 < R; r0 += kUmmaMaxReplicas) {
         const int Rc = std::min(kUmmaMaxReplicas, R - r0);
         std::vector<long long> ev((size_t)E * Rc);
         std::vector<double> en((size_t)S * Rc);
-        UmmaSpec sp{};
-        sp.R = Rc;
-        sp.precision = p->precision;
-        sp.noise_on = (p->noise_mode == OSCB_NOISE_DEVICE && p->kn != 0.0) ? 1 : 0;
-        sp.K = p->K; sp.h = p->h; sp.kn_sqrt_h = p->kn * std::sqrt(p->h); sp.ks_max = p->ks_max; sp.ks_period = p->ks_period;
-        sp.steps = steps; sp.first_step = p->first_step;
-        sp.flags = flags.data();
-        sp.n_events = E; sp.n_samples = S;
-        sp.seeds = seeds + r0;
-        sp.d_phi0 = io.p + (size_t)r0 * n;
-        sp.d_final = d_final.p + (size_t)r0 * n;
-        sp.h_best_states = out->best_states ? h_states.data() + (size_t)r0 * n : nullptr;
-        sp.h_events = ev.data();
-        sp.h_energy = en.data();
-        umma_run(g, *g->umma, sp);
-        ms += sp.ms;
+        UmmaSession ses(g, umma_spec(p, rp, sc, Rc), 1, 0);
+        ses.prepare(seeds + r0, io.p + (size_t)r0 * n);
+        ses.launch();
+        ses.export_final(d_final.p + (size_t)r0 * n);
+        ses.finish(nullptr, out->best_states ? out->best_states + (size_t)r0 * n : nullptr, ev.data(), en.data());
+        ms += ses.ms;
         launches += 1;
-        flag = std::min(flag, sp.nonfinite == ~0ull ? ~0ull : sp.nonfinite + ((unsigned long long)r0 << 20));
-        last = sp;
-        for (int r = 0; r < Rc; ++r) {
-            double best = -std::numeric_limits<double>::infinity();
-            long long first = -1;
-            size_t k = 0;
-            for (long long e = 0; e < E; ++e) {
-                const double obj = 0.5 * (double)ev[(size_t)e * Rc + r];
-                if (obj > best) {
-                    best = obj;
-                    if (p->use_target && first < 0 && obj >= p->target_objective) first = event_step[(size_t)e];
-                }
-                if (k < sample_event.size() && sample_event[k] == e) {
-                    if (out->best_trace) out->best_trace[(size_t)(r0 + r) * out->max_samples + k] = best;
-                    if (out->energy) out->energy[(size_t)(r0 + r) * out->max_samples + k] = en[k * Rc + r];
-                    ++k;
-                }
-            }
-            if (out->best_objective) out->best_objective[r0 + r] = best;
-            if (out->first_hit_step) out->first_hit_step[r0 + r] = first;
-        }
+        smem = (int64_t)ses.smem;
+        flag = std::min(flag, ses.nonfinite == ~0ull ? ~0ull : ses.nonfinite + ((unsigned long long)r0 << 20));
+        umma_bookkeeping(p, sc, ev.data(), en.data(), Rc, r0, out);
     }
     if (out->final_phases) d_final.download(out->final_phases, tot, s);
     OSCB_CUDA(cudaStreamSynchronize(s));
-    if (out->best_states) std::memcpy(out->best_states, h_states.data(), tot);
     out->device_ms = ms;
     out->kernel_launches = launches;
     out->kernel_used = OSCB_KERNEL_DENSE_TC;
     out->replicas_per_cta = std::min(R, kUmmaMaxReplicas);
-    out->smem_bytes = (int64_t)last.smem;
-    if (flag != ~0ull) {
-        decode_nonfinite(flag, out->nonfinite);
-        set_error("non-finite phase for oscillator %lld (replica row %lld) after step %lld; parameters are numerically unstable",
-                  (long long)out->nonfinite[1], (long long)out->nonfinite[0], (long long)out->nonfinite[2]);
-        throw OscbFail{OSCB_ENONFINITE};
-    }
+    out->smem_bytes = smem;
+    umma_raise_nonfinite(flag, out);
 }
 
 // workspace of the row-sharded dense driver: pairs and states of all n oscillators, row partials
@@ -678,6 +701,17 @@ static void shard_pairs_impl(oscb_graph *g, int R, int precision, const void *ph
 }
 
 } // namespace oscb
+
+// one rank of a fused row-sharded dense run (include/oscb.h: oscb_dense_fused_*)
+struct oscb_fused {
+    oscb_graph *g = nullptr;
+    oscb_run_params params{};
+    oscb::RunPlan rp;
+    oscb::UmmaSchedule sched;
+    std::unique_ptr<oscb::UmmaSession> session;
+    oscb::DevBuf<double> io;
+    int R = 0, world = 1, rank = 0;
+};
 
 using namespace oscb;
 
@@ -977,6 +1011,136 @@ int oscb_dense_shard_energy(oscb_graph *g, int64_t R, int32_t precision, const v
         if (precision == OSCB_PREC_F64) shard_pairs_impl<double>(g, (int)R, precision, phi_full_dev, 2, 2, partial_dev, s);
         else shard_pairs_impl<float>(g, (int)R, precision, phi_full_dev, 2, 2, partial_dev, s);
         check_launch("oscb_dense_shard_energy");
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_create(oscb_graph *shard, const oscb_run_params *p, int64_t R, int64_t pair_count, int32_t world,
+                            int32_t rank, oscb_fused **out)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(shard && p && out, "NULL argument");
+        *out = nullptr;
+        OSCB_REQUIRE(shard->is_dense && shard->umma, "fused dense runs need integer couplings |J| <= 127 and 128-row aligned shards");
+        OSCB_REQUIRE(p->n_states == 2 && p->objective == OSCB_OBJ_MAXCUT, "fused dense runs are N = 2 max-cut");
+        OSCB_REQUIRE(p->noise_mode != OSCB_NOISE_HOST, "fused dense runs draw their noise on the device");
+        OSCB_REQUIRE(p->precision == OSCB_PREC_F32 || p->precision == OSCB_PREC_F64, "unknown precision %d", p->precision);
+        OSCB_REQUIRE(R >= 1 && R <= kUmmaMaxReplicas, "fused dense runs take 1..%d replicas per session", kUmmaMaxReplicas);
+        OSCB_REQUIRE(p->h > 0.0 && std::isfinite(p->h) && p->ks_period > 0.0, "bad h / ks_period");
+        OSCB_REQUIRE(p->steps > 0 || (p->t_stop > 0.0 && std::isfinite(p->t_stop)), "t_stop must be finite and > 0");
+        bind_device(shard);
+        std::unique_ptr<oscb_fused> f(new oscb_fused());
+        f->g = shard;
+        f->params = *p;
+        f->R = (int)R;
+        f->world = world;
+        f->rank = rank;
+        f->rp = make_run_plan(shard, p);
+        if (p->cadence == 0) f->rp.cadence = reference_cadence(shard->n, pair_count);
+        OSCB_REQUIRE(f->rp.steps + p->first_step < (1ll << 28), "step index exceeds 2^28");
+        f->sched = umma_schedule(p, f->rp);
+        f->session.reset(new UmmaSession(shard, umma_spec(p, f->rp, f->sched, (int)R), world, rank));
+        f->io.alloc((size_t)shard->n * R);
+        *out = f.release();
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_export(oscb_fused *f, void *mem)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f && mem, "NULL argument");
+        static_assert(sizeof(UmmaExchange) == OSCB_FUSED_MEM_BYTES, "oscb.h: OSCB_FUSED_MEM_BYTES out of date");
+        f->session->export_mem(reinterpret_cast<UmmaExchange *>(mem));
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_connect(oscb_fused *f, const void *all)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f && all, "NULL argument");
+        f->session->connect(reinterpret_cast<const UmmaExchange *>(all));
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_prepare(oscb_fused *f, const uint64_t *seeds, const double *phi0)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f && seeds, "NULL argument");
+        bind_device(f->g);
+        cudaStream_t s = f->g->stream;
+        const int n = (int)f->g->n, R = f->R;
+        if (phi0) f->io.upload(phi0, (size_t)n * R, s);
+        else {
+            DevBuf<uint64_t> d_seeds(R);
+            d_seeds.upload(seeds, R, s);
+            k_initial_phases<<<blocks_for((long long)((n + 3) / 4) * R, 128), 128, 0, s>>>(d_seeds.p, f->io.p, n, R);
+            OSCB_CUDA(cudaStreamSynchronize(s));
+        }
+        f->session->prepare(seeds, f->io.p);
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_launch(oscb_fused *f)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f, "NULL argument");
+        f->session->launch();
+        check_launch("oscb_dense_fused_launch");
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_finish(oscb_fused *f, oscb_run_outputs *out)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f && out, "NULL argument");
+        const RunPlan &rp = f->rp;
+        const oscb_run_params *p = &f->params;
+        OSCB_REQUIRE((!out->energy && !out->best_trace && !out->trace_t && !out->trace_ks) || out->max_samples >= rp.n_samples,
+                     "trace buffers too small: need %lld samples, have %lld", (long long)rp.n_samples, (long long)out->max_samples);
+        const int R = f->R;
+        const long long E = (long long)f->sched.event_step.size(), S = rp.n_samples;
+        std::vector<long long> ev((size_t)E * R);
+        std::vector<double> en((size_t)S * R);
+        f->session->finish(out->final_phases, out->best_states, ev.data(), en.data());
+        out->n_samples = S;
+        out->steps_executed = rp.steps;
+        out->nonfinite[0] = out->nonfinite[1] = out->nonfinite[2] = -1;
+        for (int64_t k = 0; k < S; ++k) {
+            const double t = k == 0 ? (double)p->first_step * p->h : (double)(p->first_step + rp.sample_steps[k - 1] + 1) * p->h;
+            if (out->trace_t) out->trace_t[k] = t;
+            if (out->trace_ks) out->trace_ks[k] = ks_value(p->ks_max, p->ks_period, t);
+        }
+        umma_bookkeeping(p, f->sched, ev.data(), en.data(), R, 0, out);
+        out->device_ms = f->session->ms;
+        out->kernel_launches = 1;
+        out->kernel_used = OSCB_KERNEL_DENSE_TC;
+        out->replicas_per_cta = R;
+        out->smem_bytes = (int64_t)f->session->smem;
+        umma_raise_nonfinite(f->session->nonfinite, out);
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f && rows, "NULL argument");
+        *rows = f->session->rows();
+        return OSCB_OK;
+    });
+}
+
+int oscb_dense_fused_destroy(oscb_fused *f)
+{
+    if (!f) return OSCB_OK;
+    return guarded([&]() -> int {
+        bind_device(f->g);
+        delete f;
         return OSCB_OK;
     });
 }

@@ -2,8 +2,10 @@
 #include "oscb_umma.hpp"
 #include "oscb_umma.cuh"
 #include <algorithm>
-#include <cstdlib>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <unistd.h>
 #include <vector>
 
 namespace oscb {
@@ -28,128 +30,283 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
     return plan;
 }
 
-template <typename T>
-static void umma_run_t(oscb_graph *g, const UmmaPlan &plan, UmmaSpec &spec)
-{
-    cudaStream_t s = g->stream;
-    const int R = spec.R, n = plan.n;
-    OSCB_REQUIRE(R >= 1 && R <= UMMA_MAXR, "tensor-core dense path takes 1..%d replicas per launch", UMMA_MAXR);
+static inline size_t round256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct UmmaSession::Impl {
+    oscb_graph *g = nullptr;
+    const UmmaPlan *plan = nullptr;
+    UmmaSpec spec;
+    std::vector<uint8_t> flags;
+    int world = 1, rank = 0;
     UmmaArgs a{};
-    a.n = n;
-    a.tiles = plan.tiles;
-    a.tile_begin = plan.tile_begin;
-    a.tile_end = plan.tile_end;
-    a.R = R;
-    a.NB = (9 * R + 15) / 16 * 16;
-    const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage;
-    const size_t ctl = 2048, slack = 1024;
-    a.stages = (int)std::min<size_t>(12, ((size_t)g->smem_optin - ctl - slack) / stage);
-    OSCB_REQUIRE(a.stages >= 2, "not enough shared memory for the tensor-core dense pipeline");
-    const size_t smem = slack + (size_t)a.stages * stage + ctl;
-    a.world = 1;
-    a.rank = 0;
-    a.tmem_cols = 32;
-    while (a.tmem_cols < a.NB) a.tmem_cols *= 2;
-    const int lt = plan.tile_end - plan.tile_begin;
-    int grid = std::min(lt, g->sm_count);
-    if (const char *cap = getenv("OSCB_UMMA_MAX_GRID"))       // test knob: several row tiles per CTA on small graphs
-        grid = std::max(1, std::min(grid, atoi(cap)));
-    a.ctas_total = (unsigned)grid;
-    a.cta_offset = 0;
-    a.passes = spec.steps + 1;
-    a.first_step = spec.first_step;
-    a.K = spec.K; a.h = spec.h; a.kn_sqrt_h = spec.kn_sqrt_h; a.ks_max = spec.ks_max; a.ks_period = spec.ks_period;
-    a.tc = make_trig_const(2);
-    a.noise_on = spec.noise_on;
-    a.ld_phi = (long long)lt * UMMA_TILE;
-
-    DevBuf<uint8_t> B0((size_t)plan.tiles * b_stage), B1((size_t)plan.tiles * b_stage);
-    DevBuf<T> phi0((size_t)R * a.ld_phi), phi1((size_t)R * a.ld_phi);
-    DevBuf<uint64_t> d_seeds(R);
-    DevBuf<uint8_t> d_flags((size_t)a.passes), d_best((size_t)R * a.ld_phi);
-    DevBuf<unsigned int> d_bar(1);
-    DevBuf<long long> d_events((size_t)std::max<long long>(1, spec.n_events) * R);
-    DevBuf<double> d_en((size_t)std::max<long long>(1, spec.n_samples) * grid * R);
-    B0.zero(s); B1.zero(s); phi0.zero(s); phi1.zero(s); d_best.zero(s); d_bar.zero(s); d_events.zero(s); d_en.zero(s);
-    d_seeds.upload(spec.seeds, R, s);
-    d_flags.upload(spec.flags, (size_t)a.passes, s);
-    const unsigned long long none = ~0ull;
-    OSCB_CUDA(cudaMemcpyAsync(g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
-
-    a.A_img = plan.A_img.p;
-    a.B_img[0][0] = B0.p; a.B_img[1][0] = B1.p;
-    a.phi[0] = phi0.p; a.phi[1] = phi1.p;
-    a.W = plan.W.p;
-    a.seeds = d_seeds.p;
-    a.flags = d_flags.p;
-    a.bar[0] = d_bar.p;
-    a.events[0] = d_events.p;
-    a.en_part[0] = d_en.p;
-    a.best_states = d_best.p;
-    a.nonfinite = g->d_nonfinite.p;
-
+    // the exchange block (one cudaMalloc, so one IPC handle): [barrier counter | events | energy partials | B0 | B1]
+    unsigned char *xbase = nullptr;
+    size_t xbytes = 0, off_events = 0, off_en = 0, off_b[2] = {0, 0};
+    void *peer_base[kUmmaMaxWorld] = {};
+    bool peer_ipc[kUmmaMaxWorld] = {};
+    bool connected = false;
+    DevBuf<unsigned char> phi[2];
+    DevBuf<uint64_t> d_seeds;
+    DevBuf<uint8_t> d_flags, d_best;
     DevBuf<long long> d_trace;
-    const char *trace_path = getenv("OSCB_UMMA_TRACE");           // debug: per-CTA timeline of the first passes
-    if (trace_path) {
-        d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * 4);
-        d_trace.zero(s);
-        a.trace = d_trace.p;
-    }
-    const long long tot = (long long)n * R;
-    k_umma_init<T><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, spec.d_phi0);
-    OSCB_CUDA(cudaGetLastError());
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    size_t tsize = 4;
 
-    OSCB_CUDA(cudaFuncSetAttribute(k_dense_umma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaEvent_t ev0, ev1;
-    OSCB_CUDA(cudaEventCreate(&ev0));
-    OSCB_CUDA(cudaEventCreate(&ev1));
-    OSCB_CUDA(cudaEventRecord(ev0, s));
-    void *kargs[] = {(void *)&a};
-    OSCB_CUDA(cudaLaunchCooperativeKernel((const void *)k_dense_umma<T>, dim3((unsigned)grid), dim3(UMMA_THREADS), kargs, smem, s));
-    OSCB_CUDA(cudaEventRecord(ev1, s));
-
-    if (spec.d_final)
-        k_umma_export<T><<<(unsigned)(((long long)a.ld_phi * R + 255) / 256), 256, 0, s>>>(a, a.phi[(a.passes - 1) & 1], spec.d_final);
-    std::vector<double> h_en((size_t)std::max<long long>(1, spec.n_samples) * grid * R);
-    if (spec.h_events && spec.n_events) d_events.download(spec.h_events, (size_t)spec.n_events * R, s);
-    if (spec.h_energy && spec.n_samples) d_en.download(h_en.data(), (size_t)spec.n_samples * grid * R, s);
-    if (spec.h_best_states)
-        OSCB_CUDA(cudaMemcpy2DAsync(spec.h_best_states, (size_t)n, d_best.p, (size_t)a.ld_phi, (size_t)n, (size_t)R,
-                                    cudaMemcpyDeviceToHost, s));
-    OSCB_CUDA(cudaMemcpyAsync(&spec.nonfinite, g->d_nonfinite.p, sizeof(none), cudaMemcpyDeviceToHost, s));
-    OSCB_CUDA(cudaStreamSynchronize(s));
-    OSCB_CUDA(cudaEventElapsedTime(&spec.ms, ev0, ev1));
-    if (trace_path) {
-        std::vector<long long> h((size_t)grid * UMMA_TRACE_PASSES * 4);
-        OSCB_CUDA(cudaMemcpy(h.data(), d_trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-        if (FILE *f = fopen(trace_path, "w")) {
-            fprintf(f, "cta,pass,barrier_seen,tmem_full,arrived,barrier_wait_begin\n");
-            for (int c = 0; c < grid; ++c)
-                for (int q = 0; q < UMMA_TRACE_PASSES && q < a.passes; ++q) {
-                    const long long *t = &h[((size_t)c * UMMA_TRACE_PASSES + q) * 4];
-                    fprintf(f, "%d,%d,%lld,%lld,%lld,%lld\n", c, q, t[0], t[1], t[2], t[3]);
-                }
-            fclose(f);
-        }
+    void point_rank(int w, unsigned char *base)
+    {
+        a.bar[w] = reinterpret_cast<unsigned int *>(base);
+        a.events[w] = reinterpret_cast<long long *>(base + off_events);
+        a.en_part[w] = reinterpret_cast<double *>(base + off_en);
+        a.B_img[0][w] = base + off_b[0];
+        a.B_img[1][w] = base + off_b[1];
     }
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    if (spec.h_energy)
-        for (long long k = 0; k < spec.n_samples; ++k)
-            for (int r = 0; r < R; ++r) {
-                double e = 0.0;
-                for (int c = 0; c < grid; ++c) e += h_en[((size_t)k * grid + c) * R + r];   // CTA order: deterministic
-                spec.h_energy[k * R + r] = e;
-            }
-    spec.grid = grid;
-    spec.stages = a.stages;
-    spec.smem = smem;
+};
+
+UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int rank) : m(new Impl())
+{
+    try {
+        OSCB_REQUIRE(g && g->umma, "handle has no tensor-core plan (integer couplings |J| <= 127 on 128-row aligned shards)");
+        OSCB_REQUIRE(spec.R >= 1 && spec.R <= UMMA_MAXR, "tensor-core dense path takes 1..%d replicas per launch", UMMA_MAXR);
+        OSCB_REQUIRE(world >= 1 && world <= kUmmaMaxWorld && rank >= 0 && rank < world, "bad world / rank %d / %d", world, rank);
+        m->g = g;
+        m->plan = g->umma.get();
+        m->spec = spec;
+        m->flags.assign(spec.flags, spec.flags + spec.steps + 1);
+        m->spec.flags = m->flags.data();
+        m->world = world;
+        m->rank = rank;
+        m->tsize = spec.precision == OSCB_PREC_F64 ? 8 : 4;
+        const UmmaPlan &plan = *m->plan;
+        UmmaArgs &a = m->a;
+        a.n = plan.n;
+        a.tiles = plan.tiles;
+        a.tile_begin = plan.tile_begin;
+        a.tile_end = plan.tile_end;
+        a.R = spec.R;
+        a.NB = (9 * spec.R + 15) / 16 * 16;
+        const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage;
+        const size_t ctl = 2048, slack = 1024;
+        a.stages = (int)std::min<size_t>(12, ((size_t)g->smem_optin - ctl - slack) / stage);
+        OSCB_REQUIRE(a.stages >= 2, "not enough shared memory for the tensor-core dense pipeline");
+        smem = slack + (size_t)a.stages * stage + ctl;
+        stages = a.stages;
+        a.world = world;
+        a.rank = rank;
+        a.tmem_cols = 32;
+        while (a.tmem_cols < a.NB) a.tmem_cols *= 2;
+        const int lt = plan.tile_end - plan.tile_begin;
+        grid = std::min(lt, g->sm_count);
+        if (const char *cap = getenv("OSCB_UMMA_MAX_GRID"))       // test knob: several row tiles per CTA on small graphs
+            grid = std::max(1, std::min(grid, atoi(cap)));
+        a.ctas_total = (unsigned)grid;                            // world = 1; connect() fills in the real totals
+        a.cta_offset = 0;
+        a.passes = spec.steps + 1;
+        a.first_step = spec.first_step;
+        a.K = spec.K; a.h = spec.h; a.kn_sqrt_h = spec.kn_sqrt_h; a.ks_max = spec.ks_max; a.ks_period = spec.ks_period;
+        a.tc = make_trig_const(2);
+        a.noise_on = spec.noise_on;
+        a.ld_phi = (long long)lt * UMMA_TILE;
+
+        const size_t E = (size_t)std::max<long long>(1, spec.n_events), S = (size_t)std::max<long long>(1, spec.n_samples);
+        m->off_events = 256;
+        m->off_en = m->off_events + round256(E * spec.R * sizeof(long long));
+        m->off_b[0] = m->off_en + round256(S * (size_t)plan.tiles * spec.R * sizeof(double));   // <= one CTA per tile, all ranks
+        m->off_b[1] = m->off_b[0] + round256((size_t)plan.tiles * b_stage);
+        m->xbytes = m->off_b[1] + round256((size_t)plan.tiles * b_stage);
+        OSCB_CUDA(cudaSetDevice(g->device));
+        OSCB_CUDA(cudaMalloc(&m->xbase, m->xbytes));              // not pooled: the block is exported over CUDA IPC
+        m->point_rank(rank, m->xbase);
+        m->peer_base[rank] = m->xbase;
+        m->connected = world == 1;
+
+        for (int k = 0; k < 2; ++k) { m->phi[k].alloc((size_t)spec.R * a.ld_phi * m->tsize); a.phi[k] = m->phi[k].p; }
+        m->d_seeds.alloc(spec.R);
+        m->d_flags.alloc((size_t)a.passes);
+        m->d_best.alloc((size_t)spec.R * a.ld_phi);
+        a.A_img = plan.A_img.p;
+        a.W = plan.W.p;
+        a.seeds = m->d_seeds.p;
+        a.flags = m->d_flags.p;
+        a.best_states = m->d_best.p;
+        a.nonfinite = g->d_nonfinite.p;
+        a.trace = nullptr;
+        OSCB_CUDA(cudaEventCreate(&m->ev0));
+        OSCB_CUDA(cudaEventCreate(&m->ev1));
+    } catch (...) {
+        if (m->xbase) cudaFree(m->xbase);
+        delete m;
+        m = nullptr;
+        throw;
+    }
 }
 
-void umma_run(oscb_graph *g, const UmmaPlan &plan, UmmaSpec &spec)
+UmmaSession::~UmmaSession()
 {
-    if (spec.precision == OSCB_PREC_F64) umma_run_t<double>(g, plan, spec);
-    else umma_run_t<float>(g, plan, spec);
+    if (!m) return;
+    cudaSetDevice(m->g->device);
+    cudaStreamSynchronize(m->g->stream);
+    for (int w = 0; w < m->world; ++w)
+        if (m->peer_ipc[w] && m->peer_base[w]) cudaIpcCloseMemHandle(m->peer_base[w]);
+    if (m->xbase) cudaFree(m->xbase);
+    if (m->ev0) cudaEventDestroy(m->ev0);
+    if (m->ev1) cudaEventDestroy(m->ev1);
+    delete m;
+}
+
+int UmmaSession::rows() const
+{
+    return std::min(m->a.n, m->a.tile_end * UMMA_TILE) - m->a.tile_begin * UMMA_TILE;
+}
+
+void UmmaSession::export_mem(UmmaExchange *out) const
+{
+    std::memset(out, 0, sizeof(*out));
+    cudaIpcMemHandle_t h;
+    OSCB_CUDA(cudaSetDevice(m->g->device));
+    OSCB_CUDA(cudaIpcGetMemHandle(&h, m->xbase));
+    static_assert(sizeof(h) <= sizeof(out->ipc), "IPC handle does not fit");
+    std::memcpy(out->ipc, &h, sizeof(h));
+    out->base = (uint64_t)(uintptr_t)m->xbase;
+    out->bytes = m->xbytes;
+    out->device = m->g->device;
+    out->pid = (int32_t)getpid();
+    out->grid = grid;
+}
+
+void UmmaSession::connect(const UmmaExchange *all)
+{
+    OSCB_CUDA(cudaSetDevice(m->g->device));
+    unsigned total = 0;
+    for (int w = 0; w < m->world; ++w) {
+        const UmmaExchange &x = all[w];
+        OSCB_REQUIRE(x.bytes == m->xbytes, "rank %d exchange block is %llu bytes, expected %zu (replicas / schedule differ?)", w,
+                     (unsigned long long)x.bytes, m->xbytes);
+        if (w == m->rank) m->a.cta_offset = (int)total;
+        total += (unsigned)x.grid;
+        if (w == m->rank) continue;
+        if (x.pid == (int32_t)getpid()) {
+            // same process (one process driving several GPUs, or virtual ranks on one GPU): the address is valid as is
+            if (x.device != m->g->device) {
+                int can = 0;
+                OSCB_CUDA(cudaDeviceCanAccessPeer(&can, m->g->device, x.device));
+                OSCB_REQUIRE(can, "device %d cannot access device %d", m->g->device, x.device);
+                cudaError_t e = cudaDeviceEnablePeerAccess(x.device, 0);
+                if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+                else OSCB_CUDA(e);
+            }
+            m->peer_base[w] = (void *)(uintptr_t)x.base;
+        } else {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, x.ipc, sizeof(h));
+            OSCB_CUDA(cudaIpcOpenMemHandle(&m->peer_base[w], h, cudaIpcMemLazyEnablePeerAccess));
+            m->peer_ipc[w] = true;
+        }
+        m->point_rank(w, (unsigned char *)m->peer_base[w]);
+    }
+    m->a.ctas_total = total;
+    m->connected = true;
+}
+
+void UmmaSession::prepare(const uint64_t *seeds, const double *d_phi0)
+{
+    OSCB_REQUIRE(m->connected, "connect() the ranks before prepare()");
+    cudaStream_t s = m->g->stream;
+    UmmaArgs &a = m->a;
+    OSCB_CUDA(cudaSetDevice(m->g->device));
+    OSCB_CUDA(cudaMemsetAsync(m->xbase, 0, m->xbytes, s));
+    m->phi[0].zero(s); m->phi[1].zero(s); m->d_best.zero(s);
+    m->d_seeds.upload(seeds, a.R, s);
+    m->d_flags.upload(m->flags.data(), (size_t)a.passes, s);
+    const unsigned long long none = ~0ull;
+    OSCB_CUDA(cudaMemcpyAsync(m->g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    if (const char *trace_path = getenv("OSCB_UMMA_TRACE")) {     // debug: per-CTA timeline of the first passes
+        (void)trace_path;
+        m->d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * 4);
+        m->d_trace.zero(s);
+        a.trace = m->d_trace.p;
+    }
+    const long long tot = (long long)a.n * a.R;
+    if (m->tsize == 8) k_umma_init<double><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, d_phi0);
+    else k_umma_init<float><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, d_phi0);
+    OSCB_CUDA(cudaGetLastError());
+    OSCB_CUDA(cudaStreamSynchronize(s));      // the block is clean and initialised when prepare() returns
+}
+
+void UmmaSession::launch()
+{
+    cudaStream_t s = m->g->stream;
+    OSCB_CUDA(cudaSetDevice(m->g->device));
+    const void *fn = m->tsize == 8 ? (const void *)k_dense_umma<double> : (const void *)k_dense_umma<float>;
+    OSCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    OSCB_CUDA(cudaEventRecord(m->ev0, s));
+    void *kargs[] = {(void *)&m->a};
+    OSCB_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(UMMA_THREADS), kargs, smem, s));
+    OSCB_CUDA(cudaEventRecord(m->ev1, s));
+}
+
+void UmmaSession::export_final(double *d_final_full)
+{
+    cudaStream_t s = m->g->stream;
+    const UmmaArgs &a = m->a;
+    const unsigned blocks = (unsigned)(((long long)a.ld_phi * a.R + 255) / 256);
+    const void *fin = a.phi[(a.passes - 1) & 1];
+    if (m->tsize == 8) k_umma_export<double><<<blocks, 256, 0, s>>>(a, fin, d_final_full, a.n, (long long)a.tile_begin * UMMA_TILE);
+    else k_umma_export<float><<<blocks, 256, 0, s>>>(a, fin, d_final_full, a.n, (long long)a.tile_begin * UMMA_TILE);
+    OSCB_CUDA(cudaGetLastError());
+}
+
+void UmmaSession::finish(double *h_final_rows, uint8_t *h_best_rows, long long *h_events, double *h_energy)
+{
+    cudaStream_t s = m->g->stream;
+    const UmmaArgs &a = m->a;
+    const int R = a.R, nrows = rows();
+    const long long E = m->spec.n_events, S = m->spec.n_samples;
+    const unsigned ctas = a.ctas_total;
+    OSCB_CUDA(cudaSetDevice(m->g->device));
+    DevBuf<double> d_rows;
+    if (h_final_rows) {
+        d_rows.alloc((size_t)R * nrows);
+        const unsigned blocks = (unsigned)(((long long)a.ld_phi * R + 255) / 256);
+        const void *fin = a.phi[(a.passes - 1) & 1];
+        if (m->tsize == 8) k_umma_export<double><<<blocks, 256, 0, s>>>(a, fin, d_rows.p, nrows, 0);
+        else k_umma_export<float><<<blocks, 256, 0, s>>>(a, fin, d_rows.p, nrows, 0);
+        OSCB_CUDA(cudaGetLastError());
+        d_rows.download(h_final_rows, (size_t)R * nrows, s);
+    }
+    std::vector<double> h_en;
+    if (h_events && E) OSCB_CUDA(cudaMemcpyAsync(h_events, m->xbase + m->off_events, (size_t)E * R * sizeof(long long), cudaMemcpyDeviceToHost, s));
+    if (h_energy && S) {
+        h_en.resize((size_t)S * ctas * R);
+        OSCB_CUDA(cudaMemcpyAsync(h_en.data(), m->xbase + m->off_en, h_en.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (h_best_rows)
+        OSCB_CUDA(cudaMemcpy2DAsync(h_best_rows, (size_t)nrows, m->d_best.p, (size_t)a.ld_phi, (size_t)nrows, (size_t)R,
+                                    cudaMemcpyDeviceToHost, s));
+    OSCB_CUDA(cudaMemcpyAsync(&nonfinite, m->g->d_nonfinite.p, sizeof(nonfinite), cudaMemcpyDeviceToHost, s));
+    OSCB_CUDA(cudaStreamSynchronize(s));
+    OSCB_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    if (h_energy)
+        for (long long k = 0; k < S; ++k)
+            for (int r = 0; r < R; ++r) {
+                double e = 0.0;
+                for (unsigned c = 0; c < ctas; ++c) e += h_en[((size_t)k * ctas + c) * R + r];   // CTA order: deterministic
+                h_energy[k * R + r] = e;
+            }
+    if (const char *trace_path = getenv("OSCB_UMMA_TRACE")) {
+        if (m->d_trace.p) {
+            std::vector<long long> h((size_t)grid * UMMA_TRACE_PASSES * 4);
+            OSCB_CUDA(cudaMemcpy(h.data(), m->d_trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+            if (FILE *f = fopen(trace_path, "w")) {
+                fprintf(f, "cta,pass,barrier_seen,tmem_full,arrived,barrier_wait_begin\n");
+                for (int c = 0; c < grid; ++c)
+                    for (int q = 0; q < UMMA_TRACE_PASSES && q < a.passes; ++q) {
+                        const long long *t = &h[((size_t)c * UMMA_TRACE_PASSES + q) * 4];
+                        fprintf(f, "%d,%d,%lld,%lld,%lld,%lld\n", c, q, t[0], t[1], t[2], t[3]);
+                    }
+                fclose(f);
+            }
+        }
+    }
 }
 
 } // namespace oscb

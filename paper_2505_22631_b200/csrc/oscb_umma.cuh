@@ -215,15 +215,16 @@ __global__ void k_umma_init(UmmaArgs a, const double *__restrict__ phi0)
     if (j >= row0 && j < row1) reinterpret_cast<T *>(a.phi[0])[(long long)r * a.ld_phi + (j - row0)] = p;
 }
 
-// this rank's rows back to the host layout [R][n] (only the local columns are written)
+// this rank's rows as float64: out[r * ld_out + col0 + i] (col0 = first row and ld_out = n for
+// the host layout [R][n]; col0 = 0 and ld_out = rows for the rank's own slice)
 template <typename T>
-__global__ void k_umma_export(UmmaArgs a, const void *phi, double *__restrict__ out)
+__global__ void k_umma_export(UmmaArgs a, const void *phi, double *__restrict__ out, long long ld_out, long long col0)
 {
     const int rows = min(a.n, a.tile_end * UMMA_TILE) - a.tile_begin * UMMA_TILE;
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= (long long)rows * a.R) return;
     const int r = (int)(q / rows), i = (int)(q % rows);
-    out[(long long)r * a.n + a.tile_begin * UMMA_TILE + i] = (double)reinterpret_cast<const T *>(phi)[(long long)r * a.ld_phi + i];
+    out[(long long)r * ld_out + col0 + i] = (double)reinterpret_cast<const T *>(phi)[(long long)r * a.ld_phi + i];
 }
 
 // int8 J rows [rows][n_pad] -> swizzled tile images + row sums

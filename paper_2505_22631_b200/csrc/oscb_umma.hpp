@@ -18,8 +18,21 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
                                           cudaStream_t s);
 
 constexpr int kUmmaMaxReplicas = 28;
+constexpr int kUmmaMaxWorld = 8;
 
-// One run of up to kUmmaMaxReplicas replicas on ONE GPU holding the whole graph.
+// what one rank of a row-sharded run publishes about its exchange block (the memory its peers
+// push phase digits, cut sums, energy partials and barrier arrivals into)
+struct UmmaExchange {
+    unsigned char ipc[64];   // cudaIpcMemHandle_t of the block
+    uint64_t base;           // device address in the owning process
+    uint64_t bytes;
+    int32_t device;
+    int32_t pid;
+    int32_t grid;            // CTAs this rank launches
+    int32_t reserved;
+};
+
+// schedule and parameters of one run of <= kUmmaMaxReplicas replicas
 struct UmmaSpec {
     int R = 1;
     int precision = OSCB_PREC_F32;
@@ -28,19 +41,38 @@ struct UmmaSpec {
     long long steps = 0, first_step = 0;
     const uint8_t *flags = nullptr;     // host [steps + 1]: bit 0 score the pass's input phases, bit 1 + energy sample
     long long n_events = 0, n_samples = 0;
-    const uint64_t *seeds = nullptr;    // host [R]
-    const double *d_phi0 = nullptr;     // device [R][n] float64, host layout
-    double *d_final = nullptr;          // device [R][n] float64 (may be null)
-    uint8_t *h_best_states = nullptr;   // host [R][n] (may be null)
-    long long *h_events = nullptr;      // host [n_events][R]: 2 * cut of every scored pass
-    double *h_energy = nullptr;         // host [n_samples][R]
-    // filled by the run
+};
+
+// One rank's side of a run: the whole graph on one GPU (world = 1) or a 128-row-aligned shard of
+// it, with the per-step exchange pushed into the peers' blocks by the kernel itself.
+class UmmaSession {
+public:
+    UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int rank);
+    ~UmmaSession();
+    UmmaSession(const UmmaSession &) = delete;
+    UmmaSession &operator=(const UmmaSession &) = delete;
+
+    void export_mem(UmmaExchange *out) const;
+    void connect(const UmmaExchange *all);                       // [world]; world = 1 needs no call
+    // zero the exchange block, upload seeds, build this rank's phases and the pass-0 digit image
+    // from d_phi0 (device, float64 [R][n]).  Every rank must have prepared before any rank launches.
+    void prepare(const uint64_t *seeds, const double *d_phi0);
+    void launch();                                               // asynchronous on the handle's stream
+    // wait for the kernel; rows = this rank's rows.  Any pointer may be null.
+    void finish(double *h_final_rows /* [R][rows] */, uint8_t *h_best_rows /* [R][rows] */, long long *h_events /* [E][R] */,
+                double *h_energy /* [S][R] */);
+    // same, but the final phases go to a device buffer in the host layout [R][n] (world = 1 path)
+    void export_final(double *d_final_full);
+
+    int rows() const;
     float ms = 0.f;
     int grid = 0, stages = 0;
     size_t smem = 0;
     unsigned long long nonfinite = ~0ull;
-};
 
-void umma_run(oscb_graph *g, const UmmaPlan &plan, UmmaSpec &spec);
+private:
+    struct Impl;
+    Impl *m;
+};
 
 } // namespace oscb

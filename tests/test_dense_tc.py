@@ -105,3 +105,31 @@ def test_replica_chunks_equal_single_runs(pkg):
         assert solo.best_objective[0] == allr.best_objective[r]
         assert np.array_equal(solo.energy[0], allr.energy[r])
         assert solo.first_hit_step[0] == allr.first_hit_step[r]
+
+
+@pytest.mark.parametrize("n,cuts,precision", [
+    (512, (0, 256, 512), "f32"),
+    (600, (0, 256, 600), "f64"),          # ragged last shard
+    (600, (0, 128, 384, 600), "f32"),     # three ranks
+])
+def test_fused_virtual_ranks_equal_single_handle(pkg, n, cuts, precision):
+    """The multi-GPU protocol of the fused kernel (peer-pointer push of the digit planes, cut atomics
+    and step-counter arrivals into every rank's exchange block) with the ranks as concurrent kernels
+    on ONE GPU: row shards of J, one persistent kernel each, must reproduce the single-handle run bit
+    for bit (noise on; the integer sums are exact, so sharding cannot change a bit)."""
+    from paper_2505_22631_b200 import dense_fused
+    R = 3
+    J = sk_graph(n, 5)
+    Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.2, h=0.01, t_stop=1.2, seed=40)
+    seeds = [40, 41, 42]
+    want = pkg.run_batch(Jd, params, "maxcut", seeds, precision=precision, kernel="dense-tc", target=0.0)
+    shards = [(J[a:b], a, b, 0) for a, b in zip(cuts[:-1], cuts[1:])]
+    got = dense_fused.run_fused_in_process(shards, n, params, seeds, pair_count=n * (n - 1) // 2, precision=precision)
+    assert got.steps == want.steps == 120
+    assert np.array_equal(got.final_phases, want.final_phases)
+    assert np.array_equal(got.best_states, want.best_states)
+    assert np.array_equal(got.best_objective, want.best_objective)
+    assert np.array_equal(got.trace_t, want.trace_t) and np.array_equal(got.trace_ks, want.trace_ks)
+    assert np.array_equal(got.best_trace, want.best_trace)
+    assert np.array_equal(got.energy, want.energy)
