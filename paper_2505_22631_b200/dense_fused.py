@@ -181,19 +181,22 @@ def run_fused_in_process(shards: Sequence[tuple], n: int, params: SolverParams, 
             rk.close()
 
 
-def run_dense_fused(J_rows: np.ndarray, n: int, row_begin: int, row_end: int, params: SolverParams, seeds: Sequence[int],
-                    *, device: int, pair_count: int, phi0: Optional[np.ndarray] = None, group=None, **kw) -> BatchResult:
+def run_dense_fused(J_rows: Optional[np.ndarray], n: int, row_begin: int, row_end: int, params: SolverParams,
+                    seeds: Sequence[int], *, device: int, pair_count: int, phi0: Optional[np.ndarray] = None, group=None,
+                    graph=None, **kw) -> BatchResult:
     """This process's rank of a fused run over the ranks of `group` (torch.distributed; one process
-    per GPU).  Every rank returns the assembled result of the whole graph."""
+    per GPU).  Every rank returns the assembled result of the whole graph.  `graph` reuses an
+    already uploaded shard handle (`oscb_graph_create_dense` with the same rows; J_rows may then be
+    None) and leaves it alive."""
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()):
-        return run_fused_in_process([(J_rows, row_begin, row_end, device)], n, params, seeds, pair_count=pair_count,
-                                    device=device, phi0=phi0, **kw)
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+        rank, world = 0, 1
+    else:
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
     if phi0 is None:
         phi0 = _initial_phases_host(device, seeds, n)          # the reference's Philox stream, identical on every rank
     phi0 = np.asarray(phi0, dtype=np.float64).reshape(len(seeds), n)
-    graph = None
+    keep_graph = graph is not None
     out: List[BatchResult] = []
     try:
         for r0 in range(0, len(seeds), MAX_REPLICAS):
@@ -204,20 +207,28 @@ def run_dense_fused(J_rows: np.ndarray, n: int, row_begin: int, row_end: int, pa
             graph = rk.graph
             try:
                 blobs: List[Optional[bytes]] = [None] * world
-                dist.all_gather_object(blobs, rk.export(), group=group)
+                if world > 1:
+                    dist.all_gather_object(blobs, rk.export(), group=group)
+                else:
+                    blobs = [rk.export()]
                 rk.connect(blobs)
                 rk.prepare(chunk, phi0[r0:r0 + len(chunk)])
-                dist.barrier(group=group)                      # every block is clean before any rank pushes into it
+                if world > 1:
+                    dist.barrier(group=group)                  # every block is clean before any rank pushes into it
                 rk.launch()
                 mine = rk.finish()
                 parts: List[Optional[BatchResult]] = [None] * world
-                dist.all_gather_object(parts, mine, group=group)
+                if world > 1:
+                    dist.all_gather_object(parts, mine, group=group)
+                else:
+                    parts = [mine]
                 out.append(assemble(parts))
-                dist.barrier(group=group)                      # nobody unmaps a block a peer may still read
+                if world > 1:
+                    dist.barrier(group=group)                  # nobody unmaps a block a peer may still read
             finally:
                 rk.close()
     finally:
-        if graph:
+        if graph and not keep_graph:
             nat.lib().oscb_graph_destroy(graph)
     if len(out) == 1:
         return out[0]
