@@ -11,8 +11,9 @@
 // A warp owns one row at a time and RB replicas of it: the 32 lanes stride over the columns, each
 // J entry is loaded once and applied to the RB replicas' pairs, the lanes' partial sums are
 // combined with a shuffle tree, and lanes 0..RB-1 run the epilogue of one replica each.
-// R = 1 is a GEMV bound by the HBM read of J; for many replicas this SIMT form is compute bound
-// (the tensor-core version is future work).  Summation order is a fixed tree, not the
+// R = 1 is a GEMV bound by the HBM read of J; for many replicas this SIMT form is compute bound.
+// Integer couplings with N = 2 run on the tensor-core kernel instead (oscb_umma.cuh); this is the
+// general dense path (any weights, any N, host-injected noise) and the single-step entry point.  Summation order is a fixed tree, not the
 // reference's sequential CSR order, so dense float64 parity is to rounding (~1e-13), not bitwise.
 //
 // Reference arithmetic restated: dynamics.py:166-172 (row update), :214-223 (objectives),
