@@ -11,9 +11,9 @@
 //     tile's L2-resident slab;
 //   * N = 2 (OIM / max-cut, NMODE == 2): the SHIL harmonic is 2 s c, and scoring costs one
 //     LEA.HI per gather on the step AFTER a scored step: with c_j = cospi(2 phi_j) already in
-//     a register, [c_j < 0] IS the lattice state of j (0.25 < phi < 0.75, dynamics.py:203-213;
-//     pass B canonicalises -0 to +0, and tests/ check the equivalence over every float in
-//     [0, 1)).  A row contributes deg - neg or neg differing neighbours depending on its own
+//     a register, its SIGN BIT is the lattice state of j (0.25 < phi < 0.75, dynamics.py:203-213;
+//     trig_turns_fast sets the bit from that exact comparison, and oscb_selftest_sign_state checks
+//     it over every float in [0, 1)).  A row contributes deg - neg or neg differing neighbours depending on its own
 //     state; the tile sum is twice the cut.  Trace samples and the first/last state still go
 //     through the explicit scoring pass;
 //   * other N (NMODE == 0): lattice states as bytes in shared memory, explicit scoring pass;
@@ -83,6 +83,27 @@ __device__ __forceinline__ void normals4_fast(uint4 x, float &z0, float &z1, flo
     z2 = r1 * __cosf(a1); z3 = r1 * __sinf(a1);
 }
 
+// (sin, cos) of 2 pi y for a phase y in [0, 1), in ~17 instructions instead of sincospif's ~32:
+// exact reduction to a quarter turn (4y - rint(4y) is exact), the two MUFU approximations on
+// |angle| <= pi/4 (abs. error ~4e-7, about the rounding of float32 near 1), quadrant fix-up by
+// swap / sign flips.  The SIGN BIT of the cosine is then set from the exact comparison
+// 0.25 < y < 0.75, i.e. it IS the N = 2 lattice state of the reference (dynamics.py:203-213; ties
+// at 0.25 / 0.75 -> state 0), also when the approximate magnitude underflows to zero: -0 carries
+// state 1.  Consumers read the state from the bit, never from "c < 0".
+__device__ __forceinline__ void trig_turns_fast(float y, float &s, float &c)
+{
+    const float t = 4.0f * y;
+    const float qf = rintf(t);
+    const float ang = (t - qf) * 1.5707963267948966f;
+    const float sr = __sinf(ang), cr = __cosf(ang);
+    const int qi = (int)qf;
+    const bool odd = qi & 1;
+    const float s0 = odd ? cr : sr, c0 = odd ? sr : cr;
+    s = __uint_as_float(__float_as_uint(s0) ^ ((uint32_t)(qi & 2) << 30));
+    const uint32_t state = (y > 0.25f && y < 0.75f) ? 0x80000000u : 0u;
+    c = __uint_as_float((__float_as_uint(c0) & 0x7FFFFFFFu) | state);
+}
+
 // Everything the kernel needs, precomputed on the host so that the hot loops read constants
 // straight from the parameter bank instead of re-deriving them under register pressure.
 struct FastArgs {
@@ -124,9 +145,13 @@ __global__ void k_selftest_sign_state(unsigned long long *mismatches)
          q += (unsigned long long)gridDim.x * blockDim.x) {
         const float p = __uint_as_float((uint32_t)q);
         float s, co;
-        sincospif(2.0f * p, &s, &co);
-        const uint32_t by_sign = __float_as_uint(co + 0.0f) >> 31;
+        trig_turns_fast(p, s, co);
+        const uint32_t by_sign = __float_as_uint(co) >> 31;
         if (by_sign != (uint32_t)threshold_state((double)p, 2)) ++bad;
+        // and the values themselves stay within the MUFU error of the exact ones
+        float s_ref, c_ref;
+        sincospif(2.0f * p, &s_ref, &c_ref);
+        if (!(fabsf(s - s_ref) <= 2e-6f && fabsf(co - c_ref) <= 2e-6f)) ++bad;
     }
     if (bad) atomicAdd(mismatches, bad);
 }
@@ -273,8 +298,8 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         for (int i = tid; i < a.nRT; i += NT) {
             const float p = slab[i];
             float s, co;
-            sincospif(2.0f * p, &s, &co);
-            cs[i] = make_float2(co + 0.0f, s);
+            trig_turns_fast(p, s, co);
+            cs[i] = make_float2(co, s);
             if (PHI_SMEM) phis[i] = p;
         }
         for (int i = tid; i < OSCB_PAD_ROWS * a.RT; i += NT) {
@@ -514,8 +539,8 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                             sum[e] = __ffma2_rn(make_float2(w4.y, w4.y), v1.v[e], sum[e]);
                             sum[e] = __ffma2_rn(make_float2(w4.z, w4.z), v2.v[e], sum[e]);
                             sum[e] = __ffma2_rn(make_float2(w4.w, w4.w), v3.v[e], sum[e]);
-                            negw[e] += (v0.v[e].x < 0.f ? w4.x : 0.f) + (v1.v[e].x < 0.f ? w4.y : 0.f);
-                            negw[e] += (v2.v[e].x < 0.f ? w4.z : 0.f) + (v3.v[e].x < 0.f ? w4.w : 0.f);
+                            negw[e] += (__float_as_int(v0.v[e].x) < 0 ? w4.x : 0.f) + (__float_as_int(v1.v[e].x) < 0 ? w4.y : 0.f);
+                            negw[e] += (__float_as_int(v2.v[e].x) < 0 ? w4.z : 0.f) + (__float_as_int(v3.v[e].x) < 0 ? w4.w : 0.f);
                         }
                     } else {
 #pragma unroll
@@ -565,8 +590,9 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                 for (int e = 0; e < RPL; ++e) {
                     const float ci = own.v[e].x, si = own.v[e].y;
                     if (PIGGY && count_now) {   // differing neighbours: deg - neg if the row itself is in state 1
-                        if (WEIGHTED) twice_cut_w[e] += (ci < 0.f) ? wrow - negw[e] : negw[e];
-                        else twice_cut[e] += (ci < 0.f) ? deg - neg[e] : neg[e];
+                        const bool own1 = __float_as_int(ci) < 0;        // the row's own state: the sign BIT
+                        if (WEIGHTED) twice_cut_w[e] += own1 ? wrow - negw[e] : negw[e];
+                        else twice_cut[e] += own1 ? deg - neg[e] : neg[e];
                     }
                     const float acc = si * sum[e].x - ci * sum[e].y;
                     float shil;
@@ -584,8 +610,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     float s2[RPL], c2[RPL];
 #pragma unroll
                     for (int e = 0; e < RPL; ++e) {
-                        sincospif(2.0f * y[e], &s2[e], &c2[e]);
-                        c2[e] += 0.0f;
+                        trig_turns_fast(y[e], s2[e], c2[e]);
                     }
                     if (RPL == 2) *reinterpret_cast<float4 *>(stage_g + iRT) = make_float4(c2[0], s2[0], c2[RPL - 1], s2[RPL - 1]);
                     else stage_g[iRT] = make_float2(c2[0], s2[0]);
@@ -634,8 +659,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     float s[RPL], co[RPL];
 #pragma unroll
                     for (int e = 0; e < RPL; ++e) {
-                        sincospif(2.0f * p[e], &s[e], &co[e]);
-                        co[e] += 0.0f;
+                        trig_turns_fast(p[e], s[e], co[e]);
                     }
                     if (RPL == 2)
                         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pair_addr<3>(iRT, cs32)), "f"(co[0]), "f"(s[0]),
