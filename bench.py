@@ -3,9 +3,10 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload NAME]
 
-A "step" is one pass of the hot path over one batch: `--window` consecutive Euler steps
-(default 2048) of ALL replicas of the workload, including threshold + cut scoring at the
-reference cadence and best-state tracking (SURVEY.md 8d "unit of work").  The default
+A "step" is one pass of the hot path over one batch: a complete solve -- the whole default
+schedule ceil(t_stop / h) (66 875 Euler steps on the G22 shape; `--window N` takes N consecutive
+steps instead) -- of ALL replicas of the workload, including threshold + cut scoring at the
+reference cadence, best-state tracking and the trace samples (SURVEY.md 8d "unit of work").  The default
 workload is BASELINE.json configs[1]: G22-shape max-cut (n=2000, 19990 edges, synthetic
 G(n,m), OIM N=2, GSET tuning K=0.2 ks_max=1.0 kn=0.15), 1024 replicas per GPU.
 
@@ -60,11 +61,18 @@ def load_workload(name):
     return shape, J, params, kind, R
 
 
+def default_steps(params):
+    """The reference's step count of a full run: ceil(t_stop / h) (dynamics.py:349)."""
+    import math
+    return int(math.ceil(params.t_stop / params.h))
+
+
 def workload_label(shape, J, params, R, window):
     """The `config.workload` string shared by both arms."""
     return (f"{shape}-shape graph n={J.n} nnz={J.nnz} N={params.n_states} "
             f"K={params.K} ks_max={params.ks_max} kn={params.kn} h={params.h}, {R} replicas per GPU, "
-            f"window {window} Euler steps incl. scoring at the reference cadence")
+            f"{window} Euler steps ({'the whole default schedule t_stop=%g' % params.t_stop if window == default_steps(params) else 'a window of the schedule'}) "
+            f"incl. scoring at the reference cadence")
 
 
 def algorithmic_bytes_per_euler_step(J, R, unit_weights, s_phi=4):
@@ -143,6 +151,9 @@ def cpu_oracle_throughput(J, params, kind, R_cpu, window, threads=None):
     return R_cpu * J.nnz * window / dt, dt, threads
 
 
+CPU_SAMPLE_STEPS = 2048     # Euler steps of the CPU arm's bounded sample
+
+
 def cpu_sample_size(J, window):
     """Replicas for ~10-20 s of CPU work at ~80 M updates/s/core."""
     cores = os.cpu_count() or 1
@@ -154,17 +165,21 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return
     shape, J, params, kind, R = load_workload(args.workload)
-    window = args.window
-    R_cpu = max(1, cpu_sample_size(J, window) // 2)
+    window = args.window or default_steps(params)
+    # bounded sample: many replicas (they are what the CPU threads share) x a slice of the schedule --
+    # the CPU cost of an Euler step does not depend on where in the schedule it sits
+    steps_cpu = min(window, CPU_SAMPLE_STEPS)
+    R_cpu = max(1, cpu_sample_size(J, steps_cpu) // 2)
     for _ in range(args.warmup):
-        cpu_oracle_throughput(J, params, kind, max(1, R_cpu // 8), max(32, window // 16))
+        cpu_oracle_throughput(J, params, kind, max(1, R_cpu // 8), max(32, steps_cpu // 16))
     t_all, upd, threads = 0.0, 0.0, 1
     for _ in range(args.steps):
-        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, window)
+        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
         t_all += dt
-        upd += R_cpu * J.nnz * window
+        upd += R_cpu * J.nnz * steps_cpu
     value = upd / t_all
-    sample = f"{R_cpu} replicas x {window} Euler steps per step (of {R} replicas/GPU), linear in replicas"
+    sample = (f"{R_cpu} replicas x {steps_cpu} Euler steps per step (of {R} replicas x {window} steps per GPU), "
+              f"linear in replicas and steps")
     line = {
         "impl": "reference", "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
@@ -211,7 +226,7 @@ def bench_dense(args, rank, world, local_rank):
     from paper_2505_22631_b200.model import SolverParams
     n = int(args.workload[2:].split("x")[0])
     R = args.replicas or int(args.workload.split("x")[1])
-    window = args.window if args.window != 2048 else (1024 if world == 1 else 256)
+    window = args.window or 1024
     params = SolverParams.tuned_for(n, 2, seed=0)
     seeds = list(range(R))
     nnz = n * (n - 1)
@@ -379,7 +394,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="G22x1024", help="one of %s, or SK<n>x<replicas> (dense, row-sharded)" % sorted(WORKLOADS))
-    ap.add_argument("--window", type=int, default=2048, help="Euler steps per bench step")
+    ap.add_argument("--window", type=int, default=0,
+                    help="Euler steps per bench step; 0 = the workload's whole default schedule ceil(t_stop / h) "
+                         "(dense SK workloads: 1024)")
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
     ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "resident"])
     ap.add_argument("--replicas", type=int, default=0, help="override replicas per GPU")
@@ -417,7 +434,7 @@ def main():
     shape, J, params, kind, R = load_workload(args.workload)
     if args.replicas:
         R = args.replicas
-    window = args.window
+    window = args.window or default_steps(params)
     seeds = [rank * R + r for r in range(R)]           # contiguous replica-index block per rank
     g = dyn.device_graph(J, local_rank)
     info = g.info()
@@ -538,11 +555,12 @@ def main():
             "full_run_seconds": hit.device_ms / 1e3, "replicas": R}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        R_cpu = cpu_sample_size(J, window)
-        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, window)
+        steps_cpu = min(window, CPU_SAMPLE_STEPS)
+        R_cpu = cpu_sample_size(J, steps_cpu)
+        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
         line["cpu_baseline"] = {"value": v, "unit": "updates/s", "cores": threads, "kind": "port",
-                                "sample": f"{R_cpu} replicas x {window} Euler steps of the same workload in {dt:.1f} s "
-                                          f"(oracle/ C+OpenMP port of the reference; linear in replicas)"}
+                                "sample": f"{R_cpu} replicas x {steps_cpu} Euler steps of the same workload in {dt:.1f} s "
+                                          f"(oracle/ C+OpenMP port of the reference; linear in replicas and steps)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
