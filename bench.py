@@ -154,11 +154,16 @@ def cpu_oracle_throughput(J, params, kind, R_cpu, window, threads=None):
 CPU_SAMPLE_STEPS = 2048     # Euler steps of the CPU arm's bounded sample
 
 
-def cpu_sample_size(J, window):
-    """Replicas for ~10-20 s of CPU work at ~80 M updates/s/core."""
+def cpu_sample(J, R, window, scale=1.0):
+    """(replicas, steps) of the CPU arm's bounded sample: ~10-20 s of work at ~80 M updates/s/core,
+    never more replicas than the workload has (a 1-replica workload is timed with 1 replica), a
+    slice of CPU_SAMPLE_STEPS steps of the schedule unless few replicas leave room for more."""
     cores = os.cpu_count() or 1
-    target_updates = 12.0 * 80e6 * cores
-    return int(max(1, min(256, target_updates / (J.nnz * window))))
+    target_updates = 12.0 * 80e6 * cores * scale
+    steps = min(window, CPU_SAMPLE_STEPS)
+    replicas = int(max(1, min(256, R, target_updates / (J.nnz * steps))))
+    steps = int(min(window, max(steps, target_updates / (J.nnz * replicas))))
+    return replicas, steps
 
 
 def run_reference_arm(args, rank, world):
@@ -168,8 +173,7 @@ def run_reference_arm(args, rank, world):
     window = args.window or default_steps(params)
     # bounded sample: many replicas (they are what the CPU threads share) x a slice of the schedule --
     # the CPU cost of an Euler step does not depend on where in the schedule it sits
-    steps_cpu = min(window, CPU_SAMPLE_STEPS)
-    R_cpu = max(1, cpu_sample_size(J, steps_cpu) // 2)
+    R_cpu, steps_cpu = cpu_sample(J, R, window, scale=0.5)
     for _ in range(args.warmup):
         cpu_oracle_throughput(J, params, kind, max(1, R_cpu // 8), max(32, steps_cpu // 16))
     t_all, upd, threads = 0.0, 0.0, 1
@@ -360,7 +364,8 @@ def bench_dense(args, rank, world, local_rank):
         total += dt
         dev_ms += res.device_ms
     clocks = sampler.stop()
-    t = torch.tensor([total, dev_ms / 1e3], dtype=torch.float64, device=f"cuda:{local_rank}")
+    t = torch.tensor([total, dev_ms / 1e3], dtype=torch.float64,
+                     device=f"cuda:{local_rank}" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total, dev_s = (float(x) for x in t.cpu())
     value = R * nnz * window * args.steps / dev_s
@@ -417,11 +422,19 @@ def main():
     import torch
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    # OSCB_BENCH_BACKEND=gloo lets several ranks share one GPU (a functional check of the multi-rank
+    # paths on a single-GPU box; the timings of such a run mean nothing)
+    backend = os.environ.get("OSCB_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
 
     if args.workload.startswith("SK"):
         bench_dense(args, rank, world, local_rank)
@@ -484,7 +497,8 @@ def main():
     barrier()
     e2e_s = time.perf_counter() - e2e0
 
-    t_dev = torch.tensor([dev_ms / 1e3, e2e_s, wall], dtype=torch.float64, device=f"cuda:{local_rank}")
+    t_dev = torch.tensor([dev_ms / 1e3, e2e_s, wall], dtype=torch.float64,
+                         device=f"cuda:{local_rank}" if dist is None or dist.get_backend() == "nccl" else "cpu")
     if dist is not None:
         dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
     t_dev_s, t_e2e_s, t_wall_s = (float(x) for x in t_dev.cpu())
@@ -555,8 +569,7 @@ def main():
             "full_run_seconds": hit.device_ms / 1e3, "replicas": R}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        steps_cpu = min(window, CPU_SAMPLE_STEPS)
-        R_cpu = cpu_sample_size(J, steps_cpu)
+        R_cpu, steps_cpu = cpu_sample(J, R, window)
         v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
         line["cpu_baseline"] = {"value": v, "unit": "updates/s", "cores": threads, "kind": "port",
                                 "sample": f"{R_cpu} replicas x {steps_cpu} Euler steps of the same workload in {dt:.1f} s "
