@@ -563,9 +563,25 @@ def main():
                             target=0.99 * best, want_phases=False, want_states=False, want_traces=False)
         hits = hit.first_hit_step[hit.first_hit_step >= 0]
         first = int(hits.min()) if len(hits) else -1
+        measured = e2e_hit = None
+        if first >= 0:
+            # the solve actually stopped at the step that reaches the target: device time, and wall clock
+            # through the API with host phases in and the best states / objectives out
+            stop = max(1, first + 1)
+            for _ in range(2):
+                short = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                                      steps=stop, phi0=phi0, want_phases=False, want_traces=False)
+            t0 = time.perf_counter()
+            short = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                                  steps=stop, phi0=phi0, want_phases=False, want_traces=False)
+            e2e_hit = time.perf_counter() - t0
+            measured = short.device_ms / 1e3
+            assert float(short.best_objective.max()) >= 0.99 * best
         line["time_to_99pct_best_cut"] = {
             "best_cut": best, "target": 0.99 * best, "first_hit_step": first, "steps_total": hit.steps,
-            "seconds": (hit.device_ms / 1e3) * (first + 1) / hit.steps if first >= 0 else None,
+            "seconds": measured, "e2e_seconds": e2e_hit,
+            "how": "a run of first_hit_step + 1 Euler steps of all replicas: CUDA-event time of the launch, and wall clock "
+                   "of the API call with host buffers",
             "full_run_seconds": hit.device_ms / 1e3, "replicas": R}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
