@@ -211,9 +211,10 @@ int oscb_dense_fused_finish(oscb_fused *f, oscb_run_outputs *out);
 int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows);
 int oscb_dense_fused_destroy(oscb_fused *f);
 
-/* Device self-test behind the N = 2 scoring shortcut of the float32 kernel: counts the float32
- * phases in [0, 1) (all 2^30-ish of them) whose sign-of-cosine state differs from the reference
- * threshold (dynamics.py:203-213).  Must return 0 mismatches. */
+/* Device self-test behind the scoring shortcuts of the float32 kernel: counts the float32 phases in
+ * [0, 1) (all 2^30-ish of them) whose sign-bit-of-cosine state (N = 2), or whose state from the
+ * float32 decision-boundary table (N = 3..8), differs from the reference threshold
+ * (dynamics.py:203-213); also bounds the error of the fast trig.  Must return 0 mismatches. */
 int oscb_selftest_sign_state(int device, uint64_t *mismatches);
 
 /* Host-only: the graph compiler of the persistent kernel (no GPU needed).  Turns a canonical CSR

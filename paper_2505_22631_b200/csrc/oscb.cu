@@ -1179,6 +1179,15 @@ int oscb_selftest_sign_state(int device, uint64_t *mismatches)
         OSCB_CUDA(cudaMemset(d.p, 0, sizeof(unsigned long long)));
         k_selftest_sign_state<<<148 * 8, 256>>>(d.p);
         check_launch("oscb_selftest_sign_state");
+        // and the float32 decision boundaries of the N-state threshold (N = 3..8) against the float64 rule
+        for (int N = 3; N <= 8; ++N) {
+            FastArgs fa;
+            memset(&fa, 0, sizeof(fa));
+            fa.n_bnd = N;
+            fast_state_boundaries(N, fa.bnd);
+            k_selftest_boundaries<<<148 * 8, 256>>>(N, fa, d.p);
+            check_launch("oscb_selftest_sign_state(boundaries)");
+        }
         unsigned long long h = 0;
         OSCB_CUDA(cudaMemcpy(&h, d.p, sizeof(h), cudaMemcpyDeviceToHost));
         *mismatches = h;

@@ -143,7 +143,7 @@ template <typename T> __device__ __forceinline__ T wrap_unit(T x)
 
 // dynamics.py:203-213 evaluated in fp64 on the value the phase holds, so the rounding is the
 // reference's bit for bit for any phase representable in the kernel's precision.
-__device__ __forceinline__ int threshold_state(double p, int n_states)
+__host__ __device__ __forceinline__ int threshold_state(double p, int n_states)
 {
     // N = 2: d0 = min(p, 1-p), d1 = |p - 0.5|, both differences exact where the comparison is
     // close (Sterbenz), so "d1 < d0" is exactly 0.25 < p < 0.75 (ties at 0.25 / 0.75 -> state 0)

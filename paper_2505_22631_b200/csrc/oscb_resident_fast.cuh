@@ -29,6 +29,7 @@
 //   x   = phi + hK acc - h ks shil + kn sqrt(h) xi ;  phi' = x - floor(x)           (dynamics.py:171-172)
 #pragma once
 #include "oscb_resident.cuh"
+#include <string.h>
 
 namespace oscb {
 
@@ -104,6 +105,18 @@ __device__ __forceinline__ void trig_turns_fast(float y, float &s, float &c)
     c = __uint_as_float((__float_as_uint(c0) & 0x7FFFFFFFu) | state);
 }
 
+// Lattice state of a float32 phase for any N (dynamics.py:203-213): the reference rule is a step
+// function of the phase, so it is evaluated as "how many decision boundaries lie at or below p";
+// the boundaries are found on the host by bisection over float32 with the reference's own float64
+// expression (fast_state_boundaries), and oscb_selftest_sign_state checks the table against the
+// float64 rule for every float32 in [0, 1).
+__device__ __forceinline__ uint32_t state_from_boundaries(float p, const float *bnd, int n)
+{
+    uint32_t st = 0;
+    for (int k = 0; k < n; ++k) st += (p >= bnd[k]) ? 1u : 0u;
+    return st == (uint32_t)n ? 0u : st;
+}
+
 // Everything the kernel needs, precomputed on the host so that the hot loops read constants
 // straight from the parameter bank instead of re-deriving them under register pressure.
 struct FastArgs {
@@ -129,6 +142,9 @@ struct FastArgs {
     float2 *cs_next;                   // [tiles][n][RT] next-step (cos, sin) pairs, L2-resident staging (N = 2 kernels)
     const uint64_t *seeds;
     const long long *sample_steps;
+    const float *hks_table;            // [step_end - step_begin + 1]  ks_scale * ks(step), computed on the host in float64
+    int n_bnd;                         // > 0: lattice states from float32 decision boundaries (N <= 8), else the float64 rule
+    float bnd[8];                      // bnd[k] = smallest float32 phase whose reference state is (k + 1) % N
     double *best_obj, *energy, *best_trace;
     uint8_t *best_states;
     long long *first_hit;
@@ -154,6 +170,44 @@ __global__ void k_selftest_sign_state(unsigned long long *mismatches)
         if (!(fabsf(s - s_ref) <= 2e-6f && fabsf(co - c_ref) <= 2e-6f)) ++bad;
     }
     if (bad) atomicAdd(mismatches, bad);
+}
+
+// Self-test of the boundary table for N states: every float32 phase in [0, 1) must get the state of
+// the float64 reference rule.
+__global__ void k_selftest_boundaries(int n_states, FastArgs a, unsigned long long *mismatches)
+{
+    const unsigned long long total = 0x3F800000ull;
+    unsigned long long bad = 0;
+    for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+         q += (unsigned long long)gridDim.x * blockDim.x) {
+        const float p = __uint_as_float((uint32_t)q);
+        if (state_from_boundaries(p, a.bnd, a.n_bnd) != (uint32_t)threshold_state((double)p, n_states)) ++bad;
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
+// Decision boundaries of the reference threshold rule on float32 phases: bnd[k] = the smallest
+// float32 in [k/N, (k+1)/N] whose state is (k + 1) % N.  Inside that interval the state is k below
+// the boundary and (k + 1) % N from it on (both distances are monotone in p), so a
+// bisection over the float32 bit patterns with the float64 rule itself finds it exactly.
+inline void fast_state_boundaries(int n_states, float *bnd)
+{
+    for (int k = 0; k < n_states; ++k) {
+        uint32_t lo, hi;                 // state(lo) == k, state(hi) == (k + 1) % N
+        float flo = (float)((double)k / n_states), fhi = k + 1 == n_states ? 0.99999994f : (float)((double)(k + 1) / n_states);
+        memcpy(&lo, &flo, 4);
+        memcpy(&hi, &fhi, 4);
+        const int next = (k + 1) % n_states;
+        // make sure the bracket ends are on the right sides (float rounding of k/N can land either way)
+        auto st = [&](uint32_t bits) { float f; memcpy(&f, &bits, 4); return threshold_state((double)f, n_states); };
+        while (st(lo) != k) --lo;
+        while (st(hi) != next) hi = hi + 1 < 0x3F800000u ? hi + 1 : hi - 2;   // (the last interval ends below 1.0)
+        while (hi - lo > 1) {
+            const uint32_t mid = lo + (hi - lo) / 2;
+            if (st(mid) == k) lo = mid; else hi = mid;
+        }
+        memcpy(&bnd[k], &hi, 4);
+    }
 }
 
 // shared-memory layout of the float32 kernel; filled into FastArgs by the host
@@ -246,7 +300,7 @@ template <int NMODE, bool WEIGHTED, bool IDX_SMEM, bool PHI_SMEM, int RPL>
 __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr bool PIGGY = NMODE == 2;    // max-cut with integer couplings: score during the next gather
+    constexpr bool PIGGY = true;          // N = 2 max-cut (sign bits) and N-state colouring (state bytes): score during the next gather
     const int tid = threadIdx.x, NT = blockDim.x;
     const uint32_t smem32 = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const int lane = tid & 31, warp = tid >> 5;
@@ -271,7 +325,6 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     double *part = reinterpret_cast<double *>(smem_raw + a.off_part);
     double *best_s = reinterpret_cast<double *>(smem_raw + a.off_misc);
     int *improved_s = reinterpret_cast<int *>(smem_raw + a.off_misc + a.RT * 8);
-    float *ks_s = reinterpret_cast<float *>(smem_raw + a.off_misc + a.RT * 16);        // [2]: ks_scale * ks(step)
 
     // ---- prologue -------------------------------------------------------------------------------
     {
@@ -311,7 +364,6 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             best_s[tid] = a.best_obj[tile * a.RT + tid];
             improved_s[tid] = 0;
         }
-        if (tid == 0) ks_s[a.step_begin & 1] = (float)(a.ks_scale * ks_value(a.ks_max, a.ks_period, (double)a.step_begin * a.h));
     }
     uint2 key[RPL];
     bool live[RPL];
@@ -328,6 +380,9 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     const uint32_t w32 = smem32 + a.off_w + (uint32_t)(gp0 * a.C + c) * 16;
     __syncthreads();
 
+    auto state_of_phase = [&](float p) -> uint32_t {
+        return a.n_bnd > 0 ? state_from_boundaries(p, a.bnd, a.n_bnd) : (uint32_t)threshold_state((double)p, a.tc.n_states);
+    };
     auto load_phi = [&](uint32_t iRT, float (&p)[RPL]) {
         if (RPL == 2) {
             float2 t;
@@ -457,7 +512,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     float p[RPL];
                     load_phi(iRT, p);
 #pragma unroll
-                    for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, (uint32_t)threshold_state((double)p[e], a.tc.n_states));
+                    for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, state_of_phase(p[e]));
                 }
             }
             __syncthreads();
@@ -471,7 +526,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
     // ---- time loop ------------------------------------------------------------------------------
 #pragma unroll 1
     for (long long step = a.step_begin; step < a.step_end; ++step) {
-        const float hks = ks_s[step & 1];           // h*ks, or 2*h*ks for N = 2
+        const float hks = __ldg(a.hks_table + (step - a.step_begin));   // h*ks, or 2*h*ks for N = 2 (host table: no float64 fmod here)
         const bool is_sample = sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] == step;
         const bool cadence_hit = a.cadence > 0 && step % a.cadence == 0;
         const bool count_now = PIGGY && pending;
@@ -524,7 +579,38 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
             float negw[RPL];
 #pragma unroll
             for (int e = 0; e < RPL; ++e) { sum[e] = make_float2(0.f, 0.f); neg[e] = 0; negw[e] = 0.f; }
-            if (PIGGY && count_now) {
+            if (PIGGY && count_now && NMODE != 2) {
+                // colouring, scoring step: count the neighbours in the row's own state (state bytes of the
+                // scored phases; padding rows hold 255 and never match)
+                uint32_t own_st[RPL];
+                states_of(iRT, own_st);
+#pragma unroll 1
+                for (int gg = 0; gg < G; ++gg) {
+                    const uint2 nx = next_group();
+                    const uint32_t j0 = pk.x & 0xffffu, j1 = pk.x >> 16, j2 = pk.y & 0xffffu, j3 = pk.y >> 16;
+                    const PairPack<RPL> v0 = pairs_at(j0), v1 = pairs_at(j1), v2 = pairs_at(j2), v3 = pairs_at(j3);
+                    uint32_t s0[RPL], s1[RPL], s2[RPL], s3[RPL];
+                    states_of(j0, s0); states_of(j1, s1); states_of(j2, s2); states_of(j3, s3);
+                    if (WEIGHTED) {
+                        const float4 w4 = next_weights();
+#pragma unroll
+                        for (int e = 0; e < RPL; ++e) {              // same order as the non-scoring gather
+                            sum[e] = __ffma2_rn(make_float2(w4.x, w4.x), v0.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.y, w4.y), v1.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.z, w4.z), v2.v[e], sum[e]);
+                            sum[e] = __ffma2_rn(make_float2(w4.w, w4.w), v3.v[e], sum[e]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < RPL; ++e)
+                            sum[e] = __fadd2_rn(sum[e], __fadd2_rn(__fadd2_rn(v0.v[e], v1.v[e]), __fadd2_rn(v2.v[e], v3.v[e])));
+                    }
+#pragma unroll
+                    for (int e = 0; e < RPL; ++e)
+                        neg[e] += (int)(s0[e] == own_st[e]) + (int)(s1[e] == own_st[e]) + (int)(s2[e] == own_st[e]) + (int)(s3[e] == own_st[e]);
+                    pk = nx;
+                }
+            } else if (PIGGY && count_now) {
                 // scoring step: the sign bit of every gathered cosine is the neighbour's lattice state
 #pragma unroll 1
                 for (int gg = 0; gg < G; ++gg) {
@@ -581,7 +667,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                 const uint32_t k = (iRT >> a.LRT) & 3u;
                 int deg = 0;
                 float wrow = 0.f;
-                if (PIGGY && count_now) {
+                if (PIGGY && count_now && NMODE == 2) {
                     if (WEIGHTED) wrow = rowsum_lane[row * a.C];
                     else deg = (int)deg_lane[row * a.C];
                 }
@@ -589,7 +675,9 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
 #pragma unroll
                 for (int e = 0; e < RPL; ++e) {
                     const float ci = own.v[e].x, si = own.v[e].y;
-                    if (PIGGY && count_now) {   // differing neighbours: deg - neg if the row itself is in state 1
+                    if (PIGGY && count_now && NMODE != 2) {
+                        twice_cut[e] += neg[e];                          // equal-state neighbours: twice the conflicts
+                    } else if (PIGGY && count_now) {   // differing neighbours: deg - neg if the row itself is in state 1
                         const bool own1 = __float_as_int(ci) < 0;        // the row's own state: the sign BIT
                         if (WEIGHTED) twice_cut_w[e] += own1 ? wrow - negw[e] : negw[e];
                         else twice_cut[e] += own1 ? deg - neg[e] : neg[e];
@@ -617,12 +705,11 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                 }
             }
         }
-        if (tid == 0) ks_s[(step + 1) & 1] = (float)(a.ks_scale * ks_value(a.ks_max, a.ks_period, (double)(step + 1) * a.h));
         if (count_now) {
             // `twice_cut` counted the state after step `pending_label`; cs still holds that state
             double tc[RPL];
 #pragma unroll
-            for (int e = 0; e < RPL; ++e) tc[e] = WEIGHTED ? (double)twice_cut_w[e] : (double)twice_cut[e];
+            for (int e = 0; e < RPL; ++e) tc[e] = (WEIGHTED && NMODE == 2) ? (double)twice_cut_w[e] : (double)twice_cut[e];
             const double obj = 0.5 * tile_reduce_rpl<RPL>(tc, a.RT, a.LPS, part, tid, a.W);
             if (tid < a.RT) record_best(obj, pending_label);
             __syncthreads();
@@ -668,7 +755,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                         sts_pair(pair_addr<3>(iRT, cs32), co[0], s[0]);
                     if (score_after) {
 #pragma unroll
-                        for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, (uint32_t)threshold_state((double)p[e], a.tc.n_states));
+                        for (int e = 0; e < RPL; ++e) sts_u8(st32 + iRT + e, state_of_phase(p[e]));
                     }
                 }
             }

@@ -399,7 +399,10 @@ static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT
     const bool weighted = !g->unit_weights;
     FastFit f;
     f.states = n_states != 2;
-    f.piggy = n_states == 2 && objective == OSCB_OBJ_MAXCUT && (!weighted || exact_f32_cut);
+    // scoring rides on the next step's gather: N = 2 max-cut (sign bits; weighted only while float32 sums of
+    // the couplings stay exact) and N-state colouring (state bytes, a count)
+    f.piggy = (n_states == 2 && objective == OSCB_OBJ_MAXCUT && (!weighted || exact_f32_cut)) ||
+              (n_states != 2 && objective == OSCB_OBJ_COLORING);
     auto lay = [&](bool phi, bool idx) {
         return FastSmem::make((int)g->n, RT, C, T, W, n_group_rows, f.states, f.deg_smem, phi, idx, weighted);
     };
@@ -410,7 +413,7 @@ static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT
     // and goes to shared memory last.
     if (lay(false, true).total <= cap) f.idx_smem = true;
     if (f.idx_smem && lay(true, true).total <= cap) f.phi_smem = true;
-    if (f.piggy && !weighted) {
+    if (f.piggy && !weighted && n_states == 2) {
         f.deg_smem = true;
         if (lay(f.phi_smem, f.idx_smem).total > cap) f.deg_smem = false;
     }
@@ -420,7 +423,7 @@ static FastFit fit_fast(const oscb_graph *g, int n_states, int objective, int RT
 }
 
 static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const ResidentPlan &plan, int n_states,
-                                 const FastFit &f, int tiles, float2 *cs_next)
+                                 const FastFit &f, int tiles, float2 *cs_next, const float *hks_table)
 {
     FastArgs a;
     memset(&a, 0, sizeof(a));
@@ -445,6 +448,12 @@ static void launch_resident_fast(oscb_graph *g, const ResidentArgs &ra, const Re
     a.wstream = reinterpret_cast<const float *>(ra.wstream);
     a.phi = reinterpret_cast<float *>(ra.phi); a.seeds = ra.seeds; a.sample_steps = ra.sample_steps;
     a.cs_next = cs_next;
+    a.hks_table = hks_table;
+    a.n_bnd = 0;
+    if (n_states != 2 && n_states <= 8) {
+        a.n_bnd = n_states;
+        fast_state_boundaries(n_states, a.bnd);
+    }
     a.best_obj = ra.best_obj; a.energy = ra.energy; a.best_trace = ra.best_trace; a.best_states = ra.best_states;
     a.first_hit = ra.first_hit; a.nonfinite = ra.nonfinite;
     auto go = [&](auto kernel) {
@@ -543,10 +552,21 @@ static void run_resident_impl(oscb_graph *g, const oscb_run_params *p, const Res
     cudaEvent_t ev0, ev1;
     OSCB_CUDA(cudaEventCreate(&ev0));
     OSCB_CUDA(cudaEventCreate(&ev1));
-    OSCB_CUDA(cudaEventRecord(ev0, s));
     DevBuf<float2> d_stage;
+    DevBuf<float> d_hks;
     if (FAST && p->n_states == 2) d_stage.alloc(tot_pad + 64);
-    if (FAST) launch_resident_fast(g, a, *plan, p->n_states, fast, tiles, d_stage.p);
+    if (FAST) {
+        // h * ks(step) (x2 for N = 2, where the SHIL term is 2 s c) for every step, in the reference's float64
+        std::vector<float> hks((size_t)steps + 1);
+        const double scale = p->h * (p->n_states == 2 ? 2.0 : 1.0);
+        for (int64_t k = 0; k <= steps; ++k)
+            hks[(size_t)k] = (float)(scale * ks_value(p->ks_max, p->ks_period, (double)(p->first_step + k) * p->h));
+        d_hks.alloc(hks.size());
+        d_hks.upload(hks.data(), hks.size(), s);
+        OSCB_CUDA(cudaStreamSynchronize(s));        // the staging vector dies at the end of this block
+    }
+    OSCB_CUDA(cudaEventRecord(ev0, s));
+    if (FAST) launch_resident_fast(g, a, *plan, p->n_states, fast, tiles, d_stage.p, d_hks.p);
     else launch_resident<T, MAXT, STRICT>(g, a, tiles, plan->W * 32, smem, idx_smem, plan->weighted);
     OSCB_CUDA(cudaEventRecord(ev1, s));
     {
