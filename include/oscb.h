@@ -57,6 +57,7 @@ extern "C" {
 #define OSCB_KERNEL_STREAM 1   /* one launch per step, phases in HBM/L2                   */
 #define OSCB_KERNEL_RESIDENT 2 /* persistent CTA per replica tile, phases' (cos,sin) in smem */
 #define OSCB_KERNEL_DENSE_TC 3 /* dense integer J: persistent tcgen05 int8 GEMM J*[cos|sin] digit planes */
+#define OSCB_KERNEL_CLUSTER 4  /* latency mode: one replica per 8-CTA cluster, pairs exchanged through DSMEM */
 
 typedef struct oscb_graph oscb_graph;
 

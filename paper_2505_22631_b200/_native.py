@@ -24,8 +24,8 @@ OBJ = {"maxcut": 0, "coloring": 1}
 PREC = {"f32": 32, "f64": 64}
 NOISE_DEVICE, NOISE_HOST, NOISE_NONE = 0, 1, 2
 FUSED_MEM_BYTES = 96
-KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2, "dense-tc": 3}
-KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident", 3: "dense-tc"}
+KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2, "dense-tc": 3, "cluster": 4}
+KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident", 3: "dense-tc", 4: "cluster"}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC"]

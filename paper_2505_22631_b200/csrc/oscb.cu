@@ -13,6 +13,7 @@
 #include "oscb_resident_host.hpp"
 #include "oscb_dense_host.hpp"
 #include "oscb_umma.hpp"
+#include "oscb_cluster_host.hpp"
 #include <type_traits>
 
 #include <algorithm>
@@ -1280,6 +1281,13 @@ int oscb_run(oscb_graph *g, const oscb_run_params *p, const uint64_t *seeds, int
                 return OSCB_OK;
             }
             kernel = OSCB_KERNEL_STREAM;
+        }
+        if (kernel == OSCB_KERNEL_CLUSTER)
+            OSCB_REQUIRE(cluster_applies(g, p, R, true),
+                         "the cluster kernel takes float32, device noise, N = 2 max-cut, 64 <= n <= 65535 and unit or small integer couplings");
+        if ((kernel == OSCB_KERNEL_AUTO && cluster_applies(g, p, R, false)) || kernel == OSCB_KERNEL_CLUSTER) {
+            run_cluster(g, p, rp.steps, rp.cadence, rp.sample_steps, seeds, R, phi0, out);
+            return OSCB_OK;
         }
         if (kernel == OSCB_KERNEL_AUTO)
             kernel = resident_fits(g, p, R) ? OSCB_KERNEL_RESIDENT : OSCB_KERNEL_STREAM;
