@@ -509,8 +509,11 @@ static void run_stream(oscb_graph *g, const oscb_run_params *p, const RunPlan &r
 // (oscb_umma.cuh): one persistent launch per chunk of <= 28 replicas
 static bool umma_applies(const oscb_graph *g, const oscb_run_params *p)
 {
-    return g->is_dense && g->umma && p->n_states == 2 && p->objective == OSCB_OBJ_MAXCUT &&
-           p->noise_mode != OSCB_NOISE_HOST && p->kernel != OSCB_KERNEL_STREAM;
+    // OIM: N = 2 max-cut on any integer couplings; OPM: N-state colouring on unit couplings (the conflict
+    // count ignores weights, dynamics.py:219-222, and sum_j J_ij [s_j == s_i] counts only when J is 0/1)
+    const bool oim = p->n_states == 2 && p->objective == OSCB_OBJ_MAXCUT;
+    const bool opm = p->n_states >= 3 && p->n_states <= 16 && p->objective == OSCB_OBJ_COLORING && g->unit_weights;
+    return g->is_dense && g->umma && (oim || opm) && p->noise_mode != OSCB_NOISE_HOST && p->kernel != OSCB_KERNEL_STREAM;
 }
 
 // which passes score / sample: pass q integrates step q and first scores the phases it starts
@@ -550,6 +553,8 @@ static UmmaSpec umma_spec(const oscb_run_params *p, const RunPlan &rp, const Umm
     sp.R = R;
     sp.precision = p->precision;
     sp.noise_on = (p->noise_mode == OSCB_NOISE_DEVICE && p->kn != 0.0) ? 1 : 0;
+    sp.n_states = p->n_states;
+    sp.maximize = p->objective == OSCB_OBJ_MAXCUT ? 1 : 0;
     sp.K = p->K; sp.h = p->h; sp.kn_sqrt_h = p->kn * std::sqrt(p->h); sp.ks_max = p->ks_max; sp.ks_period = p->ks_period;
     sp.steps = rp.steps; sp.first_step = p->first_step;
     sp.flags = sc.flags.data();
@@ -565,14 +570,16 @@ static void umma_bookkeeping(const oscb_run_params *p, const UmmaSchedule &sc, c
 {
     const long long E = (long long)sc.event_step.size();
     for (int r = 0; r < Rc; ++r) {
-        double best = -std::numeric_limits<double>::infinity();
+        const bool maximize = p->objective == OSCB_OBJ_MAXCUT;
+        double best = maximize ? -std::numeric_limits<double>::infinity() : std::numeric_limits<double>::infinity();
         long long first = -1;
         size_t k = 0;
         for (long long e = 0; e < E; ++e) {
             const double obj = 0.5 * (double)ev[(size_t)e * Rc + r];
-            if (obj > best) {
+            if (maximize ? obj > best : obj < best) {
                 best = obj;
-                if (p->use_target && first < 0 && obj >= p->target_objective) first = sc.event_step[(size_t)e];
+                if (p->use_target && first < 0 && (maximize ? obj >= p->target_objective : obj <= p->target_objective))
+                    first = sc.event_step[(size_t)e];
             }
             if (k < sc.sample_event.size() && sc.sample_event[k] == e) {
                 if (out->best_trace) out->best_trace[(size_t)(r0 + r) * out->max_samples + k] = best;
@@ -612,8 +619,9 @@ static void run_umma(oscb_graph *g, const oscb_run_params *p, const RunPlan &rp,
     double ms = 0.0;
     int64_t launches = 0, smem = 0;
     unsigned long long flag = ~0ull;
-    for (int r0 = 0; r0 < R; r0 += kUmmaMaxReplicas) {
-        const int Rc = std::min(kUmmaMaxReplicas, R - r0);
+    const int chunk = umma_max_replicas(p->n_states);
+    for (int r0 = 0; r0 < R; r0 += chunk) {
+        const int Rc = std::min(chunk, R - r0);
         std::vector<long long> ev((size_t)E * Rc);
         std::vector<double> en((size_t)S * Rc);
         UmmaSession ses(g, umma_spec(p, rp, sc, Rc), 1, 0);
@@ -632,7 +640,7 @@ static void run_umma(oscb_graph *g, const oscb_run_params *p, const RunPlan &rp,
     out->device_ms = ms;
     out->kernel_launches = launches;
     out->kernel_used = OSCB_KERNEL_DENSE_TC;
-    out->replicas_per_cta = std::min(R, kUmmaMaxReplicas);
+    out->replicas_per_cta = std::min(R, chunk);
     out->smem_bytes = smem;
     umma_raise_nonfinite(flag, out);
 }
@@ -1023,10 +1031,10 @@ int oscb_dense_fused_create(oscb_graph *shard, const oscb_run_params *p, int64_t
         OSCB_REQUIRE(shard && p && out, "NULL argument");
         *out = nullptr;
         OSCB_REQUIRE(shard->is_dense && shard->umma, "fused dense runs need integer couplings |J| <= 127 and 128-row aligned shards");
-        OSCB_REQUIRE(p->n_states == 2 && p->objective == OSCB_OBJ_MAXCUT, "fused dense runs are N = 2 max-cut");
-        OSCB_REQUIRE(p->noise_mode != OSCB_NOISE_HOST, "fused dense runs draw their noise on the device");
+        OSCB_REQUIRE(p->kernel == OSCB_KERNEL_AUTO || p->kernel == OSCB_KERNEL_DENSE_TC, "fused dense runs use the tensor-core kernel");
+        OSCB_REQUIRE(umma_applies(shard, p), "fused dense runs are N = 2 max-cut (integer couplings) or N-state colouring (unit couplings), device noise");
         OSCB_REQUIRE(p->precision == OSCB_PREC_F32 || p->precision == OSCB_PREC_F64, "unknown precision %d", p->precision);
-        OSCB_REQUIRE(R >= 1 && R <= kUmmaMaxReplicas, "fused dense runs take 1..%d replicas per session", kUmmaMaxReplicas);
+        OSCB_REQUIRE(R >= 1 && R <= umma_max_replicas(p->n_states), "fused dense runs take 1..%d replicas per session", umma_max_replicas(p->n_states));
         OSCB_REQUIRE(p->h > 0.0 && std::isfinite(p->h) && p->ks_period > 0.0, "bad h / ks_period");
         OSCB_REQUIRE(p->steps > 0 || (p->t_stop > 0.0 && std::isfinite(p->t_stop)), "t_stop must be finite and > 0");
         bind_device(shard);
@@ -1275,7 +1283,7 @@ int oscb_run(oscb_graph *g, const oscb_run_params *p, const uint64_t *seeds, int
         if (g->is_dense) {
             OSCB_REQUIRE(kernel != OSCB_KERNEL_RESIDENT, "dense couplings run on the streaming loop or the tensor-core kernel (no resident kernel)");
             OSCB_REQUIRE(kernel != OSCB_KERNEL_DENSE_TC || umma_applies(g, p),
-                         "the tensor-core dense kernel needs integer couplings |J| <= 127, N = 2 max-cut and device noise");
+                         "the tensor-core dense kernel needs integer couplings |J| <= 127, device noise, and N = 2 max-cut or N <= 16 colouring on unit couplings");
             if (umma_applies(g, p)) {
                 run_umma(g, p, rp, seeds, R, phi0, out);
                 return OSCB_OK;

@@ -66,7 +66,9 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
 {
     try {
         OSCB_REQUIRE(g && g->umma, "handle has no tensor-core plan (integer couplings |J| <= 127 on 128-row aligned shards)");
-        OSCB_REQUIRE(spec.R >= 1 && spec.R <= UMMA_MAXR, "tensor-core dense path takes 1..%d replicas per launch", UMMA_MAXR);
+        OSCB_REQUIRE(spec.n_states >= 2 && spec.n_states <= 16, "tensor-core dense path takes N = 2..16 states");
+        OSCB_REQUIRE(spec.R >= 1 && spec.R <= umma_max_replicas(spec.n_states), "tensor-core dense path takes 1..%d replicas per launch at N = %d",
+                     umma_max_replicas(spec.n_states), spec.n_states);
         OSCB_REQUIRE(world >= 1 && world <= kUmmaMaxWorld && rank >= 0 && rank < world, "bad world / rank %d / %d", world, rank);
         m->g = g;
         m->plan = g->umma.get();
@@ -83,7 +85,10 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.tile_begin = plan.tile_begin;
         a.tile_end = plan.tile_end;
         a.R = spec.R;
-        a.NB = (9 * spec.R + 15) / 16 * 16;
+        a.n_states = spec.n_states;
+        a.maximize = spec.maximize;
+        a.score_cols = spec.n_states == 2 ? 1 : spec.n_states;
+        a.NB = ((8 + a.score_cols) * spec.R + 15) / 16 * 16;
         const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage;
         const size_t ctl = 2048, slack = 1024;
         a.stages = (int)std::min<size_t>(12, ((size_t)g->smem_optin - ctl - slack) / stage);
@@ -103,7 +108,7 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.passes = spec.steps + 1;
         a.first_step = spec.first_step;
         a.K = spec.K; a.h = spec.h; a.kn_sqrt_h = spec.kn_sqrt_h; a.ks_max = spec.ks_max; a.ks_period = spec.ks_period;
-        a.tc = make_trig_const(2);
+        a.tc = make_trig_const(spec.n_states);
         a.noise_on = spec.noise_on;
         a.ld_phi = (long long)lt * UMMA_TILE;
 

@@ -4,7 +4,8 @@
 //   J * [cos Theta | sin Theta]  as an exact integer GEMM
 //     A = J                    int8 [rows x n]        (SK couplings are +-1; any integer |J| <= 127)
 //     B = digit planes of the (cos, sin) pairs:  c = 2^-30 * sum_k 2^(8k) d_k,  d_k signed bytes,
-//         i.e. 4 int8 planes per component, plus one plane of spins sigma = +-1 for the cut
+//         i.e. 4 int8 planes per component, plus the score planes: one plane of spins sigma = +-1
+//         for the cut (OIM, N = 2) or N one-hot state planes for the colouring conflicts (OPM)
 //     D = A * B^T              int32 in TMEM, tcgen05.mma kind::i8 (UTCIMMA), M = 128, K = 32
 //   Integer accumulation is exact and order independent, so the coupling sums carry only the
 //   2^-31 quantisation of each pair -- tighter than a float32 FMA chain over n = 16384 terms.
@@ -58,6 +59,9 @@ struct UmmaArgs {
     double K, h, kn_sqrt_h, ks_max, ks_period;
     TrigConst tc;
     int noise_on;
+    int n_states;             // N: 2 = OIM max-cut (one spin plane), >= 3 = OPM colouring (N one-hot state planes)
+    int maximize;             // 1: max-cut (larger is better), 0: colouring conflicts (smaller is better)
+    int score_cols;           // score planes per replica: 1 (N = 2) or N
     long long ld_phi;         // leading dimension of phi / best_states: local rows padded to tiles
     const uint8_t *A_img;     // [local tiles][tiles][16384]
     uint8_t *B_img[2][UMMA_MAXW];  // per buffer and rank: [tiles][NB * 128]
@@ -66,7 +70,7 @@ struct UmmaArgs {
     const uint64_t *seeds;    // [R]
     const uint8_t *flags;     // [passes] bit 0: score the pass's input phases, bit 1: + energy sample
     unsigned int *bar[UMMA_MAXW];      // monotonic arrival counters, one per rank
-    long long *events[UMMA_MAXW];      // [n_events][R]: sum_i sum_j J_ij [s_i != s_j] = 2 * cut
+    long long *events[UMMA_MAXW];      // [n_events][R]: sum_i sum_j J_ij [s_i != s_j] = 2 * cut (N = 2); sum_i sum_j J_ij [s_i == s_j] = 2 * conflicts (N >= 3)
     double *en_part[UMMA_MAXW];        // [n_samples][ctas_total][R]
     uint8_t *best_states;     // [R][ld_phi]
     unsigned long long *nonfinite;
@@ -170,7 +174,7 @@ __device__ __forceinline__ long long digits_sum(const int *D)
 
 // write the 8 digit bytes and the spin of oscillator (tile kb, column c) for replica r into one B image
 template <typename T>
-__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state)
+__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state, int n_states)
 {
     uint8_t *base = Bimg + (size_t)kb * NB * 128;
     int dc[4], ds[4];
@@ -181,7 +185,12 @@ __device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, in
         base[swz(8 * r + k, c)] = (uint8_t)dc[k];
         base[swz(8 * r + 4 + k, c)] = (uint8_t)ds[k];
     }
-    base[swz(8 * R + r, c)] = (uint8_t)(state ? -1 : 1);
+    if (n_states == 2) {
+        base[swz(8 * R + r, c)] = (uint8_t)(state ? -1 : 1);                     // spin plane: sum_j J_ij sigma_j
+    } else {
+        for (int k = 0; k < n_states; ++k)                                       // one-hot planes: sum_j J_ij [s_j == k]
+            base[swz(8 * R + r * n_states + k, c)] = (uint8_t)(k == state ? 1 : 0);
+    }
 }
 
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p, bool sys)
@@ -210,7 +219,7 @@ __global__ void k_umma_init(UmmaArgs a, const double *__restrict__ phi0)
     const T p = (T)phi0[q];
     T s, c;
     phase_trig(p, s, c);
-    umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, threshold_state((double)p, 2));
+    umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, threshold_state((double)p, a.n_states), a.n_states);
     const int row0 = a.tile_begin * UMMA_TILE, row1 = a.tile_end * UMMA_TILE;
     if (j >= row0 && j < row1) reinterpret_cast<T *>(a.phi[0])[(long long)r * a.ld_phi + (j - row0)] = p;
 }
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (threadIdx.x >= 64 && threadIdx.x - 64 < 32) {
-        best_s[threadIdx.x - 64] = LLONG_MIN;
+        best_s[threadIdx.x - 64] = a.maximize ? LLONG_MIN : LLONG_MAX;
         en_acc[threadIdx.x - 64] = 0.0;
         improved_s[threadIdx.x - 64] = 0;
     }
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     // the grid barrier of the previous pass is behind us: its cut totals are complete
                     if (prev_scored && et < R) {
                         const long long tot = *reinterpret_cast<volatile long long *>(a.events[a.rank] + (e_idx - 1) * R + et);
-                        const int imp = tot > best_s[et];
+                        const int imp = a.maximize ? (tot > best_s[et]) : (tot < best_s[et]);
                         improved_s[et] = imp;
                         if (imp) best_s[et] = tot;
                     }
@@ -439,17 +448,31 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     if (r >= R) break;                       // warp uniform
                     int D[8], Dsig = 0;
                     umma::tmem_ld8(tlane + (uint32_t)(8 * r), D);
-                    if (flags & 1) umma::tmem_ld1(tlane + (uint32_t)(8 * R + r), Dsig);
+                    const T p = pre_p[k], si = pre_s[k], ci = pre_c[k];
+                    const int st = (flags & 1) ? threshold_state((double)p, a.n_states) : 0;
+                    if (flags & 1) {
+                        if (a.n_states == 2) {
+                            umma::tmem_ld1(tlane + (uint32_t)(8 * R + r), Dsig);
+                        } else {
+                            // tcgen05.ld takes ONE column address for the whole warp: read the N state planes, keep the own state's
+                            for (int q = 0; q < a.n_states; ++q) {
+                                int v;
+                                umma::tmem_ld1(tlane + (uint32_t)(8 * R + r * a.n_states + q), v);
+                                umma::tmem_ld_wait();
+                                if (q == st) Dsig = v;
+                            }
+                        }
+                    }
                     umma::tmem_ld_wait();
 
                     const long long Sx = umma::digits_sum(D), Sy = umma::digits_sum(D + 4);
                     const long long at = (long long)r * a.ld_phi + rowl;
-                    const T p = pre_p[k], si = pre_s[k], ci = pre_c[k];
                     if (prev_scored && improved_s[r] && valid)
-                        a.best_states[at] = (uint8_t)threshold_state((double)phi_out[at], 2);   // phi_out still holds the scored phases
+                        a.best_states[at] = (uint8_t)threshold_state((double)phi_out[at], a.n_states);   // phi_out still holds the scored phases
                     if (flags & 1) {
-                        const int st = threshold_state((double)p, 2);
-                        long long contrib = valid ? ((long long)Wi - (st ? -(long long)Dsig : (long long)Dsig)) / 2 : 0;
+                        // N = 2: sum_j J_ij [s_i != s_j] = (W_i - sigma_i sum_j J_ij sigma_j) / 2;  N >= 3: sum_j J_ij [s_j == s_i]
+                        long long contrib = 0;
+                        if (valid) contrib = a.n_states == 2 ? ((long long)Wi - (st ? -(long long)Dsig : (long long)Dsig)) / 2 : (long long)Dsig;
                         for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
                         if (lane == 0)
                             for (int w = 0; w < a.world; ++w) {
@@ -474,9 +497,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         phi_out[at] = y;
                         T s2, c2;
                         phase_trig(y, s2, c2);
-                        const int st2 = threshold_state((double)y, 2);
+                        const int st2 = threshold_state((double)y, a.n_states);
                         for (int w = 0; w < a.world; ++w)
-                            umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2);
+                            umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2, a.n_states);
                     }
                 }
                 umma::tc_fence_before();
@@ -514,7 +537,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         umma::named_bar_sync(1, UMMA_EPI_THREADS);
         if ((a.flags[a.passes - 1] & 1) && et < R) {
             const long long tot = *reinterpret_cast<volatile long long *>(a.events[a.rank] + (e_idx - 1) * R + et);
-            improved_s[et] = tot > best_s[et];
+            improved_s[et] = a.maximize ? (tot > best_s[et]) : (tot < best_s[et]);
         }
         umma::named_bar_sync(1, UMMA_EPI_THREADS);
         if (a.flags[a.passes - 1] & 1) {
@@ -523,7 +546,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 const int rowl = ((int)blockIdx.x + tk * (int)gridDim.x) * UMMA_TILE + rowt;
                 if (row0 + rowl < a.n)
                     for (int r = group; r < R; r += 4)
-                        if (improved_s[r]) a.best_states[(long long)r * a.ld_phi + rowl] = (uint8_t)threshold_state((double)phi_fin[(long long)r * a.ld_phi + rowl], 2);
+                        if (improved_s[r]) a.best_states[(long long)r * a.ld_phi + rowl] = (uint8_t)threshold_state((double)phi_fin[(long long)r * a.ld_phi + rowl], a.n_states);
             }
         }
     }

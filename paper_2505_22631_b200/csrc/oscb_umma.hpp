@@ -2,6 +2,7 @@
 // with the C ABI translation unit (oscb.cu).
 #pragma once
 #include "oscb_host.hpp"
+#include <algorithm>
 
 namespace oscb {
 
@@ -17,7 +18,8 @@ struct UmmaPlan {
 std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n_pad, int64_t row_begin, int64_t row_end,
                                           cudaStream_t s);
 
-constexpr int kUmmaMaxReplicas = 28;
+constexpr int kUmmaMaxReplicas = 28;      // N = 2: 9 B rows per replica; use umma_max_replicas(N) in general
+inline int umma_max_replicas(int n_states) { return std::min(kUmmaMaxReplicas, 256 / (8 + (n_states == 2 ? 1 : n_states))); }
 constexpr int kUmmaMaxWorld = 8;
 
 // what one rank of a row-sharded run publishes about its exchange block (the memory its peers
@@ -37,6 +39,7 @@ struct UmmaSpec {
     int R = 1;
     int precision = OSCB_PREC_F32;
     int noise_on = 1;
+    int n_states = 2, maximize = 1;     // N = 2 max-cut, or N-state colouring (unit couplings)
     double K = 0, h = 0, kn_sqrt_h = 0, ks_max = 0, ks_period = 1;
     long long steps = 0, first_step = 0;
     const uint8_t *flags = nullptr;     // host [steps + 1]: bit 0 score the pass's input phases, bit 1 + energy sample

@@ -133,3 +133,38 @@ def test_fused_virtual_ranks_equal_single_handle(pkg, n, cuts, precision):
     assert np.array_equal(got.trace_t, want.trace_t) and np.array_equal(got.trace_ks, want.trace_ks)
     assert np.array_equal(got.best_trace, want.best_trace)
     assert np.array_equal(got.energy, want.energy)
+
+
+@pytest.mark.parametrize("n,N,R", [(256, 3, 4), (300, 4, 3), (200, 7, 2)])
+def test_potts_colouring_on_the_tensor_cores(pkg, oracle, n, N, R):
+    """OPM on a dense unit-coupled graph: N one-hot state planes in B give sum_j J_ij [s_j == s_i] exactly;
+    the N-th harmonic SHIL and the N-state threshold run in the epilogue.  Noise-free float64 epilogue vs
+    the oracle (1e-6 rad after 150 steps, conflicts / states / traces equal), then a noisy float32 run
+    through the result contract."""
+    rng = np.random.default_rng(N)
+    U = np.triu((rng.random((n, n)) < 0.4).astype(np.float64), 1)
+    A = U + U.T
+    Jd = pkg.CouplingMatrix.from_dense(A, storage="dense")
+    Js = pkg.CouplingMatrix.from_dense(A, storage="sparse")
+    params = pkg.SolverParams(K=0.01, ks_max=0.5, ks_period=0.5, kn=0.0, h=0.01, t_stop=1.5, n_states=N, seed=8)
+    seeds = list(range(8, 8 + R))
+    got = pkg.run_batch(Jd, params, "coloring", seeds, precision="f64", kernel="dense-tc")
+    assert got.kernel == "dense-tc" and got.steps == 150
+    ref = oracle.simulate(Js.indptr, Js.indices, Js.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period,
+                          kn=0.0, h=params.h, t_stop=params.t_stop, n_states=N, seeds=seeds, objective="coloring")
+    assert circ(got.final_phases, ref.final_phases).max() <= 1e-6          # N = 150 steps
+    assert np.array_equal(got.best_objective, ref.best_objective)
+    assert np.array_equal(got.best_states.astype(np.int64), ref.best_states)
+    assert np.array_equal(got.best_trace, ref.best_trace)
+    assert np.abs(got.energy - ref.energy).max() <= 1e-6 * n * n
+    noisy = pkg.run_batch(Jd, pkg.SolverParams.tuned_for(n, N, seed=1, t_stop=4.0), "coloring", seeds, precision="f32")
+    assert noisy.kernel == "dense-tc"
+    iu, jv = np.nonzero(np.triu(A, 1))
+    s = noisy.best_states.astype(np.int64)
+    assert s.max() < N
+    assert np.array_equal((s[:, iu] == s[:, jv]).sum(axis=1).astype(np.float64), noisy.best_objective)
+    assert np.all(np.diff(noisy.best_trace, axis=1) <= 0)
+    # weighted couplings with the colouring objective are not a tensor-core case: the SIMT path takes them
+    W = A * 2.0
+    Jw = pkg.CouplingMatrix.from_dense(W, storage="dense")
+    assert pkg.run_batch(Jw, params, "coloring", seeds[:1], precision="f32", steps=5).kernel == "stream"
