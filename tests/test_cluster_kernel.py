@@ -108,3 +108,24 @@ def test_numerical_error(pkg):
     with pytest.raises(pkg.NumericalError) as err:
         pkg.run(J, bad, "maxcut", kernel="cluster")
     assert "oscillator" in str(err.value) and "step" in str(err.value)
+
+
+def test_best_cut_distribution_matches_reference_oracle(pkg, oracle):
+    """Noise ON, the cluster kernel's device Philox stream vs the reference's numpy stream (replayed by the
+    oracle): best cuts and final-state cuts over 96 seeds agree in distribution (two-sample KS)."""
+    from scipy import stats
+    n = 96
+    iu, iv, w = random_graph_arrays(n, 0.12, seed=77, weights=(1.0,))
+    J = pkg.CouplingMatrix.from_edges(n, (iu, iv, w))
+    params = pkg.SolverParams(K=0.2, ks_max=1.0, ks_period=3.0, kn=0.15, h=0.01, t_stop=9.0, seed=1000)
+    seeds = [params.seed + r for r in range(96)]
+    want = oracle.simulate(J.indptr, J.indices, J.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period, kn=params.kn,
+                           h=params.h, t_stop=params.t_stop, n_states=2, seeds=seeds, objective="maxcut", threads=oracle.max_threads())
+    got = pkg.run_batch(J, params, "maxcut", seeds, kernel="cluster")
+    assert got.kernel == "cluster"
+    assert stats.ks_2samp(got.best_objective, want.best_objective).pvalue > 0.01
+    assert abs(got.best_objective.mean() - want.best_objective.mean()) < 0.6 * (want.best_objective.std() + 0.5)
+    iu_, jv_, w_ = J.pairs()
+    _, cut_got = oracle.score(got.final_phases, 2, iu_, jv_, w_, True)
+    _, cut_want = oracle.score(want.final_phases, 2, iu_, jv_, w_, True)
+    assert stats.ks_2samp(cut_got, cut_want).pvalue > 0.01

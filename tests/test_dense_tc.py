@@ -168,3 +168,28 @@ def test_potts_colouring_on_the_tensor_cores(pkg, oracle, n, N, R):
     W = A * 2.0
     Jw = pkg.CouplingMatrix.from_dense(W, storage="dense")
     assert pkg.run_batch(Jw, params, "coloring", seeds[:1], precision="f32", steps=5).kernel == "stream"
+
+
+@pytest.mark.parametrize("kind,N", [("maxcut", 2), ("coloring", 3)])
+def test_best_objective_distribution_matches_reference_oracle(pkg, oracle, kind, N):
+    """Noise ON, the tensor-core kernel (float32 epilogue, device Philox noise) vs the oracle with the
+    reference's numpy stream: best objectives over 96 seeds agree in distribution (two-sample KS)."""
+    from scipy import stats
+    n = 256
+    rng = np.random.default_rng(31)
+    if kind == "maxcut":
+        A = sk_graph(n, 31)
+        params = pkg.SolverParams(K=0.05, ks_max=1.0, ks_period=2.0, kn=0.15, h=0.01, t_stop=6.0, seed=500)
+    else:
+        U = np.triu((rng.random((n, n)) < 0.3).astype(np.float64), 1)
+        A = U + U.T
+        params = pkg.SolverParams(K=0.02, ks_max=0.5, ks_period=2.0, kn=0.1, h=0.01, t_stop=6.0, n_states=3, seed=500)
+    Jd = pkg.CouplingMatrix.from_dense(A, storage="dense")
+    Js = pkg.CouplingMatrix.from_dense(A, storage="sparse")
+    seeds = [params.seed + r for r in range(96)]
+    want = oracle.simulate(Js.indptr, Js.indices, Js.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period, kn=params.kn,
+                           h=params.h, t_stop=params.t_stop, n_states=N, seeds=seeds, objective=kind, threads=oracle.max_threads())
+    got = pkg.run_batch(Jd, params, kind, seeds, precision="f32")
+    assert got.kernel == "dense-tc"
+    assert stats.ks_2samp(got.best_objective, want.best_objective).pvalue > 0.01
+    assert abs(got.best_objective.mean() - want.best_objective.mean()) < 0.6 * (want.best_objective.std() + 0.5)
