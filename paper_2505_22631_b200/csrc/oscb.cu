@@ -809,7 +809,7 @@ int oscb_graph_create_dense(int device, int64_t n, const double *J, int64_t row_
         build_dense(g.get(), J);
         // integer couplings on 128-row aligned shards also get the tile images of the tensor-core kernel
         if (g->dense->kind == DENSE_I8 && row_begin % 128 == 0 && (row_end % 128 == 0 || row_end == n))
-            g->umma = umma_build_plan(g->dense->J8.p, n, g->dense->n_pad, row_begin, row_end, g->stream);
+            g->umma = umma_build_plan(g->dense->J8.p, n, g->dense->n_pad, row_begin, row_end, g->dense->complete_pm1, g->stream);
         *out = g.release();
         return OSCB_OK;
     });

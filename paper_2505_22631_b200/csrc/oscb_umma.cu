@@ -11,7 +11,7 @@
 namespace oscb {
 
 std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n_pad, int64_t row_begin, int64_t row_end,
-                                          cudaStream_t s)
+                                          bool complete_pm1, cudaStream_t s)
 {
     OSCB_REQUIRE(row_begin % UMMA_TILE == 0 && (row_end % UMMA_TILE == 0 || row_end == n),
                  "tensor-core dense path needs row shards aligned to %d rows", UMMA_TILE);
@@ -26,6 +26,15 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
     k_umma_build_a<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
                                                                             plan->tiles, plan->A_img.p, plan->W.p);
     OSCB_CUDA(cudaGetLastError());
+    plan->complete_pm1 = complete_pm1;
+    if (complete_pm1) {
+        // 1 bit per coupling: n^2 / 8 bytes (32 MB at n = 16384) stay L2 resident between Euler steps
+        plan->A_bits.alloc((size_t)lt * plan->tiles * UMMA_BITS_STAGE);
+        k_umma_build_bits<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
+                                                                                   (int)row_begin, plan->tiles,
+                                                                                   reinterpret_cast<uint32_t *>(plan->A_bits.p));
+        OSCB_CUDA(cudaGetLastError());
+    }
     OSCB_CUDA(cudaStreamSynchronize(s));
     return plan;
 }
@@ -89,8 +98,12 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.maximize = spec.maximize;
         a.score_cols = spec.n_states == 2 ? 1 : spec.n_states;
         a.NB = ((8 + a.score_cols) * spec.R + 15) / 16 * 16;
-        const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage;
-        const size_t ctl = 2048, slack = 1024;
+        // complete +-1 couplings (SK) stream as sign bits and are expanded to int8 inside the SM (OSCB_UMMA_BITS=0 disables)
+        const char *bits_env = getenv("OSCB_UMMA_BITS");
+        a.bits = (plan.complete_pm1 && spec.n_states == 2 && !(bits_env && atoi(bits_env) == 0)) ? 1 : 0;
+        a.A_bits = plan.A_bits.p;
+        const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage + (a.bits ? UMMA_BITS_STAGE : 0);
+        const size_t ctl = 2560, slack = 1024;
         a.stages = (int)std::min<size_t>(12, ((size_t)g->smem_optin - ctl - slack) / stage);
         OSCB_REQUIRE(a.stages >= 2, "not enough shared memory for the tensor-core dense pipeline");
         smem = slack + (size_t)a.stages * stage + ctl;

@@ -36,6 +36,7 @@ namespace oscb {
 constexpr int UMMA_MAXW = 8;          // ranks a row-sharded run may span
 constexpr int UMMA_TILE = 128;        // rows per tile = bytes of K per stage
 constexpr int UMMA_A_STAGE = UMMA_TILE * UMMA_TILE;
+constexpr int UMMA_BITS_STAGE = UMMA_TILE * UMMA_TILE / 8;   // the same tile as sign bits
 constexpr int UMMA_EPI_WARPS = 16;      // 4 groups x 4 TMEM lane quadrants
 constexpr int UMMA_EPI_THREADS = UMMA_EPI_WARPS * 32;
 constexpr int UMMA_THREADS = 64 + UMMA_EPI_THREADS;
@@ -64,6 +65,8 @@ struct UmmaArgs {
     int score_cols;           // score planes per replica: 1 (N = 2) or N
     long long ld_phi;         // leading dimension of phi / best_states: local rows padded to tiles
     const uint8_t *A_img;     // [local tiles][tiles][16384]
+    const uint8_t *A_bits;    // [local tiles][tiles][2048]: J as sign bits (complete +-1 graphs), expanded to int8 in shared memory
+    int bits;                 // 1: stream A_bits (L2 resident: n^2 / 8 bytes) instead of A_img
     uint8_t *B_img[2][UMMA_MAXW];  // per buffer and rank: [tiles][NB * 128]
     void *phi[2];             // [R][ld_phi] in T
     const int *W;             // [local rows] row sums of J
@@ -261,6 +264,26 @@ __global__ void k_umma_build_a(const int8_t *__restrict__ J, int n, int n_pad, i
     }
 }
 
+// int8 J rows of a complete +-1 graph -> sign-bit tile images: bit b of 32-bit word q of row r = [J > 0] of column
+// 32 q + b.  The (zero) diagonal is stored as +1; the kernel takes the self term out again in the epilogue.
+__global__ void k_umma_build_bits(const int8_t *__restrict__ J, int n, int n_pad, int rows, int row_begin, int tiles,
+                                  uint32_t *__restrict__ A_bits)
+{
+    const int lt = blockIdx.y, kb = blockIdx.x;
+    uint32_t *img = A_bits + ((size_t)lt * tiles + kb) * (UMMA_BITS_STAGE / 4);
+    for (int t = threadIdx.x; t < UMMA_TILE * 4; t += blockDim.x) {
+        const int r = t >> 2, q = t & 3;
+        const int row = lt * UMMA_TILE + r;
+        uint32_t word = 0;
+        if (row < rows)
+            for (int b = 0; b < 32; ++b) {
+                const int col = kb * UMMA_TILE + 32 * q + b;
+                if (col < n && (J[(size_t)row * n_pad + col] > 0 || col == row_begin + row)) word |= 1u << b;
+            }
+        img[t] = word;
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a)
 {
@@ -271,11 +294,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     const int stages = a.stages;
     const uint32_t b_stage = (uint32_t)a.NB * 128u;
     const uint32_t sA = base, sB = base + (uint32_t)stages * UMMA_A_STAGE;
-    uint8_t *ctl = smem + (size_t)stages * (UMMA_A_STAGE + b_stage);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(ctl);            // full[stages], empty[stages], tmem_full, tmem_empty
-    const uint32_t bar_full = umma::smem_u32(bars), bar_empty = bar_full + 8u * stages;
-    const uint32_t bar_tfull = bar_empty + 8u * stages, bar_tempty = bar_tfull + 8u;
-    long long *best_s = reinterpret_cast<long long *>(ctl + 8 * (2 * 16 + 2));   // [32]
+    const uint32_t r_stage = a.bits ? (uint32_t)UMMA_BITS_STAGE : 0u;
+    const uint32_t sR = sB + (uint32_t)stages * b_stage;                      // raw sign-bit tiles (bits mode)
+    uint8_t *ctl = smem + (size_t)stages * (UMMA_A_STAGE + b_stage + r_stage);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ctl);            // full[16], empty[16], a_full[16], tmem_full, tmem_empty
+    const uint32_t bar_full = umma::smem_u32(bars), bar_empty = bar_full + 8u * 16, bar_afull = bar_empty + 8u * 16;
+    const uint32_t bar_tfull = bar_afull + 8u * 16, bar_tempty = bar_tfull + 8u;
+    long long *best_s = reinterpret_cast<long long *>(ctl + 512);                // [32]
     double *en_acc = reinterpret_cast<double *>(best_s + 32);                    // [32]
     double *en_w = en_acc + 32;                                                  // [4][32]
     int *improved_s = reinterpret_cast<int *>(en_w + 128);                       // [32]
@@ -285,10 +310,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     const bool sys = a.world > 1;
     const int my_tiles = (a.tile_end - a.tile_begin - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const long long per_pass = (long long)my_tiles * a.tiles;
-    const uint32_t stage_tx = UMMA_A_STAGE + b_stage;
+    const uint32_t stage_tx = (a.bits ? (uint32_t)UMMA_BITS_STAGE : (uint32_t)UMMA_A_STAGE) + b_stage;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < stages; ++s) { umma::mbar_init(bar_full + 8u * s, 1); umma::mbar_init(bar_empty + 8u * s, 1); }
+        for (int s = 0; s < stages; ++s) {
+            umma::mbar_init(bar_full + 8u * s, 1);
+            umma::mbar_init(bar_empty + 8u * s, 1);
+            umma::mbar_init(bar_afull + 8u * s, 4);                 // the four warps of the expanding group
+        }
         umma::mbar_init(bar_tfull, 1);
         umma::mbar_init(bar_tempty, UMMA_EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -322,8 +351,12 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 umma::mbar_wait(bar_empty + 8u * c.s, c.ph ^ 1u);
                 umma::mbar_expect_tx(bar_full + 8u * c.s, stage_tx);
                 const int lt = (int)blockIdx.x + c.tk * (int)gridDim.x;
-                umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
-                               bar_full + 8u * c.s);
+                if (a.bits)
+                    umma::bulk_g2s(sR + (uint32_t)c.s * UMMA_BITS_STAGE, a.A_bits + ((size_t)lt * a.tiles + c.kb) * UMMA_BITS_STAGE,
+                                   UMMA_BITS_STAGE, bar_full + 8u * c.s);
+                else
+                    umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
+                                   bar_full + 8u * c.s);
                 advance(c);
             };
             auto issue_b = [&](Cursor &c, const uint8_t *Bsrc) {
@@ -363,7 +396,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     umma::mbar_wait(bar_tempty, (uint32_t)((acc_it & 1) ^ 1));
                     umma::tc_fence_after();
                     for (int kb = 0; kb < a.tiles; ++kb) {
-                        umma::mbar_wait(bar_full + 8u * s, ph);
+                        umma::mbar_wait((a.bits ? bar_afull : bar_full) + 8u * s, ph);   // bits mode: the expanded tile, not the raw one
                         umma::tc_fence_after();
                         const uint64_t ad = umma::smem_desc(sA + (uint32_t)s * UMMA_A_STAGE);
                         const uint64_t bd = umma::smem_desc(sB + (uint32_t)s * b_stage);
@@ -390,6 +423,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         const int R = a.R;
         const T hT = (T)a.h, KT = (T)a.K, knT = (T)a.kn_sqrt_h;
         long long e_idx = 0, s_idx = 0, acc_it = 0;
+        unsigned x_base = 0;        // bits mode: index of the current tile's first stage in the producer's stage sequence
         const int row0 = a.tile_begin * UMMA_TILE;
         const int cta_global = a.cta_offset + (int)blockIdx.x;
         for (long long pass = 0; pass < a.passes; ++pass) {
@@ -428,6 +462,38 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         pre_d[k] = kick;
                     }
                 }
+                if (a.bits) {
+                    // Expand this tile's sign-bit stages to the int8 K-major swizzled image the MMA reads.  The four warps of
+                    // epilogue group g take the stages it = g, g + 4, ...; inside a group thread r owns row r of the tile:
+                    // 128 sign bits (one 16-byte load) -> 128 bytes of +1 / -1 (eight 16-byte stores).  Four bits at a time:
+                    // m = (x * 0x00204081) & 0x01010101 puts bit k into byte k (the four shifted copies do not overlap, so
+                    // the product has no carries), (m * 0xFE) ^ 0xFFFFFFFF maps 1 -> 0x01 and 0 -> 0xFF.
+                    const int r = ((warp - 2) & 3) * 32 + lane;
+                    for (int kb = group; kb < a.tiles; kb += 4) {
+                        const unsigned it = x_base + (unsigned)kb;           // position in the producer's stage sequence
+                        const int xs = (int)(it % (unsigned)stages);
+                        const uint32_t xph = (it / (unsigned)stages) & 1u;
+                        umma::mbar_wait(bar_full + 8u * xs, xph);
+                        const uint4 rowbits = *reinterpret_cast<const uint4 *>(smem + (sR - base) + (size_t)xs * UMMA_BITS_STAGE + r * 16);
+                        const uint32_t words[4] = {rowbits.x, rowbits.y, rowbits.z, rowbits.w};
+                        uint8_t *dstA = smem + (size_t)xs * UMMA_A_STAGE + r * 128;
+#pragma unroll
+                        for (int cw = 0; cw < 8; ++cw) {                 // 16 output bytes = 16 bits
+                            const uint32_t half = (words[cw >> 1] >> (16 * (cw & 1))) & 0xFFFFu;
+                            uint32_t o[4];
+#pragma unroll
+                            for (int nb = 0; nb < 4; ++nb) {
+                                const uint32_t x = (half >> (4 * nb)) & 0xFu;
+                                o[nb] = (((x * 0x00204081u) & 0x01010101u) * 0xFEu) ^ 0xFFFFFFFFu;
+                            }
+                            *reinterpret_cast<uint4 *>(dstA + ((cw ^ (r & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
+                        }
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // generic stores -> the tensor core's async-proxy reads
+                        __syncwarp();
+                        if (lane == 0) umma::mbar_arrive(bar_afull + 8u * xs);
+                    }
+                    x_base += (unsigned)a.tiles;
+                }
                 umma::mbar_wait(bar_tfull, (uint32_t)(acc_it & 1));
                 umma::tc_fence_after();
                 if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 1] = clock64();
@@ -465,6 +531,15 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     }
                     umma::tmem_ld_wait();
 
+                    if (a.bits && valid) {
+                        // the sign-bit image carries +1 on the diagonal: take the self term out (exact integers)
+                        int dc[4], ds[4];
+                        umma::pair_digits<T>(pre_c[k], dc);
+                        umma::pair_digits<T>(pre_s[k], ds);
+#pragma unroll
+                        for (int q4 = 0; q4 < 4; ++q4) { D[q4] -= dc[q4]; D[4 + q4] -= ds[q4]; }
+                        if (flags & 1) Dsig -= st ? -1 : 1;
+                    }
                     const long long Sx = umma::digits_sum(D), Sy = umma::digits_sum(D + 4);
                     const long long at = (long long)r * a.ld_phi + rowl;
                     if (prev_scored && improved_s[r] && valid)

@@ -10,13 +10,15 @@ namespace oscb {
 struct UmmaPlan {
     int n = 0, tiles = 0, tile_begin = 0, tile_end = 0;
     DevBuf<uint8_t> A_img;
+    DevBuf<uint8_t> A_bits;   // sign-bit images, only for complete +-1 graphs (every off-diagonal coupling is +1 or -1)
+    bool complete_pm1 = false;
     DevBuf<int> W;
 };
 
 // rows [row_begin, row_end) of J as int8 [rows][n_pad] on the device -> plan (row_begin % 128 == 0;
 // row_end % 128 == 0 or row_end == n)
 std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n_pad, int64_t row_begin, int64_t row_end,
-                                          cudaStream_t s);
+                                          bool complete_pm1, cudaStream_t s);
 
 constexpr int kUmmaMaxReplicas = 28;      // N = 2: 9 B rows per replica; use umma_max_replicas(N) in general
 inline int umma_max_replicas(int n_states) { return std::min(kUmmaMaxReplicas, 256 / (8 + (n_states == 2 ? 1 : n_states))); }
