@@ -296,25 +296,31 @@ def bench_dense(args, rank, world, local_rank):
         e2e_s = time.perf_counter() - t0
         value = R * nnz * window * args.steps / (dev_ms / 1e3)
         e2e_value = R * nnz * window * args.steps / e2e_s
-        chunks = -(-R // 28)                                      # launches per window (28 replicas per launch)
-        # algorithmic HBM bytes per Euler step: J once (1 B per coupling, int8) per launch + phases read and written
-        bytes_step = chunks * n * n + 2 * R * n * s_phi
+        bits, per_launch = g.tc_stream(2, R)                      # 8 = int8 J tiles, 4 = packed e2m1 tiles (R <= 8)
+        chunks = -(-R // per_launch)                              # launches per window
+        # algorithmic HBM bytes per Euler step: J once (bits / 8 bytes per coupling) per launch + phases read and written
+        bytes_step = chunks * n * n * bits // 8 + 2 * R * n * s_phi
         kernel_ms = dev_ms / args.steps
         achieved = bytes_step * window / (kernel_ms * 1e-3) / 1e9
         traffic = None
         tpath = ROOT / "profiles" / "dram_traffic.json"
         if tpath.exists():
-            t = json.loads(tpath.read_text()).get(f"{args.workload}:{last.kernel}:{args.precision}:{window}")
+            tj = json.loads(tpath.read_text())
+            t = tj.get(f"{args.workload}:{last.kernel}-{bits}b:{args.precision}:{window}") or \
+                (tj.get(f"{args.workload}:{last.kernel}:{args.precision}:{window}") if bits == 8 else None)
             if t:
                 traffic = t["dram_bytes_per_launch"]
-        # int8 tensor work issued: 2 * 128-row tiles * N columns * n per step (N = 16-padded 9 planes per replica)
-        nb = -(-9 * min(R, 28) // 16) * 16
+        # tensor work issued: 2 * 128-row tiles * N columns * n per step (N = 16-padded digit planes: 9 per replica
+        # against the int8 tiles, 17 against the e2m1 tiles)
+        nb = -(-(9 if bits == 8 else 17) * min(R, per_launch) // 16) * 16
         tensor_tops = 2.0 * n * n * nb * chunks * window / (kernel_ms * 1e-3) / 1e12
         line = {
             "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": args.precision + " epilogue, int8 x int8 -> int32 tensor-core sums", "data": "synthetic",
-            "config": {"workload": label, "replicas": R, "window": window, "kernel": last.kernel,
+            "vs_baseline": None, "dtype": args.precision + (" epilogue, int8 x int8 -> int32 tensor-core sums" if bits == 8 else
+                                                           " epilogue, e2m1 x e4m3 -> f32 tensor-core sums (exact integers)"),
+            "data": "synthetic",
+            "config": {"workload": label, "replicas": R, "window": window, "kernel": last.kernel, "coupling_bits": bits,
                        "replicas_per_launch": last.replicas_per_cta, "smem_bytes": last.smem_bytes, "parallelism": "one GPU",
                        "l2": "J (n^2 bytes = %.0f MB) exceeds the 126 MB L2 and is re-read from HBM every Euler step; no flush needed" % (n * n / 1e6)},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
@@ -323,8 +329,12 @@ def bench_dense(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_kind": peak_kind, "kernel": "k_dense_umma",
                          "algorithmic_bytes_per_launch": bytes_step * window / chunks, "bytes_per_update": bytes_step / (R * nnz),
-                         "tensor_int8_tops_issued": tensor_tops,
-                         "note": "one persistent launch = the whole window; per Euler step it streams J (int8) once from HBM"},
+                         "tensor_tops_issued": tensor_tops,
+                         "note": ("one persistent launch = the whole window; per Euler step it streams J (int8) once from HBM" if bits == 8 else
+                                  "one persistent launch = the whole window; per Euler step it streams J (packed e2m1, n^2/2 bytes) once "
+                                  "from HBM. This stream is paced by the tensor core reading the unpacked 16 KB A tile from shared memory "
+                                  "(~150 clk per M128xK32 MMA), not by HBM: frac is the share of HBM bandwidth it uses, "
+                                  "the same step on the int8 stream (OSCB_UMMA_FP4=0) sits at 1.0 of HBM and is slower")},
         }
         if not args.no_cpu_baseline:
             steps_cpu = max(2, min(window, int(12.0 * 80e6 * (os.cpu_count() or 1) / nnz)))
@@ -370,8 +380,10 @@ def bench_dense(args, rank, world, local_rank):
     total, dev_s = (float(x) for x in t.cpu())
     value = R * nnz * window * args.steps / dev_s
     e2e_value = R * nnz * window * args.steps / total
-    chunks = -(-R // 28)
-    bytes_step = chunks * (hi - lo) * n + 2 * R * n * s_phi           # per GPU: its shard of J once per Euler step
+    # per GPU: its shard of J once per Euler step and session (sessions of <= 28 replicas; one of <= 8 streams e2m1 tiles)
+    sessions = [min(dense_fused.MAX_REPLICAS, R - r0) for r0 in range(0, R, dense_fused.MAX_REPLICAS)]
+    chunks = len(sessions)
+    bytes_step = sum((hi - lo) * n * g.tc_stream(2, r)[0] // 8 for r in sessions) + 2 * R * n * s_phi
     achieved = bytes_step * window * args.steps / dev_s / 1e9
     if rank == 0:
         print(json.dumps({

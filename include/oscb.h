@@ -211,6 +211,13 @@ int oscb_dense_fused_launch(oscb_fused *f);
 int oscb_dense_fused_finish(oscb_fused *f, oscb_run_outputs *out);
 int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows);
 int oscb_dense_fused_destroy(oscb_fused *f);
+/* What a tensor-core dense run of R replicas on this handle streams: bits per coupling of the J
+ * image it reads every Euler step (8 = int8 tiles; 4 = packed e2m1 tiles, taken when every coupling
+ * is in {0, +-1, +-2, +-3, +-4, +-6} and R <= 8, where the halved HBM bytes win) and the replicas one
+ * launch integrates (R above that runs as several launches).  OSCB_EINVAL when the handle has no
+ * tensor-core plan (non-integer couplings, or not a dense handle). */
+int oscb_dense_tc_stream(const oscb_graph *g, int32_t n_states, int64_t R, int32_t *coupling_bits,
+                         int32_t *replicas_per_launch);
 
 /* Device self-test behind the scoring shortcuts of the float32 kernel: counts the float32 phases in
  * [0, 1) (all 2^30-ish of them) whose sign-bit-of-cosine state (N = 2), or whose state from the

@@ -13,7 +13,7 @@ enum DenseKind { DENSE_I8 = 0, DENSE_F = 1 };
 struct DensePlan {
     int kind = DENSE_F;
     int n_pad = 0;
-    bool complete_pm1 = false;   // every off-diagonal coupling of the shard's rows is +1 or -1 (SK-type)
+    bool fp4_ok = false;         // every coupling of the shard's rows is in {0, +-1, +-2, +-3, +-4, +-6} (e2m1 values)
     DevBuf<int8_t> J8;
     DevBuf<float> J32;
     DevBuf<double> J64;
@@ -24,7 +24,7 @@ static void build_dense(oscb_graph *g, const double *J)
 {
     const int64_t n = g->n, rows = g->row_end - g->row_begin;
     const int n_pad = (int)((n + 3) / 4 * 4);
-    bool unit = true, integral = true, small = true, pm1 = true;
+    bool unit = true, integral = true, small = true, fp4 = true;
     int64_t nnz = 0, pairs = 0, maxdeg = 0;
     for (int64_t q = 0; q < rows; ++q) {
         const int64_t i = g->row_begin + q;
@@ -33,7 +33,7 @@ static void build_dense(oscb_graph *g, const double *J)
             const double v = J[q * n + j];
             OSCB_REQUIRE(std::isfinite(v), "non-finite coupling at (%lld, %lld)", (long long)i, (long long)j);
             OSCB_REQUIRE(i != j || v == 0.0, "coupling diagonal must be zero");
-            if (i != j && v != 1.0 && v != -1.0) pm1 = false;
+            { const double m = std::fabs(v); if (!(m == 0.0 || m == 1.0 || m == 2.0 || m == 3.0 || m == 4.0 || m == 6.0)) fp4 = false; }
             if (v != 0.0) {
                 ++d;
                 if (j > i) ++pairs;
@@ -52,7 +52,7 @@ static void build_dense(oscb_graph *g, const double *J)
     g->int_weights = integral;
     auto plan = std::make_shared<DensePlan>();
     plan->n_pad = n_pad;
-    plan->complete_pm1 = pm1 && n > 1;
+    plan->fp4_ok = fp4;
     cudaStream_t s = g->stream;
     const size_t elems = (size_t)rows * n_pad;
     if (integral && small) {

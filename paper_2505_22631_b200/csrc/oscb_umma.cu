@@ -11,7 +11,7 @@
 namespace oscb {
 
 std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n_pad, int64_t row_begin, int64_t row_end,
-                                          bool complete_pm1, cudaStream_t s)
+                                          bool fp4_ok, cudaStream_t s)
 {
     OSCB_REQUIRE(row_begin % UMMA_TILE == 0 && (row_end % UMMA_TILE == 0 || row_end == n),
                  "tensor-core dense path needs row shards aligned to %d rows", UMMA_TILE);
@@ -26,13 +26,12 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
     k_umma_build_a<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
                                                                             plan->tiles, plan->A_img.p, plan->W.p);
     OSCB_CUDA(cudaGetLastError());
-    plan->complete_pm1 = complete_pm1;
-    if (complete_pm1) {
-        // 1 bit per coupling: n^2 / 8 bytes (32 MB at n = 16384) stay L2 resident between Euler steps
-        plan->A_bits.alloc((size_t)lt * plan->tiles * UMMA_BITS_STAGE);
-        k_umma_build_bits<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
-                                                                                   (int)row_begin, plan->tiles,
-                                                                                   reinterpret_cast<uint32_t *>(plan->A_bits.p));
+    plan->fp4_ok = fp4_ok;
+    if (fp4_ok) {
+        // 4 bits per coupling: half the HBM bytes of the int8 image
+        plan->A_fp4.alloc((size_t)lt * plan->tiles * UMMA_RAW_STAGE);
+        k_umma_build_fp4<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
+                                                                                  plan->tiles, 0, plan->A_fp4.p);
         OSCB_CUDA(cudaGetLastError());
     }
     OSCB_CUDA(cudaStreamSynchronize(s));
@@ -41,6 +40,51 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
 
 static inline size_t round256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point: no link-time dependency on libcuda
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *, const cuuint64_t *,
+                                  const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled()
+{
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        OSCB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        OSCB_REQUIRE(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled is not available from this driver");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// the packed e2m1 image as a 2-D tensor of 4-bit elements: 128 per row (64 bytes), one row per (tile, k-block, row)
+static CUtensorMap fp4_tensor_map(const UmmaPlan &plan)
+{
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    const cuuint64_t rows = (cuuint64_t)(plan.tile_end - plan.tile_begin) * plan.tiles * UMMA_TILE;
+    const cuuint64_t dims[2] = {UMMA_TILE, rows};
+    const cuuint64_t strides[1] = {UMMA_TILE / 2};
+    const cuuint32_t box[2] = {UMMA_TILE, UMMA_TILE}, estr[2] = {1, 1};
+    const CUresult rc = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2, (void *)plan.A_fp4.p, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    OSCB_REQUIRE(rc == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
+    return map;
+}
+
+// The e2m1 stream halves the HBM bytes of J and is bit-identical to the int8 stream.  With J as the A operand the
+// tensor core reads the 16 KB unpacked tile from shared memory at ~26-29 B/clk/SM (4 MMAs of M 128 x K 32 per stage),
+// so it is MMA-paced, not HBM-paced: 36.8 us per Euler step of SK 16384 at R = 1 against 41.8 us for the HBM-bound int8
+// stream, ahead up to 8 replicas per launch (17 B columns per replica instead of 9), behind beyond that.
+// OSCB_UMMA_FP4 = 0 / 1 forces the choice.
+bool umma_uses_fp4(const UmmaPlan &plan, int R)
+{
+    if (!plan.fp4_ok) return false;
+    if (const char *env = getenv("OSCB_UMMA_FP4")) return atoi(env) == 1;
+    return R <= 8;
+}
+
 struct UmmaSession::Impl {
     oscb_graph *g = nullptr;
     const UmmaPlan *plan = nullptr;
@@ -48,6 +92,7 @@ struct UmmaSession::Impl {
     std::vector<uint8_t> flags;
     int world = 1, rank = 0;
     UmmaArgs a{};
+    CUtensorMap tmap_a4;      // fp4 mode: the packed e2m1 image (zero otherwise)
     // the exchange block (one cudaMalloc, so one IPC handle): [barrier counter | events | energy partials | B0 | B1]
     unsigned char *xbase = nullptr;
     size_t xbytes = 0, off_events = 0, off_en = 0, off_b[2] = {0, 0};
@@ -76,8 +121,9 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
     try {
         OSCB_REQUIRE(g && g->umma, "handle has no tensor-core plan (integer couplings |J| <= 127 on 128-row aligned shards)");
         OSCB_REQUIRE(spec.n_states >= 2 && spec.n_states <= 16, "tensor-core dense path takes N = 2..16 states");
-        OSCB_REQUIRE(spec.R >= 1 && spec.R <= umma_max_replicas(spec.n_states), "tensor-core dense path takes 1..%d replicas per launch at N = %d",
-                     umma_max_replicas(spec.n_states), spec.n_states);
+        const bool want_fp4 = umma_uses_fp4(*g->umma, spec.R_total > 0 ? spec.R_total : spec.R);
+        OSCB_REQUIRE(spec.R >= 1 && spec.R <= umma_max_replicas(spec.n_states, want_fp4),
+                     "tensor-core dense path takes 1..%d replicas per launch at N = %d", umma_max_replicas(spec.n_states, want_fp4), spec.n_states);
         OSCB_REQUIRE(world >= 1 && world <= kUmmaMaxWorld && rank >= 0 && rank < world, "bad world / rank %d / %d", world, rank);
         m->g = g;
         m->plan = g->umma.get();
@@ -94,15 +140,18 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.tile_begin = plan.tile_begin;
         a.tile_end = plan.tile_end;
         a.R = spec.R;
+        // couplings representable in e2m1 stream as packed 4-bit codes through the TMA unpack path when few replicas share the launch
+        a.fp4 = umma_uses_fp4(plan, spec.R_total > 0 ? spec.R_total : spec.R) ? 1 : 0;
+        a.A_fp4 = plan.A_fp4.p;
+        std::memset(&m->tmap_a4, 0, sizeof(m->tmap_a4));
+        if (a.fp4) m->tmap_a4 = fp4_tensor_map(plan);
+        a.dcols = a.fp4 ? 16 : 8;
         a.n_states = spec.n_states;
         a.maximize = spec.maximize;
         a.score_cols = spec.n_states == 2 ? 1 : spec.n_states;
-        a.NB = ((8 + a.score_cols) * spec.R + 15) / 16 * 16;
-        // complete +-1 couplings (SK) stream as sign bits and are expanded to int8 inside the SM (OSCB_UMMA_BITS=0 disables)
-        const char *bits_env = getenv("OSCB_UMMA_BITS");
-        a.bits = (plan.complete_pm1 && spec.n_states == 2 && !(bits_env && atoi(bits_env) == 0)) ? 1 : 0;
-        a.A_bits = plan.A_bits.p;
-        const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage + (a.bits ? UMMA_BITS_STAGE : 0);
+        a.NB = ((a.dcols + a.score_cols) * spec.R + 15) / 16 * 16;
+        OSCB_REQUIRE(a.NB <= 256, "too many replicas for one launch (%d B rows)", a.NB);
+        const size_t b_stage = (size_t)a.NB * 128, stage = UMMA_A_STAGE + b_stage;
         const size_t ctl = 2560, slack = 1024;
         a.stages = (int)std::min<size_t>(12, ((size_t)g->smem_optin - ctl - slack) / stage);
         OSCB_REQUIRE(a.stages >= 2, "not enough shared memory for the tensor-core dense pipeline");
@@ -254,10 +303,11 @@ void UmmaSession::launch()
 {
     cudaStream_t s = m->g->stream;
     OSCB_CUDA(cudaSetDevice(m->g->device));
-    const void *fn = m->tsize == 8 ? (const void *)k_dense_umma<double> : (const void *)k_dense_umma<float>;
+    const void *fn = m->a.fp4 ? (m->tsize == 8 ? (const void *)k_dense_umma<double, true> : (const void *)k_dense_umma<float, true>)
+                              : (m->tsize == 8 ? (const void *)k_dense_umma<double, false> : (const void *)k_dense_umma<float, false>);
     OSCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     OSCB_CUDA(cudaEventRecord(m->ev0, s));
-    void *kargs[] = {(void *)&m->a};
+    void *kargs[] = {(void *)&m->a, (void *)&m->tmap_a4};
     OSCB_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(UMMA_THREADS), kargs, smem, s));
     OSCB_CUDA(cudaEventRecord(m->ev1, s));
 }

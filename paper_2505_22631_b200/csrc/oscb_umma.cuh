@@ -29,6 +29,7 @@
 // r*128 + ((c/16 ^ r%8)*16) + c%16), so a stage is filled by two plain bulk copies.
 #pragma once
 #include "oscb_device.cuh"
+#include <cuda.h>      // CUtensorMap (type only; the encoder is fetched at run time, no libcuda link dependency)
 #include <limits.h>
 
 namespace oscb {
@@ -36,7 +37,7 @@ namespace oscb {
 constexpr int UMMA_MAXW = 8;          // ranks a row-sharded run may span
 constexpr int UMMA_TILE = 128;        // rows per tile = bytes of K per stage
 constexpr int UMMA_A_STAGE = UMMA_TILE * UMMA_TILE;
-constexpr int UMMA_BITS_STAGE = UMMA_TILE * UMMA_TILE / 8;   // the same tile as sign bits
+constexpr int UMMA_RAW_STAGE = UMMA_TILE * UMMA_TILE / 2;    // the same tile as packed 4-bit (e2m1) codes
 constexpr int UMMA_EPI_WARPS = 16;      // 4 groups x 4 TMEM lane quadrants
 constexpr int UMMA_EPI_THREADS = UMMA_EPI_WARPS * 32;
 constexpr int UMMA_THREADS = 64 + UMMA_EPI_THREADS;
@@ -65,8 +66,9 @@ struct UmmaArgs {
     int score_cols;           // score planes per replica: 1 (N = 2) or N
     long long ld_phi;         // leading dimension of phi / best_states: local rows padded to tiles
     const uint8_t *A_img;     // [local tiles][tiles][16384]
-    const uint8_t *A_bits;    // [local tiles][tiles][2048]: J as sign bits (complete +-1 graphs), expanded to int8 in shared memory
-    int bits;                 // 1: stream A_bits (L2 resident: n^2 / 8 bytes) instead of A_img
+    const uint8_t *A_fp4;     // [local tiles][tiles][8192]: J as packed e2m1 codes (couplings in {0, +-1, +-2, +-3, +-4, +-6})
+    int fp4;                  // 1: stream A_fp4 (half the HBM bytes), kind::f8f6f4 MMA against e4m3 base-16 digit planes
+    int dcols;                // digit columns per replica: 8 (int8 mode: 4 base-256 digits per component) or 16 (fp4 mode: 8 base-16 digits)
     uint8_t *B_img[2][UMMA_MAXW];  // per buffer and rank: [tiles][NB * 128]
     void *phi[2];             // [R][ld_phi] in T
     const int *W;             // [local rows] row sums of J
@@ -112,6 +114,12 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes
 {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// TMA tile load: box (x .. x + 127 elements, y .. y + 127 rows) of a 2-D tensor map into shared memory
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar)
+{
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                 ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar) : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar)
@@ -122,6 +130,18 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t b
 {
     asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
                  ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void mma_f8f6f4(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate)
+{
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p; }"
+                 ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]),
+                   "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(taddr) : "memory");
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8])
 {
@@ -152,6 +172,12 @@ __host__ __device__ inline uint32_t instr_desc_i8(int nb)
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(UMMA_TILE >> 4) << 24);
 }
 
+// D = float32, A = e2m1 (4-bit codes, 16 per 16-byte slot: 8 bytes of data + 8 of padding), B = e4m3, both K-major
+__host__ __device__ inline uint32_t instr_desc_fp4(int nb)
+{
+    return (1u << 4) | (5u << 7) | (0u << 10) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(UMMA_TILE >> 4) << 24);
+}
+
 // byte offset of (row r, k-byte c) inside a swizzled [rows x 128 B] tile image
 __host__ __device__ inline uint32_t swz(uint32_t r, uint32_t c)
 {
@@ -175,24 +201,64 @@ __device__ __forceinline__ long long digits_sum(const int *D)
     return (long long)D[0] + ((long long)D[1] << 8) + ((long long)D[2] << 16) + ((long long)D[3] << 24);
 }
 
+// fp4 mode: round(c 2^30) as eight signed base-16 digits (d0 least significant, |d| <= 8), stored as e4m3 bytes
+template <typename T> __device__ __forceinline__ void pair_digits16(T v, int (&d)[8])
+{
+    int q = (sizeof(T) == 8) ? __double2int_rn((double)v * 1073741824.0) : __float2int_rn((float)v * 1073741824.0f);
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const int lo = ((q & 0xF) ^ 0x8) - 0x8;
+        d[k] = lo;
+        q = (q - lo) >> 4;
+    }
+    d[7] = q;
+}
+__device__ __forceinline__ long long digits_sum16(const int *D)
+{
+    long long s = 0;
+#pragma unroll
+    for (int k = 7; k >= 0; --k) s = (s << 4) + (long long)D[k];
+    return s;
+}
+// e4m3 byte of an integer |d| <= 8 (exactly representable: 3 mantissa bits)
+__device__ __forceinline__ uint8_t e4m3_of_small_int(int d)
+{
+    const int m = d < 0 ? -d : d;
+    const uint32_t mag = m == 8 ? 0x50u : (uint32_t)((0x4E4C4A4844403800ull >> (8 * m)) & 0xFFu);
+    return (uint8_t)(mag | (d < 0 ? 0x80u : 0u));
+}
+
 // write the 8 digit bytes and the spin of oscillator (tile kb, column c) for replica r into one B image
 template <typename T>
-__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state, int n_states)
+__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state, int n_states, int fp4)
 {
     uint8_t *base = Bimg + (size_t)kb * NB * 128;
-    int dc[4], ds[4];
-    pair_digits<T>(cv, dc);
-    pair_digits<T>(sv, ds);
+    const int dcols = fp4 ? 16 : 8;
+    if (fp4) {
+        int dc[8], ds[8];
+        pair_digits16<T>(cv, dc);
+        pair_digits16<T>(sv, ds);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        base[swz(8 * r + k, c)] = (uint8_t)dc[k];
-        base[swz(8 * r + 4 + k, c)] = (uint8_t)ds[k];
+        for (int k = 0; k < 8; ++k) {
+            base[swz(16 * r + k, c)] = e4m3_of_small_int(dc[k]);
+            base[swz(16 * r + 8 + k, c)] = e4m3_of_small_int(ds[k]);
+        }
+    } else {
+        int dc[4], ds[4];
+        pair_digits<T>(cv, dc);
+        pair_digits<T>(sv, ds);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            base[swz(8 * r + k, c)] = (uint8_t)dc[k];
+            base[swz(8 * r + 4 + k, c)] = (uint8_t)ds[k];
+        }
     }
+    const uint8_t plus = fp4 ? 0x38 : 0x01, minus = fp4 ? 0xB8 : 0xFF;           // +1 / -1 as e4m3 or int8
     if (n_states == 2) {
-        base[swz(8 * R + r, c)] = (uint8_t)(state ? -1 : 1);                     // spin plane: sum_j J_ij sigma_j
+        base[swz(dcols * R + r, c)] = state ? minus : plus;                      // spin plane: sum_j J_ij sigma_j
     } else {
         for (int k = 0; k < n_states; ++k)                                       // one-hot planes: sum_j J_ij [s_j == k]
-            base[swz(8 * R + r * n_states + k, c)] = (uint8_t)(k == state ? 1 : 0);
+            base[swz(dcols * R + r * n_states + k, c)] = k == state ? plus : (uint8_t)0;
     }
 }
 
@@ -222,7 +288,7 @@ __global__ void k_umma_init(UmmaArgs a, const double *__restrict__ phi0)
     const T p = (T)phi0[q];
     T s, c;
     phase_trig(p, s, c);
-    umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, threshold_state((double)p, a.n_states), a.n_states);
+    umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, threshold_state((double)p, a.n_states), a.n_states, a.fp4);
     const int row0 = a.tile_begin * UMMA_TILE, row1 = a.tile_end * UMMA_TILE;
     if (j >= row0 && j < row1) reinterpret_cast<T *>(a.phi[0])[(long long)r * a.ld_phi + (j - row0)] = p;
 }
@@ -264,28 +330,32 @@ __global__ void k_umma_build_a(const int8_t *__restrict__ J, int n, int n_pad, i
     }
 }
 
-// int8 J rows of a complete +-1 graph -> sign-bit tile images: bit b of 32-bit word q of row r = [J > 0] of column
-// 32 q + b.  The (zero) diagonal is stored as +1; the kernel takes the self term out again in the epilogue.
-__global__ void k_umma_build_bits(const int8_t *__restrict__ J, int n, int n_pad, int rows, int row_begin, int tiles,
-                                  uint32_t *__restrict__ A_bits)
+// int8 J rows with every coupling in {0, +-1, +-2, +-3, +-4, +-6} -> packed e2m1 tiles in plain row-major form (the TMA
+// unit swizzles and unpacks): tile (lt, kb) is 128 consecutive rows of 64 bytes, byte b of a row holds column 2b in its
+// low nibble and column 2b + 1 in its high nibble.
+__global__ void k_umma_build_fp4(const int8_t *__restrict__ J, int n, int n_pad, int rows, int tiles, int hi_first,
+                                 uint8_t *__restrict__ A_fp4)
 {
     const int lt = blockIdx.y, kb = blockIdx.x;
-    uint32_t *img = A_bits + ((size_t)lt * tiles + kb) * (UMMA_BITS_STAGE / 4);
-    for (int t = threadIdx.x; t < UMMA_TILE * 4; t += blockDim.x) {
-        const int r = t >> 2, q = t & 3;
+    uint8_t *img = A_fp4 + ((size_t)lt * tiles + kb) * UMMA_RAW_STAGE;
+    for (int t = threadIdx.x; t < UMMA_RAW_STAGE; t += blockDim.x) {
+        const int r = t >> 6, b = t & 63;
         const int row = lt * UMMA_TILE + r;
-        uint32_t word = 0;
-        if (row < rows)
-            for (int b = 0; b < 32; ++b) {
-                const int col = kb * UMMA_TILE + 32 * q + b;
-                if (col < n && (J[(size_t)row * n_pad + col] > 0 || col == row_begin + row)) word |= 1u << b;
-            }
-        img[t] = word;
+        uint32_t code[2] = {0, 0};
+        for (int h = 0; h < 2; ++h) {
+            const int col = kb * UMMA_TILE + 2 * b + h;
+            int v = 0;
+            if (row < rows && col < n) v = J[(size_t)row * n_pad + col];
+            const int m = v < 0 ? -v : v;
+            const uint32_t mag = m == 0 ? 0u : m == 1 ? 2u : m == 2 ? 4u : m == 3 ? 5u : m == 4 ? 6u : 7u;   // 6 -> 7
+            code[h] = mag | (v < 0 ? 8u : 0u);
+        }
+        img[t] = (uint8_t)(hi_first ? (code[1] | (code[0] << 4)) : (code[0] | (code[1] << 4)));
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a)
+template <typename T, bool FP4>
+__global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a, const __grid_constant__ CUtensorMap tmap_a4)
 {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = umma::smem_u32(smem_raw);
@@ -294,12 +364,10 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     const int stages = a.stages;
     const uint32_t b_stage = (uint32_t)a.NB * 128u;
     const uint32_t sA = base, sB = base + (uint32_t)stages * UMMA_A_STAGE;
-    const uint32_t r_stage = a.bits ? (uint32_t)UMMA_BITS_STAGE : 0u;
-    const uint32_t sR = sB + (uint32_t)stages * b_stage;                      // raw sign-bit tiles (bits mode)
-    uint8_t *ctl = smem + (size_t)stages * (UMMA_A_STAGE + b_stage + r_stage);
-    uint64_t *bars = reinterpret_cast<uint64_t *>(ctl);            // full[16], empty[16], a_full[16], tmem_full, tmem_empty
-    const uint32_t bar_full = umma::smem_u32(bars), bar_empty = bar_full + 8u * 16, bar_afull = bar_empty + 8u * 16;
-    const uint32_t bar_tfull = bar_afull + 8u * 16, bar_tempty = bar_tfull + 8u;
+    uint8_t *ctl = smem + (size_t)stages * (UMMA_A_STAGE + b_stage);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ctl);            // full[16], empty[16], tmem_full, tmem_empty
+    const uint32_t bar_full = umma::smem_u32(bars), bar_empty = bar_full + 8u * 16;
+    const uint32_t bar_tfull = bar_empty + 8u * 16, bar_tempty = bar_tfull + 8u;
     long long *best_s = reinterpret_cast<long long *>(ctl + 512);                // [32]
     double *en_acc = reinterpret_cast<double *>(best_s + 32);                    // [32]
     double *en_w = en_acc + 32;                                                  // [4][32]
@@ -310,13 +378,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     const bool sys = a.world > 1;
     const int my_tiles = (a.tile_end - a.tile_begin - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const long long per_pass = (long long)my_tiles * a.tiles;
-    const uint32_t stage_tx = (a.bits ? (uint32_t)UMMA_BITS_STAGE : (uint32_t)UMMA_A_STAGE) + b_stage;
+    // transaction bytes of a stage: the TMA unit counts the PACKED bytes it fetched for the e2m1 tile (8 KB), not the 16 KB it writes
+    const uint32_t stage_tx = (FP4 ? (uint32_t)UMMA_RAW_STAGE : (uint32_t)UMMA_A_STAGE) + b_stage;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
             umma::mbar_init(bar_full + 8u * s, 1);
             umma::mbar_init(bar_empty + 8u * s, 1);
-            umma::mbar_init(bar_afull + 8u * s, 4);                 // the four warps of the expanding group
         }
         umma::mbar_init(bar_tfull, 1);
         umma::mbar_init(bar_tempty, UMMA_EPI_WARPS);
@@ -351,9 +419,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 umma::mbar_wait(bar_empty + 8u * c.s, c.ph ^ 1u);
                 umma::mbar_expect_tx(bar_full + 8u * c.s, stage_tx);
                 const int lt = (int)blockIdx.x + c.tk * (int)gridDim.x;
-                if (a.bits)
-                    umma::bulk_g2s(sR + (uint32_t)c.s * UMMA_BITS_STAGE, a.A_bits + ((size_t)lt * a.tiles + c.kb) * UMMA_BITS_STAGE,
-                                   UMMA_BITS_STAGE, bar_full + 8u * c.s);
+                if (FP4)      // packed e2m1 rows (64 B each) -> 16 codes per 16-byte slot, 128-byte swizzled: the TMA unit unpacks
+                    umma::tma_load_2d(sA + (uint32_t)c.s * UMMA_A_STAGE, &tmap_a4, 0, (lt * a.tiles + c.kb) * UMMA_TILE, bar_full + 8u * c.s);
                 else
                     umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
                                    bar_full + 8u * c.s);
@@ -387,7 +454,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            const uint32_t idesc = umma::instr_desc_i8(a.NB);
+            const uint32_t idesc = FP4 ? umma::instr_desc_fp4(a.NB) : umma::instr_desc_i8(a.NB);
             long long acc_it = 0;
             int s = 0;
             uint32_t ph = 0;
@@ -396,12 +463,15 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     umma::mbar_wait(bar_tempty, (uint32_t)((acc_it & 1) ^ 1));
                     umma::tc_fence_after();
                     for (int kb = 0; kb < a.tiles; ++kb) {
-                        umma::mbar_wait((a.bits ? bar_afull : bar_full) + 8u * s, ph);   // bits mode: the expanded tile, not the raw one
+                        umma::mbar_wait(bar_full + 8u * s, ph);
                         umma::tc_fence_after();
                         const uint64_t ad = umma::smem_desc(sA + (uint32_t)s * UMMA_A_STAGE);
                         const uint64_t bd = umma::smem_desc(sB + (uint32_t)s * b_stage);
 #pragma unroll
-                        for (int k = 0; k < 4; ++k) umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
+                        for (int k = 0; k < 4; ++k) {
+                            if (FP4) umma::mma_f8f6f4(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
+                            else umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
+                        }
                         umma::tc_commit(bar_empty + 8u * s);
                         if (++s == stages) { s = 0; ph ^= 1u; }
                     }
@@ -423,7 +493,6 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         const int R = a.R;
         const T hT = (T)a.h, KT = (T)a.K, knT = (T)a.kn_sqrt_h;
         long long e_idx = 0, s_idx = 0, acc_it = 0;
-        unsigned x_base = 0;        // bits mode: index of the current tile's first stage in the producer's stage sequence
         const int row0 = a.tile_begin * UMMA_TILE;
         const int cta_global = a.cta_offset + (int)blockIdx.x;
         for (long long pass = 0; pass < a.passes; ++pass) {
@@ -462,38 +531,6 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         pre_d[k] = kick;
                     }
                 }
-                if (a.bits) {
-                    // Expand this tile's sign-bit stages to the int8 K-major swizzled image the MMA reads.  The four warps of
-                    // epilogue group g take the stages it = g, g + 4, ...; inside a group thread r owns row r of the tile:
-                    // 128 sign bits (one 16-byte load) -> 128 bytes of +1 / -1 (eight 16-byte stores).  Four bits at a time:
-                    // m = (x * 0x00204081) & 0x01010101 puts bit k into byte k (the four shifted copies do not overlap, so
-                    // the product has no carries), (m * 0xFE) ^ 0xFFFFFFFF maps 1 -> 0x01 and 0 -> 0xFF.
-                    const int r = ((warp - 2) & 3) * 32 + lane;
-                    for (int kb = group; kb < a.tiles; kb += 4) {
-                        const unsigned it = x_base + (unsigned)kb;           // position in the producer's stage sequence
-                        const int xs = (int)(it % (unsigned)stages);
-                        const uint32_t xph = (it / (unsigned)stages) & 1u;
-                        umma::mbar_wait(bar_full + 8u * xs, xph);
-                        const uint4 rowbits = *reinterpret_cast<const uint4 *>(smem + (sR - base) + (size_t)xs * UMMA_BITS_STAGE + r * 16);
-                        const uint32_t words[4] = {rowbits.x, rowbits.y, rowbits.z, rowbits.w};
-                        uint8_t *dstA = smem + (size_t)xs * UMMA_A_STAGE + r * 128;
-#pragma unroll
-                        for (int cw = 0; cw < 8; ++cw) {                 // 16 output bytes = 16 bits
-                            const uint32_t half = (words[cw >> 1] >> (16 * (cw & 1))) & 0xFFFFu;
-                            uint32_t o[4];
-#pragma unroll
-                            for (int nb = 0; nb < 4; ++nb) {
-                                const uint32_t x = (half >> (4 * nb)) & 0xFu;
-                                o[nb] = (((x * 0x00204081u) & 0x01010101u) * 0xFEu) ^ 0xFFFFFFFFu;
-                            }
-                            *reinterpret_cast<uint4 *>(dstA + ((cw ^ (r & 7)) << 4)) = make_uint4(o[0], o[1], o[2], o[3]);
-                        }
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");     // generic stores -> the tensor core's async-proxy reads
-                        __syncwarp();
-                        if (lane == 0) umma::mbar_arrive(bar_afull + 8u * xs);
-                    }
-                    x_base += (unsigned)a.tiles;
-                }
                 umma::mbar_wait(bar_tfull, (uint32_t)(acc_it & 1));
                 umma::tc_fence_after();
                 if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 1] = clock64();
@@ -512,18 +549,20 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 for (int k = 0; k < UMMA_RPG; ++k) {
                     const int r = group + 4 * k;
                     if (r >= R) break;                       // warp uniform
-                    int D[8], Dsig = 0;
-                    umma::tmem_ld8(tlane + (uint32_t)(8 * r), D);
+                    int D[16], Dsig = 0;
+                    const int dcols = a.dcols;
+                    if (FP4) umma::tmem_ld16(tlane + (uint32_t)(16 * r), D);
+                    else umma::tmem_ld8(tlane + (uint32_t)(8 * r), reinterpret_cast<int (&)[8]>(D));
                     const T p = pre_p[k], si = pre_s[k], ci = pre_c[k];
                     const int st = (flags & 1) ? threshold_state((double)p, a.n_states) : 0;
                     if (flags & 1) {
                         if (a.n_states == 2) {
-                            umma::tmem_ld1(tlane + (uint32_t)(8 * R + r), Dsig);
+                            umma::tmem_ld1(tlane + (uint32_t)(dcols * R + r), Dsig);
                         } else {
                             // tcgen05.ld takes ONE column address for the whole warp: read the N state planes, keep the own state's
                             for (int q = 0; q < a.n_states; ++q) {
                                 int v;
-                                umma::tmem_ld1(tlane + (uint32_t)(8 * R + r * a.n_states + q), v);
+                                umma::tmem_ld1(tlane + (uint32_t)(dcols * R + r * a.n_states + q), v);
                                 umma::tmem_ld_wait();
                                 if (q == st) Dsig = v;
                             }
@@ -531,16 +570,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     }
                     umma::tmem_ld_wait();
 
-                    if (a.bits && valid) {
-                        // the sign-bit image carries +1 on the diagonal: take the self term out (exact integers)
-                        int dc[4], ds[4];
-                        umma::pair_digits<T>(pre_c[k], dc);
-                        umma::pair_digits<T>(pre_s[k], ds);
+                    if (FP4) {
+                        // the f8f6f4 accumulator is float32 holding exact integers (|sum| < 2^24): back to int
 #pragma unroll
-                        for (int q4 = 0; q4 < 4; ++q4) { D[q4] -= dc[q4]; D[4 + q4] -= ds[q4]; }
-                        if (flags & 1) Dsig -= st ? -1 : 1;
+                        for (int q4 = 0; q4 < 16; ++q4) D[q4] = __float2int_rn(__int_as_float(D[q4]));
+                        Dsig = __float2int_rn(__int_as_float(Dsig));
                     }
-                    const long long Sx = umma::digits_sum(D), Sy = umma::digits_sum(D + 4);
+                    const long long Sx = FP4 ? umma::digits_sum16(D) : umma::digits_sum(D);
+                    const long long Sy = FP4 ? umma::digits_sum16(D + 8) : umma::digits_sum(D + 4);
                     const long long at = (long long)r * a.ld_phi + rowl;
                     if (prev_scored && improved_s[r] && valid)
                         a.best_states[at] = (uint8_t)threshold_state((double)phi_out[at], a.n_states);   // phi_out still holds the scored phases
@@ -574,7 +611,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         phase_trig(y, s2, c2);
                         const int st2 = threshold_state((double)y, a.n_states);
                         for (int w = 0; w < a.world; ++w)
-                            umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2, a.n_states);
+                            umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2, a.n_states, FP4);
                     }
                 }
                 umma::tc_fence_before();

@@ -10,18 +10,22 @@ namespace oscb {
 struct UmmaPlan {
     int n = 0, tiles = 0, tile_begin = 0, tile_end = 0;
     DevBuf<uint8_t> A_img;
-    DevBuf<uint8_t> A_bits;   // sign-bit images, only for complete +-1 graphs (every off-diagonal coupling is +1 or -1)
-    bool complete_pm1 = false;
+    DevBuf<uint8_t> A_fp4;    // packed e2m1 images, when every coupling is in {0, +-1, +-2, +-3, +-4, +-6}
+    bool fp4_ok = false;
     DevBuf<int> W;
 };
 
 // rows [row_begin, row_end) of J as int8 [rows][n_pad] on the device -> plan (row_begin % 128 == 0;
 // row_end % 128 == 0 or row_end == n)
 std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n_pad, int64_t row_begin, int64_t row_end,
-                                          bool complete_pm1, cudaStream_t s);
+                                          bool fp4_ok, cudaStream_t s);
 
 constexpr int kUmmaMaxReplicas = 28;      // N = 2: 9 B rows per replica; use umma_max_replicas(N) in general
-inline int umma_max_replicas(int n_states) { return std::min(kUmmaMaxReplicas, 256 / (8 + (n_states == 2 ? 1 : n_states))); }
+inline int umma_max_replicas(int n_states, bool fp4 = false)
+{
+    return std::min(kUmmaMaxReplicas, 256 / ((fp4 ? 16 : 8) + (n_states == 2 ? 1 : n_states)));
+}
+bool umma_uses_fp4(const UmmaPlan &plan, int R);   // the packed e2m1 stream for a call of R replicas in all (see oscb_umma.cu)
 constexpr int kUmmaMaxWorld = 8;
 
 // what one rank of a row-sharded run publishes about its exchange block (the memory its peers
@@ -39,6 +43,7 @@ struct UmmaExchange {
 // schedule and parameters of one run of <= kUmmaMaxReplicas replicas
 struct UmmaSpec {
     int R = 1;
+    int R_total = 0;                    // replicas of the whole call (several launches): picks the stream; 0 = R
     int precision = OSCB_PREC_F32;
     int noise_on = 1;
     int n_states = 2, maximize = 1;     // N = 2 max-cut, or N-state colouring (unit couplings)

@@ -31,7 +31,7 @@ from . import _native as nat
 from .dynamics import BatchResult, _initial_phases_host, _raise, _sample_capacity
 from .model import SolverParams
 
-MAX_REPLICAS = 28
+MAX_REPLICAS = 28      # replicas per session on the int8 stream (9 B columns per replica)
 
 
 class FusedDenseRank:

@@ -218,6 +218,14 @@ class DeviceGraph:
             _raise(rc, "oscb_graph_get_info")
         return gi
 
+    def tc_stream(self, n_states: int, replicas: int) -> Tuple[int, int]:
+        """(bits per coupling, replicas per launch) of a tensor-core dense run of `replicas` replicas."""
+        bits, per = C.c_int32(0), C.c_int32(0)
+        rc = nat.lib().oscb_dense_tc_stream(self.handle, n_states, replicas, C.byref(bits), C.byref(per))
+        if rc != nat.OK:
+            _raise(rc, "oscb_dense_tc_stream")
+        return bits.value, per.value
+
     def close(self) -> None:
         if self.handle:
             nat.lib().oscb_graph_destroy(self.handle)

@@ -195,27 +195,31 @@ def test_best_objective_distribution_matches_reference_oracle(pkg, oracle, kind,
     assert abs(got.best_objective.mean() - want.best_objective.mean()) < 0.6 * (want.best_objective.std() + 0.5)
 
 
-def test_sign_bit_stream_equals_int8_stream(pkg):
-    """Complete +-1 couplings are streamed as sign bits (n^2 / 8 bytes, L2 resident) and expanded to int8 inside
-    the SM; the diagonal's +1 is taken out in the epilogue.  The integer sums are the same numbers as with the int8
-    image, so the two modes must agree bit for bit (noise on, ragged n, several tiles per CTA included)."""
-    for n, cap in ((256, None), (300, None), (640, "2")):
-        J = sk_graph(n, 900 + n)
+def test_fp4_stream_equals_int8_stream(pkg):
+    """Couplings in {0, +-1, +-2, +-3, +-4, +-6} can stream as packed e2m1 codes (half the bytes; the TMA unit unpacks
+    them into the 16-byte-slot form) and be multiplied on the f8f6f4 tensor path against e4m3 base-16 digit planes,
+    float32 accumulators holding exact integers (the default for up to 8 replicas per call).  The
+    reassembled sums are the same integers as on the int8 path, so the two modes must agree bit for bit (noise on,
+    ragged n, several tiles per CTA, zeros and weights up to 6 included)."""
+    for n, cap, weights in ((256, None, (-1.0, 1.0)), (300, None, (-6.0, -3.0, -1.0, 0.0, 0.0, 1.0, 2.0, 4.0)), (640, "2", (-1.0, 1.0))):
+        J = sk_graph(n, 900 + n, weights)
         Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
-        params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.2, h=0.01, t_stop=1.0, seed=70)
+        params = pkg.SolverParams(K=0.01, ks_max=1.0, ks_period=0.5, kn=0.2, h=0.01, t_stop=1.0, seed=70)
         seeds = [70, 71, 72]
         if cap:
             os.environ["OSCB_UMMA_MAX_GRID"] = cap
         try:
-            bits = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", kernel="dense-tc")
-            os.environ["OSCB_UMMA_BITS"] = "0"
-            try:
-                int8 = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", kernel="dense-tc")
-            finally:
-                os.environ.pop("OSCB_UMMA_BITS", None)
+            runs = {}
+            for mode in ("0", "1"):                    # 0: int8 stream, 1: packed e2m1 stream through the TMA unpack path
+                os.environ["OSCB_UMMA_FP4"] = mode
+                try:
+                    runs[mode] = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", kernel="dense-tc")
+                finally:
+                    os.environ.pop("OSCB_UMMA_FP4", None)
+            int8, fp4 = runs["0"], runs["1"]
         finally:
             os.environ.pop("OSCB_UMMA_MAX_GRID", None)
-        assert np.array_equal(bits.final_phases, int8.final_phases)
-        assert np.array_equal(bits.best_states, int8.best_states)
-        assert np.array_equal(bits.best_objective, int8.best_objective)
-        assert np.array_equal(bits.energy, int8.energy)
+        assert np.array_equal(fp4.final_phases, int8.final_phases)
+        assert np.array_equal(fp4.best_states, int8.best_states)
+        assert np.array_equal(fp4.best_objective, int8.best_objective)
+        assert np.array_equal(fp4.energy, int8.energy)
