@@ -31,7 +31,7 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
         // 4 bits per coupling: half the HBM bytes of the int8 image
         plan->A_fp4.alloc((size_t)lt * plan->tiles * UMMA_RAW_STAGE);
         k_umma_build_fp4<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
-                                                                                  plan->tiles, 0, plan->A_fp4.p);
+                                                                                  plan->tiles, plan->A_fp4.p);
         OSCB_CUDA(cudaGetLastError());
     }
     OSCB_CUDA(cudaStreamSynchronize(s));

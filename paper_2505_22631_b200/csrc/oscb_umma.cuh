@@ -110,10 +110,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
-__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes)
-{
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // TMA tile load: box (x .. x + 127 elements, y .. y + 127 rows) of a 2-D tensor map into shared memory
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar)
 {
@@ -333,7 +329,7 @@ __global__ void k_umma_build_a(const int8_t *__restrict__ J, int n, int n_pad, i
 // int8 J rows with every coupling in {0, +-1, +-2, +-3, +-4, +-6} -> packed e2m1 tiles in plain row-major form (the TMA
 // unit swizzles and unpacks): tile (lt, kb) is 128 consecutive rows of 64 bytes, byte b of a row holds column 2b in its
 // low nibble and column 2b + 1 in its high nibble.
-__global__ void k_umma_build_fp4(const int8_t *__restrict__ J, int n, int n_pad, int rows, int tiles, int hi_first,
+__global__ void k_umma_build_fp4(const int8_t *__restrict__ J, int n, int n_pad, int rows, int tiles,
                                  uint8_t *__restrict__ A_fp4)
 {
     const int lt = blockIdx.y, kb = blockIdx.x;
@@ -350,7 +346,7 @@ __global__ void k_umma_build_fp4(const int8_t *__restrict__ J, int n, int n_pad,
             const uint32_t mag = m == 0 ? 0u : m == 1 ? 2u : m == 2 ? 4u : m == 3 ? 5u : m == 4 ? 6u : 7u;   // 6 -> 7
             code[h] = mag | (v < 0 ? 8u : 0u);
         }
-        img[t] = (uint8_t)(hi_first ? (code[1] | (code[0] << 4)) : (code[0] | (code[1] << 4)));
+        img[t] = (uint8_t)(code[0] | (code[1] << 4));   // low nibble first: the order the TMA unpack keeps
     }
 }
 
