@@ -296,7 +296,7 @@ def bench_dense(args, rank, world, local_rank):
         e2e_s = time.perf_counter() - t0
         value = R * nnz * window * args.steps / (dev_ms / 1e3)
         e2e_value = R * nnz * window * args.steps / e2e_s
-        bits, per_launch = g.tc_stream(2, R)                      # 8 = int8 J tiles, 4 = packed e2m1 tiles (R <= 8)
+        bits, per_launch = g.tc_stream(2, R)                      # 8 = int8 J tiles, 4 = packed e2m1 tiles (R <= 12)
         chunks = -(-R // per_launch)                              # launches per window
         # algorithmic HBM bytes per Euler step: J once (bits / 8 bytes per coupling) per launch + phases read and written
         bytes_step = chunks * n * n * bits // 8 + 2 * R * n * s_phi
@@ -311,14 +311,14 @@ def bench_dense(args, rank, world, local_rank):
             if t:
                 traffic = t["dram_bytes_per_launch"]
         # tensor work issued: 2 * 128-row tiles * N columns * n per step (N = 16-padded digit planes: 9 per replica
-        # against the int8 tiles, 17 against the e2m1 tiles)
-        nb = -(-(9 if bits == 8 else 17) * min(R, per_launch) // 16) * 16
+        # against the int8 tiles, 21 against the e2m1 tiles)
+        nb = -(-(9 if bits == 8 else 21) * min(R, per_launch) // 16) * 16
         tensor_tops = 2.0 * n * n * nb * chunks * window / (kernel_ms * 1e-3) / 1e12
         line = {
             "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": kernel_ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.precision + (" epilogue, int8 x int8 -> int32 tensor-core sums" if bits == 8 else
-                                                           " epilogue, e2m1 x e4m3 -> f32 tensor-core sums (exact integers)"),
+                                                           " epilogue, e2m1 x e2m1 -> f32 tensor-core sums (exact integers)"),
             "data": "synthetic",
             "config": {"workload": label, "replicas": R, "window": window, "kernel": last.kernel, "coupling_bits": bits,
                        "replicas_per_launch": last.replicas_per_cta, "smem_bytes": last.smem_bytes, "parallelism": "one GPU",
@@ -332,9 +332,8 @@ def bench_dense(args, rank, world, local_rank):
                          "tensor_tops_issued": tensor_tops,
                          "note": ("one persistent launch = the whole window; per Euler step it streams J (int8) once from HBM" if bits == 8 else
                                   "one persistent launch = the whole window; per Euler step it streams J (packed e2m1, n^2/2 bytes) once "
-                                  "from HBM. This stream is paced by the tensor core reading the unpacked 16 KB A tile from shared memory "
-                                  "(~150 clk per M128xK32 MMA), not by HBM: frac is the share of HBM bandwidth it uses, "
-                                  "the same step on the int8 stream (OSCB_UMMA_FP4=0) sits at 1.0 of HBM and is slower")},
+                                  "from HBM (kind::mxf4 MMAs against e2m1 base-9 digit planes); the same step on the int8 stream "
+                                  "(OSCB_UMMA_FP4=0) sits at 1.0 of HBM with twice the bytes")},
         }
         if not args.no_cpu_baseline:
             steps_cpu = max(2, min(window, int(12.0 * 80e6 * (os.cpu_count() or 1) / nnz)))
@@ -380,7 +379,7 @@ def bench_dense(args, rank, world, local_rank):
     total, dev_s = (float(x) for x in t.cpu())
     value = R * nnz * window * args.steps / dev_s
     e2e_value = R * nnz * window * args.steps / total
-    # per GPU: its shard of J once per Euler step and session (sessions of <= 28 replicas; one of <= 8 streams e2m1 tiles)
+    # per GPU: its shard of J once per Euler step and session (sessions of <= 28 replicas; one of <= 12 streams e2m1 tiles)
     sessions = [min(dense_fused.MAX_REPLICAS, R - r0) for r0 in range(0, R, dense_fused.MAX_REPLICAS)]
     chunks = len(sessions)
     bytes_step = sum((hi - lo) * n * g.tc_stream(2, r)[0] // 8 for r in sessions) + 2 * R * n * s_phi

@@ -213,7 +213,7 @@ int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows);
 int oscb_dense_fused_destroy(oscb_fused *f);
 /* What a tensor-core dense run of R replicas on this handle streams: bits per coupling of the J
  * image it reads every Euler step (8 = int8 tiles; 4 = packed e2m1 tiles, taken when every coupling
- * is in {0, +-1, +-2, +-3, +-4, +-6} and R <= 8, where the halved HBM bytes win) and the replicas one
+ * is in {0, +-1, +-2, +-3, +-4, +-6} and the R replicas fit one launch of that stream: 12 at N = 2) and the replicas one
  * launch integrates (R above that runs as several launches).  OSCB_EINVAL when the handle has no
  * tensor-core plan (non-integer couplings, or not a dense handle). */
 int oscb_dense_tc_stream(const oscb_graph *g, int32_t n_states, int64_t R, int32_t *coupling_bits,

@@ -619,7 +619,7 @@ static void run_umma(oscb_graph *g, const oscb_run_params *p, const RunPlan &rp,
     double ms = 0.0;
     int64_t launches = 0, smem = 0;
     unsigned long long flag = ~0ull;
-    const int chunk = umma_max_replicas(p->n_states, umma_uses_fp4(*g->umma, R));
+    const int chunk = umma_max_replicas(p->n_states, umma_uses_fp4(*g->umma, R, p->n_states));
     for (int r0 = 0; r0 < R; r0 += chunk) {
         const int Rc = std::min(chunk, R - r0);
         std::vector<long long> ev((size_t)E * Rc);
@@ -1036,8 +1036,8 @@ int oscb_dense_fused_create(oscb_graph *shard, const oscb_run_params *p, int64_t
         OSCB_REQUIRE(p->kernel == OSCB_KERNEL_AUTO || p->kernel == OSCB_KERNEL_DENSE_TC, "fused dense runs use the tensor-core kernel");
         OSCB_REQUIRE(umma_applies(shard, p), "fused dense runs are N = 2 max-cut (integer couplings) or N-state colouring (unit couplings), device noise");
         OSCB_REQUIRE(p->precision == OSCB_PREC_F32 || p->precision == OSCB_PREC_F64, "unknown precision %d", p->precision);
-        OSCB_REQUIRE(R >= 1 && R <= umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R)), "fused dense runs take 1..%d replicas per session",
-                     umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R)));
+        OSCB_REQUIRE(R >= 1 && R <= umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R, p->n_states)), "fused dense runs take 1..%d replicas per session",
+                     umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R, p->n_states)));
         OSCB_REQUIRE(p->h > 0.0 && std::isfinite(p->h) && p->ks_period > 0.0, "bad h / ks_period");
         OSCB_REQUIRE(p->steps > 0 || (p->t_stop > 0.0 && std::isfinite(p->t_stop)), "t_stop must be finite and > 0");
         bind_device(shard);
@@ -1153,7 +1153,7 @@ int oscb_dense_tc_stream(const oscb_graph *g, int32_t n_states, int64_t R, int32
         OSCB_REQUIRE(g && coupling_bits && replicas_per_launch, "NULL argument");
         OSCB_REQUIRE(g->umma != nullptr, "the handle has no tensor-core plan (dense integer couplings only)");
         OSCB_REQUIRE(n_states >= 2 && n_states <= 16 && R >= 1, "n_states in 2..16 and R >= 1");
-        const bool fp4 = umma_uses_fp4(*g->umma, (int)std::min<int64_t>(R, 1 << 20));
+        const bool fp4 = umma_uses_fp4(*g->umma, (int)std::min<int64_t>(R, 1 << 20), n_states);
         *coupling_bits = fp4 ? 4 : 8;
         *replicas_per_launch = umma_max_replicas(n_states, fp4);
         return OSCB_OK;

@@ -28,10 +28,11 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
     OSCB_CUDA(cudaGetLastError());
     plan->fp4_ok = fp4_ok;
     if (fp4_ok) {
-        // 4 bits per coupling: half the HBM bytes of the int8 image
-        plan->A_fp4.alloc((size_t)lt * plan->tiles * UMMA_RAW_STAGE);
-        k_umma_build_fp4<<<dim3((unsigned)plan->tiles, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin),
-                                                                                  plan->tiles, plan->A_fp4.p);
+        // 4 bits per coupling: half the HBM bytes of the int8 image (tiles of 128 rows x 256 couplings)
+        const int kt4 = (int)((n + UMMA_K4 - 1) / UMMA_K4);
+        plan->A_fp4.alloc((size_t)lt * kt4 * UMMA_A_STAGE);
+        k_umma_build_fp4<<<dim3((unsigned)kt4, (unsigned)lt), 256, 0, s>>>(J8_dev, (int)n, n_pad, (int)(row_end - row_begin), kt4,
+                                                                          plan->A_fp4.p);
         OSCB_CUDA(cudaGetLastError());
     }
     OSCB_CUDA(cudaStreamSynchronize(s));
@@ -40,49 +41,16 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
 
 static inline size_t round256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-// cuTensorMapEncodeTiled through the runtime's driver entry point: no link-time dependency on libcuda
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *, const cuuint64_t *,
-                                  const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static EncodeTiledFn encode_tiled()
-{
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        OSCB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        OSCB_REQUIRE(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled is not available from this driver");
-        fn = reinterpret_cast<EncodeTiledFn>(p);
-    }
-    return fn;
-}
-
-// the packed e2m1 image as a 2-D tensor of 4-bit elements: 128 per row (64 bytes), one row per (tile, k-block, row)
-static CUtensorMap fp4_tensor_map(const UmmaPlan &plan)
-{
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof(map));
-    const cuuint64_t rows = (cuuint64_t)(plan.tile_end - plan.tile_begin) * plan.tiles * UMMA_TILE;
-    const cuuint64_t dims[2] = {UMMA_TILE, rows};
-    const cuuint64_t strides[1] = {UMMA_TILE / 2};
-    const cuuint32_t box[2] = {UMMA_TILE, UMMA_TILE}, estr[2] = {1, 1};
-    const CUresult rc = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, 2, (void *)plan.A_fp4.p, dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    OSCB_REQUIRE(rc == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
-    return map;
-}
-
-// The e2m1 stream halves the HBM bytes of J and is bit-identical to the int8 stream.  With J as the A operand the
-// tensor core reads the 16 KB unpacked tile from shared memory at ~26-29 B/clk/SM (4 MMAs of M 128 x K 32 per stage),
-// so it is MMA-paced, not HBM-paced: 36.8 us per Euler step of SK 16384 at R = 1 against 41.8 us for the HBM-bound int8
-// stream, ahead up to 8 replicas per launch (17 B columns per replica instead of 9), behind beyond that.
+// The e2m1 stream halves the HBM bytes of J and is bit-identical to the int8 stream.  It runs on the block-scaled 4-bit
+// tensor path (kind::mxf4, K = 64 per MMA, all scales 1.0), which also reads half the shared-memory bytes per coupling on the
+// A side: 24.5 us per Euler step of SK 16384 at R = 1 against 41.8 us for the HBM-bound int8 stream.  It needs 21 B
+// columns per replica instead of 9, so a launch takes at most 12 replicas; up to there it is ahead (R = 12: 44.6 vs 47.3 us).
 // OSCB_UMMA_FP4 = 0 / 1 forces the choice.
-bool umma_uses_fp4(const UmmaPlan &plan, int R)
+bool umma_uses_fp4(const UmmaPlan &plan, int R, int n_states)
 {
     if (!plan.fp4_ok) return false;
     if (const char *env = getenv("OSCB_UMMA_FP4")) return atoi(env) == 1;
-    return R <= 8;
+    return R <= umma_max_replicas(n_states, true);      // the whole call fits one launch of the e2m1 stream (N = 2: 12)
 }
 
 struct UmmaSession::Impl {
@@ -92,7 +60,6 @@ struct UmmaSession::Impl {
     std::vector<uint8_t> flags;
     int world = 1, rank = 0;
     UmmaArgs a{};
-    CUtensorMap tmap_a4;      // fp4 mode: the packed e2m1 image (zero otherwise)
     // the exchange block (one cudaMalloc, so one IPC handle): [barrier counter | events | energy partials | B0 | B1]
     unsigned char *xbase = nullptr;
     size_t xbytes = 0, off_events = 0, off_en = 0, off_b[2] = {0, 0};
@@ -121,7 +88,7 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
     try {
         OSCB_REQUIRE(g && g->umma, "handle has no tensor-core plan (integer couplings |J| <= 127 on 128-row aligned shards)");
         OSCB_REQUIRE(spec.n_states >= 2 && spec.n_states <= 16, "tensor-core dense path takes N = 2..16 states");
-        const bool want_fp4 = umma_uses_fp4(*g->umma, spec.R_total > 0 ? spec.R_total : spec.R);
+        const bool want_fp4 = umma_uses_fp4(*g->umma, spec.R_total > 0 ? spec.R_total : spec.R, spec.n_states);
         OSCB_REQUIRE(spec.R >= 1 && spec.R <= umma_max_replicas(spec.n_states, want_fp4),
                      "tensor-core dense path takes 1..%d replicas per launch at N = %d", umma_max_replicas(spec.n_states, want_fp4), spec.n_states);
         OSCB_REQUIRE(world >= 1 && world <= kUmmaMaxWorld && rank >= 0 && rank < world, "bad world / rank %d / %d", world, rank);
@@ -141,11 +108,10 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.tile_end = plan.tile_end;
         a.R = spec.R;
         // couplings representable in e2m1 stream as packed 4-bit codes through the TMA unpack path when few replicas share the launch
-        a.fp4 = umma_uses_fp4(plan, spec.R_total > 0 ? spec.R_total : spec.R) ? 1 : 0;
+        a.fp4 = umma_uses_fp4(plan, spec.R_total > 0 ? spec.R_total : spec.R, spec.n_states) ? 1 : 0;
         a.A_fp4 = plan.A_fp4.p;
-        std::memset(&m->tmap_a4, 0, sizeof(m->tmap_a4));
-        if (a.fp4) m->tmap_a4 = fp4_tensor_map(plan);
-        a.dcols = a.fp4 ? 16 : 8;
+        a.ktiles = a.fp4 ? (plan.n + UMMA_K4 - 1) / UMMA_K4 : plan.tiles;
+        a.dcols = a.fp4 ? 2 * UMMA_D9 : 8;
         a.n_states = spec.n_states;
         a.maximize = spec.maximize;
         a.score_cols = spec.n_states == 2 ? 1 : spec.n_states;
@@ -160,7 +126,7 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.world = world;
         a.rank = rank;
         a.tmem_cols = 32;
-        while (a.tmem_cols < a.NB) a.tmem_cols *= 2;
+        while (a.tmem_cols < a.NB + (a.fp4 ? UMMA_SF_COLS : 0)) a.tmem_cols *= 2;
         const int lt = plan.tile_end - plan.tile_begin;
         grid = std::min(lt, g->sm_count);
         if (const char *cap = getenv("OSCB_UMMA_MAX_GRID"))       // test knob: several row tiles per CTA on small graphs
@@ -178,8 +144,8 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         m->off_events = 256;
         m->off_en = m->off_events + round256(E * spec.R * sizeof(long long));
         m->off_b[0] = m->off_en + round256(S * (size_t)plan.tiles * spec.R * sizeof(double));   // <= one CTA per tile, all ranks
-        m->off_b[1] = m->off_b[0] + round256((size_t)plan.tiles * b_stage);
-        m->xbytes = m->off_b[1] + round256((size_t)plan.tiles * b_stage);
+        m->off_b[1] = m->off_b[0] + round256((size_t)a.ktiles * b_stage);
+        m->xbytes = m->off_b[1] + round256((size_t)a.ktiles * b_stage);
         OSCB_CUDA(cudaSetDevice(g->device));
         OSCB_CUDA(cudaMalloc(&m->xbase, m->xbytes));              // not pooled: the block is exported over CUDA IPC
         m->point_rank(rank, m->xbase);
@@ -292,7 +258,7 @@ void UmmaSession::prepare(const uint64_t *seeds, const double *d_phi0)
         m->d_trace.zero(s);
         a.trace = m->d_trace.p;
     }
-    const long long tot = (long long)a.n * a.R;
+    const long long tot = (long long)((a.n + 1) / 2) * a.R;      // one thread per pair of oscillators
     if (m->tsize == 8) k_umma_init<double><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, d_phi0);
     else k_umma_init<float><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, d_phi0);
     OSCB_CUDA(cudaGetLastError());
@@ -307,7 +273,7 @@ void UmmaSession::launch()
                               : (m->tsize == 8 ? (const void *)k_dense_umma<double, false> : (const void *)k_dense_umma<float, false>);
     OSCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     OSCB_CUDA(cudaEventRecord(m->ev0, s));
-    void *kargs[] = {(void *)&m->a, (void *)&m->tmap_a4};
+    void *kargs[] = {(void *)&m->a};
     OSCB_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(UMMA_THREADS), kargs, smem, s));
     OSCB_CUDA(cudaEventRecord(m->ev1, s));
 }

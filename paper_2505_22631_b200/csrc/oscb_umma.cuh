@@ -10,6 +10,12 @@
 //   Integer accumulation is exact and order independent, so the coupling sums carry only the
 //   2^-31 quantisation of each pair -- tighter than a float32 FMA chain over n = 16384 terms.
 //
+//   Second stream (template FP4), taken when every coupling is an e2m1 value {0, +-1, +-2, +-3, +-4, +-6} and the
+//   replicas fit one launch: A = J as packed 4-bit e2m1 codes (tiles of 128 rows x 256 couplings, half the HBM and
+//   shared-memory bytes), B = the same fixed-point pairs as 10 balanced base-9 digits per component (|d| <= 4, also
+//   e2m1), D = float32 in TMEM holding exact integers (|sum| <= 24 n < 2^24), block-scaled tcgen05.mma kind::mxf4
+//   (SASS UTCOMMA, K = 64 per instruction) with every ue8m0 block scale = 1.0.  Same integers, same results, bit for bit.
+//
 // Roles of the 576 threads of a CTA (one CTA per SM, one 128-row tile of J at a time):
 //   warp 0   producer: cp.async.bulk (UBLKCP) of the 16 KB tile images of A (HBM stream) and
 //            of B (L2 resident) into a ring of shared-memory stages, signalled on mbarriers;
@@ -37,7 +43,9 @@ namespace oscb {
 constexpr int UMMA_MAXW = 8;          // ranks a row-sharded run may span
 constexpr int UMMA_TILE = 128;        // rows per tile = bytes of K per stage
 constexpr int UMMA_A_STAGE = UMMA_TILE * UMMA_TILE;
-constexpr int UMMA_RAW_STAGE = UMMA_TILE * UMMA_TILE / 2;    // the same tile as packed 4-bit (e2m1) codes
+constexpr int UMMA_K4 = 256;          // e2m1 stream: oscillators per k-block (128 bytes of packed 4-bit codes per row)
+constexpr int UMMA_D9 = 10;           // e2m1 stream: balanced base-9 digits per component (9^10 / 2 > 2^30)
+constexpr int UMMA_SF_COLS = 32;      // e2m1 stream: TMEM columns in front of the accumulator holding the (all 1.0) block scales
 constexpr int UMMA_EPI_WARPS = 16;      // 4 groups x 4 TMEM lane quadrants
 constexpr int UMMA_EPI_THREADS = UMMA_EPI_WARPS * 32;
 constexpr int UMMA_THREADS = 64 + UMMA_EPI_THREADS;
@@ -47,7 +55,8 @@ constexpr int UMMA_TRACE_PASSES = 64;
 
 struct UmmaArgs {
     int n;                    // oscillators
-    int tiles;                // ceil(n / 128): row tiles of the whole graph = k-blocks
+    int tiles;                // ceil(n / 128): row tiles of the whole graph
+    int ktiles;               // k-blocks of a row tile: tiles (int8 stream, 128 couplings per 128-byte row) or ceil(n / 256) (e2m1)
     int tile_begin, tile_end; // this rank's row tiles
     int R;                    // replicas (<= UMMA_MAXR)
     int NB;                   // rows of B: round_up(9 R, 16) -- the MMA N
@@ -66,10 +75,10 @@ struct UmmaArgs {
     int score_cols;           // score planes per replica: 1 (N = 2) or N
     long long ld_phi;         // leading dimension of phi / best_states: local rows padded to tiles
     const uint8_t *A_img;     // [local tiles][tiles][16384]
-    const uint8_t *A_fp4;     // [local tiles][tiles][8192]: J as packed e2m1 codes (couplings in {0, +-1, +-2, +-3, +-4, +-6})
-    int fp4;                  // 1: stream A_fp4 (half the HBM bytes), kind::f8f6f4 MMA against e4m3 base-16 digit planes
-    int dcols;                // digit columns per replica: 8 (int8 mode: 4 base-256 digits per component) or 16 (fp4 mode: 8 base-16 digits)
-    uint8_t *B_img[2][UMMA_MAXW];  // per buffer and rank: [tiles][NB * 128]
+    const uint8_t *A_fp4;     // [local tiles][ktiles][16384]: J as packed e2m1 codes (couplings in {0, +-1, +-2, +-3, +-4, +-6})
+    int fp4;                  // 1: stream A_fp4 (half the HBM bytes), kind::mxf4 MMA against e2m1 base-9 digit planes
+    int dcols;                // digit columns per replica: 8 (int8 stream: 4 base-256 digits per component) or 20 (e2m1: 10 base-9 digits)
+    uint8_t *B_img[2][UMMA_MAXW];  // per buffer and rank: [ktiles][NB * 128]
     void *phi[2];             // [R][ld_phi] in T
     const int *W;             // [local rows] row sums of J
     const uint64_t *seeds;    // [R]
@@ -110,12 +119,6 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
-// TMA tile load: box (x .. x + 127 elements, y .. y + 127 rows) of a 2-D tensor map into shared memory
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int x, int y, uint32_t bar)
-{
-    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                 ::"r"(dst), "l"(map), "r"(x), "r"(y), "r"(bar) : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar)
@@ -127,17 +130,22 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t adesc, uint64_t b
     asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }"
                  ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
 }
-__device__ __forceinline__ void mma_f8f6f4(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate)
+// block-scaled 4-bit MMA, K = 64 per instruction; one ue8m0 scale per 32 elements of a row, read from TMEM
+__device__ __forceinline__ void mma_mxf4(uint32_t tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                         uint32_t accumulate)
 {
-    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p; }"
-                 ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate) : "memory");
+    asm volatile("{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p; }"
+                 ::"r"(tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16])
+// 16 consecutive columns of the warp's 32 TMEM lanes <- one 32-bit value
+__device__ __forceinline__ void tmem_fill16(uint32_t taddr, uint32_t v)
 {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]),
-                   "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                 : "r"(taddr) : "memory");
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, int *v)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(taddr) : "memory");
 }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8])
 {
@@ -168,10 +176,10 @@ __host__ __device__ inline uint32_t instr_desc_i8(int nb)
     return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(UMMA_TILE >> 4) << 24);
 }
 
-// D = float32, A = e2m1 (4-bit codes, 16 per 16-byte slot: 8 bytes of data + 8 of padding), B = e4m3, both K-major
-__host__ __device__ inline uint32_t instr_desc_fp4(int nb)
+// kind::mxf4 (block scaled): D = float32, A = B = e2m1 packed two per byte, both K-major, ue8m0 scales (scale ids 0), K = 64
+__host__ __device__ inline uint32_t instr_desc_mxf4(int nb)
 {
-    return (1u << 4) | (5u << 7) | (0u << 10) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(UMMA_TILE >> 4) << 24);
+    return (1u << 7) | (1u << 10) | ((uint32_t)(nb >> 3) << 17) | (1u << 23) | ((uint32_t)(UMMA_TILE >> 4) << 24);
 }
 
 // byte offset of (row r, k-byte c) inside a swizzled [rows x 128 B] tile image
@@ -197,64 +205,92 @@ __device__ __forceinline__ long long digits_sum(const int *D)
     return (long long)D[0] + ((long long)D[1] << 8) + ((long long)D[2] << 16) + ((long long)D[3] << 24);
 }
 
-// fp4 mode: round(c 2^30) as eight signed base-16 digits (d0 least significant, |d| <= 8), stored as e4m3 bytes
-template <typename T> __device__ __forceinline__ void pair_digits16(T v, int (&d)[8])
+// e2m1 stream: round(c 2^30) as ten balanced base-9 digits (d0 least significant, |d| <= 4: every digit is an e2m1 value),
+// returned as ten 4-bit e2m1 codes, digit k in bits [4k, 4k + 4)
+__device__ __forceinline__ uint32_t e2m1_of_small_int(int d)      // |d| <= 4:  0, 1, 2, 3, 4 -> codes 0, 2, 4, 5, 6; sign in bit 3
+{
+    const int m = d < 0 ? -d : d;
+    return ((0x65420u >> (4 * m)) & 0xFu) | (d < 0 ? 8u : 0u);
+}
+template <typename T> __device__ __forceinline__ uint64_t pair_codes9(T v)
 {
     int q = (sizeof(T) == 8) ? __double2int_rn((double)v * 1073741824.0) : __float2int_rn((float)v * 1073741824.0f);
+    uint64_t codes = 0;
 #pragma unroll
-    for (int k = 0; k < 7; ++k) {
-        const int lo = ((q & 0xF) ^ 0x8) - 0x8;
-        d[k] = lo;
-        q = (q - lo) >> 4;
+    for (int k = 0; k < UMMA_D9; ++k) {
+        int lo = q % 9;                      // sign of q
+        lo = lo > 4 ? lo - 9 : (lo < -4 ? lo + 9 : lo);
+        codes |= (uint64_t)e2m1_of_small_int(lo) << (4 * k);
+        q = (q - lo) / 9;
     }
-    d[7] = q;
+    return codes;
 }
-__device__ __forceinline__ long long digits_sum16(const int *D)
+__device__ __forceinline__ long long digits_sum9(const int *D)
 {
     long long s = 0;
 #pragma unroll
-    for (int k = 7; k >= 0; --k) s = (s << 4) + (long long)D[k];
+    for (int k = UMMA_D9 - 1; k >= 0; --k) s = s * 9 + (long long)D[k];
     return s;
 }
-// e4m3 byte of an integer |d| <= 8 (exactly representable: 3 mantissa bits)
-__device__ __forceinline__ uint8_t e4m3_of_small_int(int d)
+// the 4-bit codes of one oscillator and replica for the e2m1 B image: cos digits, sin digits, score planes
+// (N = 2: one spin code; N >= 3: N one-hot codes, plane k in bits [4k, 4k + 4))
+struct B4Codes {
+    uint64_t c, s, sc;
+};
+template <typename T> __device__ __forceinline__ B4Codes make_b4(T cv, T sv, int state, int n_states)
 {
-    const int m = d < 0 ? -d : d;
-    const uint32_t mag = m == 8 ? 0x50u : (uint32_t)((0x4E4C4A4844403800ull >> (8 * m)) & 0xFFu);
-    return (uint8_t)(mag | (d < 0 ? 0x80u : 0u));
+    B4Codes o;
+    o.c = pair_codes9<T>(cv);
+    o.s = pair_codes9<T>(sv);
+    o.sc = n_states == 2 ? (state ? 0xAull : 0x2ull) : (0x2ull << (4 * state));      // -1 / +1; one-hot +1
+    return o;
+}
+// Two oscillators share every byte of the packed image (even index in the low nibble).  `which` selects what this
+// caller stores for the pair (ev = codes of the even oscillator, od = of the odd one): bit 0 the cos planes, bit 1 the
+// sin planes, bit 2 the score planes -- so two lanes can split the bytes of their pair.  kk = index of the EVEN
+// oscillator inside its 256-wide k-block.
+__device__ __forceinline__ void write_b4(uint8_t *Bimg, int NB, int R, int kb4, int kk, int r, const B4Codes &ev, const B4Codes &od,
+                                         int n_states, int which)
+{
+    uint8_t *base = Bimg + (size_t)kb4 * NB * 128;
+    const uint32_t c = (uint32_t)kk >> 1;
+    const int row0 = 2 * UMMA_D9 * r;
+    if (which & 1) {
+#pragma unroll
+        for (int k = 0; k < UMMA_D9; ++k)
+            base[swz(row0 + k, c)] = (uint8_t)(((ev.c >> (4 * k)) & 0xF) | (((od.c >> (4 * k)) & 0xF) << 4));
+    }
+    if (which & 2) {
+#pragma unroll
+        for (int k = 0; k < UMMA_D9; ++k)
+            base[swz(row0 + UMMA_D9 + k, c)] = (uint8_t)(((ev.s >> (4 * k)) & 0xF) | (((od.s >> (4 * k)) & 0xF) << 4));
+    }
+    if (which & 4) {
+        const int srow = 2 * UMMA_D9 * R + (n_states == 2 ? r : r * n_states);
+        const int planes = n_states == 2 ? 1 : n_states;
+        for (int k = 0; k < planes; ++k)
+            base[swz(srow + k, c)] = (uint8_t)(((ev.sc >> (4 * k)) & 0xF) | (((od.sc >> (4 * k)) & 0xF) << 4));
+    }
 }
 
-// write the 8 digit bytes and the spin of oscillator (tile kb, column c) for replica r into one B image
+// int8 stream: write the 8 digit bytes and the spin of oscillator (tile kb, column c) for replica r into one B image
 template <typename T>
-__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state, int n_states, int fp4)
+__device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, int c, int r, T cv, T sv, int state, int n_states)
 {
     uint8_t *base = Bimg + (size_t)kb * NB * 128;
-    const int dcols = fp4 ? 16 : 8;
-    if (fp4) {
-        int dc[8], ds[8];
-        pair_digits16<T>(cv, dc);
-        pair_digits16<T>(sv, ds);
+    int dc[4], ds[4];
+    pair_digits<T>(cv, dc);
+    pair_digits<T>(sv, ds);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            base[swz(16 * r + k, c)] = e4m3_of_small_int(dc[k]);
-            base[swz(16 * r + 8 + k, c)] = e4m3_of_small_int(ds[k]);
-        }
-    } else {
-        int dc[4], ds[4];
-        pair_digits<T>(cv, dc);
-        pair_digits<T>(sv, ds);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            base[swz(8 * r + k, c)] = (uint8_t)dc[k];
-            base[swz(8 * r + 4 + k, c)] = (uint8_t)ds[k];
-        }
+    for (int k = 0; k < 4; ++k) {
+        base[swz(8 * r + k, c)] = (uint8_t)dc[k];
+        base[swz(8 * r + 4 + k, c)] = (uint8_t)ds[k];
     }
-    const uint8_t plus = fp4 ? 0x38 : 0x01, minus = fp4 ? 0xB8 : 0xFF;           // +1 / -1 as e4m3 or int8
     if (n_states == 2) {
-        base[swz(dcols * R + r, c)] = state ? minus : plus;                      // spin plane: sum_j J_ij sigma_j
+        base[swz(8 * R + r, c)] = state ? 0xFF : 0x01;                           // spin plane: sum_j J_ij sigma_j
     } else {
         for (int k = 0; k < n_states; ++k)                                       // one-hot planes: sum_j J_ij [s_j == k]
-            base[swz(dcols * R + r * n_states + k, c)] = k == state ? plus : (uint8_t)0;
+            base[swz(8 * R + r * n_states + k, c)] = k == state ? (uint8_t)1 : (uint8_t)0;
     }
 }
 
@@ -274,19 +310,29 @@ __device__ __forceinline__ void red_release(unsigned int *p, bool sys)
 } // namespace umma
 
 // phases [R][n] float64 (host layout) -> this rank's rows in T, plus the B image of ALL n
-// oscillators for pass 0 (every rank builds the full image locally).
+// oscillators for pass 0 (every rank builds the full image locally).  One thread per PAIR of oscillators
+// (the e2m1 image packs two per byte).
 template <typename T>
 __global__ void k_umma_init(UmmaArgs a, const double *__restrict__ phi0)
 {
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q >= (long long)a.n * a.R) return;
-    const int r = (int)(q / a.n), j = (int)(q % a.n);
-    const T p = (T)phi0[q];
-    T s, c;
-    phase_trig(p, s, c);
-    umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, threshold_state((double)p, a.n_states), a.n_states, a.fp4);
+    const int half = (a.n + 1) / 2;
+    if (q >= (long long)half * a.R) return;
+    const int r = (int)(q / half), j0 = 2 * (int)(q % half);
     const int row0 = a.tile_begin * UMMA_TILE, row1 = a.tile_end * UMMA_TILE;
-    if (j >= row0 && j < row1) reinterpret_cast<T *>(a.phi[0])[(long long)r * a.ld_phi + (j - row0)] = p;
+    umma::B4Codes cd[2] = {{0, 0, 0}, {0, 0, 0}};
+    for (int e = 0; e < 2; ++e) {
+        const int j = j0 + e;
+        if (j >= a.n) break;
+        const T p = (T)phi0[(long long)r * a.n + j];
+        T s, c;
+        phase_trig(p, s, c);
+        const int st = threshold_state((double)p, a.n_states);
+        if (a.fp4) cd[e] = umma::make_b4<T>(c, s, st, a.n_states);
+        else umma::write_b<T>(a.B_img[0][a.rank], a.NB, a.R, j / UMMA_TILE, j % UMMA_TILE, r, c, s, st, a.n_states);
+        if (j >= row0 && j < row1) reinterpret_cast<T *>(a.phi[0])[(long long)r * a.ld_phi + (j - row0)] = p;
+    }
+    if (a.fp4) umma::write_b4(a.B_img[0][a.rank], a.NB, a.R, j0 / UMMA_K4, j0 % UMMA_K4, r, cd[0], cd[1], a.n_states, 7);
 }
 
 // this rank's rows as float64: out[r * ld_out + col0 + i] (col0 = first row and ld_out = n for
@@ -326,32 +372,30 @@ __global__ void k_umma_build_a(const int8_t *__restrict__ J, int n, int n_pad, i
     }
 }
 
-// int8 J rows with every coupling in {0, +-1, +-2, +-3, +-4, +-6} -> packed e2m1 tiles in plain row-major form (the TMA
-// unit swizzles and unpacks): tile (lt, kb) is 128 consecutive rows of 64 bytes, byte b of a row holds column 2b in its
-// low nibble and column 2b + 1 in its high nibble.
-__global__ void k_umma_build_fp4(const int8_t *__restrict__ J, int n, int n_pad, int rows, int tiles,
-                                 uint8_t *__restrict__ A_fp4)
+// int8 J rows with every coupling in {0, +-1, +-2, +-3, +-4, +-6} -> swizzled tile images of packed e2m1 codes: tile
+// (lt, kb) covers 128 rows x 256 columns; byte c of a row holds column 2c in its low nibble and 2c + 1 in its high nibble.
+__global__ void k_umma_build_fp4(const int8_t *__restrict__ J, int n, int n_pad, int rows, int ktiles, uint8_t *__restrict__ A_fp4)
 {
     const int lt = blockIdx.y, kb = blockIdx.x;
-    uint8_t *img = A_fp4 + ((size_t)lt * tiles + kb) * UMMA_RAW_STAGE;
-    for (int t = threadIdx.x; t < UMMA_RAW_STAGE; t += blockDim.x) {
-        const int r = t >> 6, b = t & 63;
+    uint8_t *img = A_fp4 + ((size_t)lt * ktiles + kb) * UMMA_A_STAGE;
+    for (int t = threadIdx.x; t < UMMA_A_STAGE; t += blockDim.x) {
+        const int r = t >> 7, c = t & 127;
         const int row = lt * UMMA_TILE + r;
         uint32_t code[2] = {0, 0};
         for (int h = 0; h < 2; ++h) {
-            const int col = kb * UMMA_TILE + 2 * b + h;
+            const int col = kb * UMMA_K4 + 2 * c + h;
             int v = 0;
             if (row < rows && col < n) v = J[(size_t)row * n_pad + col];
             const int m = v < 0 ? -v : v;
             const uint32_t mag = m == 0 ? 0u : m == 1 ? 2u : m == 2 ? 4u : m == 3 ? 5u : m == 4 ? 6u : 7u;   // 6 -> 7
             code[h] = mag | (v < 0 ? 8u : 0u);
         }
-        img[t] = (uint8_t)(code[0] | (code[1] << 4));   // low nibble first: the order the TMA unpack keeps
+        img[umma::swz((uint32_t)r, (uint32_t)c)] = (uint8_t)(code[0] | (code[1] << 4));
     }
 }
 
 template <typename T, bool FP4>
-__global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a, const __grid_constant__ CUtensorMap tmap_a4)
+__global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a)
 {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = umma::smem_u32(smem_raw);
@@ -373,9 +417,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool sys = a.world > 1;
     const int my_tiles = (a.tile_end - a.tile_begin - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const long long per_pass = (long long)my_tiles * a.tiles;
-    // transaction bytes of a stage: the TMA unit counts the PACKED bytes it fetched for the e2m1 tile (8 KB), not the 16 KB it writes
-    const uint32_t stage_tx = (FP4 ? (uint32_t)UMMA_RAW_STAGE : (uint32_t)UMMA_A_STAGE) + b_stage;
+    const long long per_pass = (long long)my_tiles * a.ktiles;
+    const uint32_t stage_tx = (uint32_t)UMMA_A_STAGE + b_stage;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < stages; ++s) {
@@ -398,7 +441,20 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     umma::tc_fence_before();
     __syncthreads();
     umma::tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem_sf = *tmem_slot;
+    const uint32_t tmem = tmem_sf + (FP4 ? (uint32_t)UMMA_SF_COLS : 0u);          // the accumulator
+    if (FP4) {
+        // block scales of the mxf4 MMA: every ue8m0 byte = 127 (2^0), so their layout inside the columns does not matter
+        if (warp >= 2 && warp < 6) {
+            const uint32_t t = tmem_sf + ((uint32_t)((warp & 3) * 32) << 16);
+            umma::tmem_fill16(t, 0x7F7F7F7Fu);
+            umma::tmem_fill16(t + 16u, 0x7F7F7F7Fu);
+            umma::tmem_st_wait();
+        }
+        umma::tc_fence_before();
+        __syncthreads();
+        umma::tc_fence_after();
+    }
 
     if (warp == 0) {
         // ===== producer =====  (one thread; no divisions on this path: it paces the whole CTA)
@@ -409,17 +465,15 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             Cursor ca{0, 0, 0, 0}, cb{0, 0, 0, 0};
             auto advance = [&](Cursor &c) {
                 if (++c.s == stages) { c.s = 0; c.ph ^= 1u; }
-                if (++c.kb == a.tiles) { c.kb = 0; if (++c.tk == my_tiles) c.tk = 0; }
+                if (++c.kb == a.ktiles) { c.kb = 0; if (++c.tk == my_tiles) c.tk = 0; }
             };
             auto issue_a = [&](Cursor &c) {
                 umma::mbar_wait(bar_empty + 8u * c.s, c.ph ^ 1u);
                 umma::mbar_expect_tx(bar_full + 8u * c.s, stage_tx);
                 const int lt = (int)blockIdx.x + c.tk * (int)gridDim.x;
-                if (FP4)      // packed e2m1 rows (64 B each) -> 16 codes per 16-byte slot, 128-byte swizzled: the TMA unit unpacks
-                    umma::tma_load_2d(sA + (uint32_t)c.s * UMMA_A_STAGE, &tmap_a4, 0, (lt * a.tiles + c.kb) * UMMA_TILE, bar_full + 8u * c.s);
-                else
-                    umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, a.A_img + ((size_t)lt * a.tiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
-                                   bar_full + 8u * c.s);
+                const uint8_t *img = FP4 ? a.A_fp4 : a.A_img;
+                umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, img + ((size_t)lt * a.ktiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
+                               bar_full + 8u * c.s);
                 advance(c);
             };
             auto issue_b = [&](Cursor &c, const uint8_t *Bsrc) {
@@ -450,7 +504,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            const uint32_t idesc = FP4 ? umma::instr_desc_fp4(a.NB) : umma::instr_desc_i8(a.NB);
+            const uint32_t idesc = FP4 ? umma::instr_desc_mxf4(a.NB) : umma::instr_desc_i8(a.NB);
+            const uint32_t sfa = tmem_sf, sfb = tmem_sf + (uint32_t)(UMMA_SF_COLS / 2);
             long long acc_it = 0;
             int s = 0;
             uint32_t ph = 0;
@@ -458,14 +513,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 for (int tk = 0; tk < my_tiles; ++tk) {
                     umma::mbar_wait(bar_tempty, (uint32_t)((acc_it & 1) ^ 1));
                     umma::tc_fence_after();
-                    for (int kb = 0; kb < a.tiles; ++kb) {
+                    for (int kb = 0; kb < a.ktiles; ++kb) {
                         umma::mbar_wait(bar_full + 8u * s, ph);
                         umma::tc_fence_after();
                         const uint64_t ad = umma::smem_desc(sA + (uint32_t)s * UMMA_A_STAGE);
                         const uint64_t bd = umma::smem_desc(sB + (uint32_t)s * b_stage);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            if (FP4) umma::mma_f8f6f4(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
+                            if (FP4) umma::mma_mxf4(tmem, ad + 2u * k, bd + 2u * k, idesc, sfa, sfb, (uint32_t)((kb | k) != 0));
                             else umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
                         }
                         umma::tc_commit(bar_empty + 8u * s);
@@ -545,10 +600,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 for (int k = 0; k < UMMA_RPG; ++k) {
                     const int r = group + 4 * k;
                     if (r >= R) break;                       // warp uniform
-                    int D[16], Dsig = 0;
+                    int D[2 * UMMA_D9], Dsig = 0;
                     const int dcols = a.dcols;
-                    if (FP4) umma::tmem_ld16(tlane + (uint32_t)(16 * r), D);
-                    else umma::tmem_ld8(tlane + (uint32_t)(8 * r), reinterpret_cast<int (&)[8]>(D));
+                    if (FP4) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 2 * UMMA_D9; q4 += 4) umma::tmem_ld4(tlane + (uint32_t)(2 * UMMA_D9 * r + q4), D + q4);
+                    } else {
+                        umma::tmem_ld8(tlane + (uint32_t)(8 * r), reinterpret_cast<int (&)[8]>(D));
+                    }
                     const T p = pre_p[k], si = pre_s[k], ci = pre_c[k];
                     const int st = (flags & 1) ? threshold_state((double)p, a.n_states) : 0;
                     if (flags & 1) {
@@ -567,13 +626,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     umma::tmem_ld_wait();
 
                     if (FP4) {
-                        // the f8f6f4 accumulator is float32 holding exact integers (|sum| < 2^24): back to int
+                        // the mxf4 accumulator is float32 holding exact integers (|sum| < 2^24): back to int
 #pragma unroll
-                        for (int q4 = 0; q4 < 16; ++q4) D[q4] = __float2int_rn(__int_as_float(D[q4]));
+                        for (int q4 = 0; q4 < 2 * UMMA_D9; ++q4) D[q4] = __float2int_rn(__int_as_float(D[q4]));
                         Dsig = __float2int_rn(__int_as_float(Dsig));
                     }
-                    const long long Sx = FP4 ? umma::digits_sum16(D) : umma::digits_sum(D);
-                    const long long Sy = FP4 ? umma::digits_sum16(D + 8) : umma::digits_sum(D + 4);
+                    const long long Sx = FP4 ? umma::digits_sum9(D) : umma::digits_sum(D);
+                    const long long Sy = FP4 ? umma::digits_sum9(D + UMMA_D9) : umma::digits_sum(D + 4);
                     const long long at = (long long)r * a.ld_phi + rowl;
                     if (prev_scored && improved_s[r] && valid)
                         a.best_states[at] = (uint8_t)threshold_state((double)phi_out[at], a.n_states);   // phi_out still holds the scored phases
@@ -595,6 +654,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         for (int off = 16; off > 0; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
                         if (lane == 0) en_w[quad * 32 + r] = e;
                     }
+                    umma::B4Codes mine = {0, 0, 0};
                     if (!last && valid) {
                         const T scale = (T)9.313225746154785e-10;
                         const T accv = si * ((T)Sx * scale) - ci * ((T)Sy * scale);
@@ -606,8 +666,27 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         T s2, c2;
                         phase_trig(y, s2, c2);
                         const int st2 = threshold_state((double)y, a.n_states);
-                        for (int w = 0; w < a.world; ++w)
-                            umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2, a.n_states, FP4);
+                        if (FP4) {
+                            mine = umma::make_b4<T>(c2, s2, st2, a.n_states);
+                        } else {
+                            for (int w = 0; w < a.world; ++w)
+                                umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2, a.n_states);
+                        }
+                    }
+                    if (FP4 && !last) {
+                        // two oscillators per byte: lanes 2i and 2i + 1 swap codes, the even lane stores the pair's cos and
+                        // score planes, the odd lane its sin planes (rows past n carry zero codes)
+                        umma::B4Codes other;
+                        other.c = __shfl_xor_sync(0xffffffffu, mine.c, 1);
+                        other.s = __shfl_xor_sync(0xffffffffu, mine.s, 1);
+                        other.sc = __shfl_xor_sync(0xffffffffu, mine.sc, 1);
+                        const bool odd = lane & 1;
+                        if (row - (int)odd < a.n) {
+                            const int kk = (tile & 1) * UMMA_TILE + (rowt & ~1);
+                            for (int w = 0; w < a.world; ++w)
+                                umma::write_b4(a.B_img[(pass + 1) & 1][w], a.NB, R, tile >> 1, kk, r, odd ? other : mine, odd ? mine : other,
+                                               a.n_states, odd ? 2 : 5);
+                        }
                     }
                 }
                 umma::tc_fence_before();
@@ -660,7 +739,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
     }
     umma::tc_fence_before();
     __syncthreads();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(a.tmem_cols) : "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_sf), "r"(a.tmem_cols) : "memory");
 }
 
 } // namespace oscb

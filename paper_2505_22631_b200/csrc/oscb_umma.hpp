@@ -23,9 +23,9 @@ std::shared_ptr<UmmaPlan> umma_build_plan(const int8_t *J8_dev, int64_t n, int n
 constexpr int kUmmaMaxReplicas = 28;      // N = 2: 9 B rows per replica; use umma_max_replicas(N) in general
 inline int umma_max_replicas(int n_states, bool fp4 = false)
 {
-    return std::min(kUmmaMaxReplicas, 256 / ((fp4 ? 16 : 8) + (n_states == 2 ? 1 : n_states)));
+    return std::min(kUmmaMaxReplicas, 256 / ((fp4 ? 20 : 8) + (n_states == 2 ? 1 : n_states)));
 }
-bool umma_uses_fp4(const UmmaPlan &plan, int R);   // the packed e2m1 stream for a call of R replicas in all (see oscb_umma.cu)
+bool umma_uses_fp4(const UmmaPlan &plan, int R, int n_states);   // the packed e2m1 stream for a call of R replicas in all (see oscb_umma.cu)
 constexpr int kUmmaMaxWorld = 8;
 
 // what one rank of a row-sharded run publishes about its exchange block (the memory its peers

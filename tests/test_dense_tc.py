@@ -196,9 +196,9 @@ def test_best_objective_distribution_matches_reference_oracle(pkg, oracle, kind,
 
 
 def test_fp4_stream_equals_int8_stream(pkg):
-    """Couplings in {0, +-1, +-2, +-3, +-4, +-6} can stream as packed e2m1 codes (half the bytes; the TMA unit unpacks
-    them into the 16-byte-slot form) and be multiplied on the f8f6f4 tensor path against e4m3 base-16 digit planes,
-    float32 accumulators holding exact integers (the default for up to 8 replicas per call).  The
+    """Couplings in {0, +-1, +-2, +-3, +-4, +-6} can stream as packed e2m1 codes (half the bytes) and be multiplied on the
+    block-scaled 4-bit tensor path (kind::mxf4, all scales 1.0) against e2m1 balanced base-9 digit planes, float32
+    accumulators holding exact integers (the default for up to 12 replicas per call).  The
     reassembled sums are the same integers as on the int8 path, so the two modes must agree bit for bit (noise on,
     ragged n, several tiles per CTA, zeros and weights up to 6 included)."""
     for n, cap, weights in ((256, None, (-1.0, 1.0)), (300, None, (-6.0, -3.0, -1.0, 0.0, 0.0, 1.0, 2.0, 4.0)), (640, "2", (-1.0, 1.0))):
@@ -210,7 +210,7 @@ def test_fp4_stream_equals_int8_stream(pkg):
             os.environ["OSCB_UMMA_MAX_GRID"] = cap
         try:
             runs = {}
-            for mode in ("0", "1"):                    # 0: int8 stream, 1: packed e2m1 stream through the TMA unpack path
+            for mode in ("0", "1"):                    # 0: int8 stream, 1: packed e2m1 stream
                 os.environ["OSCB_UMMA_FP4"] = mode
                 try:
                     runs[mode] = pkg.run_batch(Jd, params, "maxcut", seeds, precision="f32", kernel="dense-tc")
