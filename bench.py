@@ -108,6 +108,12 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def samples(self):
+        try:
+            return sum(1 for line in open(self.path) if line.count(",") >= 6)
+        except Exception:
+            return 0
+
     def stop(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         if self.proc is None:
@@ -282,6 +288,12 @@ def bench_dense(args, rank, world, local_rank):
             dev_ms += last.device_ms
             launches += last.kernel_launches
         torch.cuda.synchronize()
+        # a dense window is tens of milliseconds, nvidia-smi needs a few hundred to deliver its first sample: keep the
+        # same kernel running (untimed) until the sampler has seen the load
+        t_s = time.perf_counter()
+        while sampler.proc is not None and sampler.samples() < 3 and time.perf_counter() - t_s < 5.0:
+            device_step()
+            torch.cuda.synchronize()
         clocks = sampler.stop()
         phi0_pinned = torch.empty((R, n), dtype=torch.float64, pin_memory=True)
         phi0 = phi0_pinned.numpy()
