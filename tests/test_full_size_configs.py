@@ -3,6 +3,8 @@ properties (the oracle cannot run these sizes in seconds): phase containment, be
 objective recomputed on the host from the best states (the reference recomputes it the same way,
 dynamics.py:416-421), monotone best trace, kernels agreeing with each other.  configs[1] at full
 size is in test_gpu_parity.py::test_full_size_g22_properties."""
+import os
+
 import numpy as np
 import pytest
 
@@ -90,6 +92,15 @@ def test_sk_16384_dense_tensor_core(pkg):
             total = float(J8.sum(dtype=np.int64)) / 2.0
             assert (total - quad) / 2.0 == b.best_objective[r]
         assert np.all(np.diff(b.best_trace, axis=1) >= 0)
+        # the call above streamed J as packed e2m1 tiles (<= 12 replicas); the int8 stream must give the same bits
+        os.environ["OSCB_UMMA_FP4"] = "0"
+        try:
+            b8 = dyn.run_batch(None, params, "maxcut", seeds, steps=60, graph=g)
+        finally:
+            os.environ.pop("OSCB_UMMA_FP4", None)
+        assert g.tc_stream(2, len(seeds)) == (4, 12)
+        assert np.array_equal(b8.final_phases, b.final_phases) and np.array_equal(b8.best_states, b.best_states)
+        assert np.array_equal(b8.best_objective, b.best_objective) and np.array_equal(b8.energy, b.energy)
         # (K = 1 on 16384 all-to-all couplings moves a phase by ~1 turn per step -- any two float32
         # evaluations decorrelate within a few steps; the comparison runs in the contractive regime)
         mild = pkg.SolverParams.tuned_for(n, 2, seed=0, K=0.02)
