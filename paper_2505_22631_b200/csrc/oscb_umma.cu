@@ -254,7 +254,7 @@ void UmmaSession::prepare(const uint64_t *seeds, const double *d_phi0)
     OSCB_CUDA(cudaMemcpyAsync(m->g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
     if (const char *trace_path = getenv("OSCB_UMMA_TRACE")) {     // debug: per-CTA timeline of the first passes
         (void)trace_path;
-        m->d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * 4);
+        m->d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * UMMA_TRACE_SLOTS);
         m->d_trace.zero(s);
         a.trace = m->d_trace.p;
     }
@@ -328,14 +328,14 @@ void UmmaSession::finish(double *h_final_rows, uint8_t *h_best_rows, long long *
             }
     if (const char *trace_path = getenv("OSCB_UMMA_TRACE")) {
         if (m->d_trace.p) {
-            std::vector<long long> h((size_t)grid * UMMA_TRACE_PASSES * 4);
+            std::vector<long long> h((size_t)grid * UMMA_TRACE_PASSES * UMMA_TRACE_SLOTS);
             OSCB_CUDA(cudaMemcpy(h.data(), m->d_trace.p, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
             if (FILE *f = fopen(trace_path, "w")) {
-                fprintf(f, "cta,pass,barrier_seen,tmem_full,arrived,barrier_wait_begin\n");
+                fprintf(f, "cta,pass,barrier_seen,tmem_full,arrived,barrier_wait_begin,tmem_loaded,updated,stored,cta_synced\n");
                 for (int c = 0; c < grid; ++c)
                     for (int q = 0; q < UMMA_TRACE_PASSES && q < a.passes; ++q) {
-                        const long long *t = &h[((size_t)c * UMMA_TRACE_PASSES + q) * 4];
-                        fprintf(f, "%d,%d,%lld,%lld,%lld,%lld\n", c, q, t[0], t[1], t[2], t[3]);
+                        const long long *t = &h[((size_t)c * UMMA_TRACE_PASSES + q) * UMMA_TRACE_SLOTS];
+                        fprintf(f, "%d,%d,%lld,%lld,%lld,%lld,%lld,%lld,%lld,%lld\n", c, q, t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7]);
                     }
                 fclose(f);
             }

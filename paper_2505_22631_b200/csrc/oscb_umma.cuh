@@ -52,6 +52,7 @@ constexpr int UMMA_THREADS = 64 + UMMA_EPI_THREADS;
 constexpr int UMMA_MAXR = 28;         // 9 B rows per replica, N <= 256
 constexpr int UMMA_RPG = UMMA_MAXR / 4; // replicas per epilogue group
 constexpr int UMMA_TRACE_PASSES = 64;
+constexpr int UMMA_TRACE_SLOTS = 8;
 
 struct UmmaArgs {
     int n;                    // oscillators
@@ -488,9 +489,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 if (pass > 0) {
                     for (int j = 0; j < pre; ++j) issue_a(ca);                  // J does not depend on the step: run ahead
                     const unsigned int target = a.ctas_total * (unsigned int)pass;
-                    if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 3] = clock64();
+                    if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 3] = clock64();
                     while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
-                    if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 0] = clock64();
+                    if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 0] = clock64();
                     umma::fence_proxy_async();
                     for (int j = 0; j < pre; ++j) issue_b(cb, Bsrc);
                     start = pre;
@@ -584,7 +585,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 }
                 umma::mbar_wait(bar_tfull, (uint32_t)(acc_it & 1));
                 umma::tc_fence_after();
-                if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 1] = clock64();
+                if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 1] = clock64();
                 if (!checked) {
                     // the grid barrier of the previous pass is behind us: its cut totals are complete
                     if (prev_scored && et < R) {
@@ -624,6 +625,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         }
                     }
                     umma::tmem_ld_wait();
+                    if (a.trace && et == 0 && k == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 4] = clock64();
 
                     if (FP4) {
                         // the mxf4 accumulator is float32 holding exact integers (|sum| < 2^24): back to int
@@ -673,6 +675,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                                 umma::write_b<T>(a.B_img[(pass + 1) & 1][w], a.NB, R, tile, rowt, r, c2, s2, st2, a.n_states);
                         }
                     }
+                    if (a.trace && et == 0 && k == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 5] = clock64();
                     if (FP4 && !last) {
                         // two oscillators per byte: lanes 2i and 2i + 1 swap codes, the even lane stores the pair's cos and
                         // score planes, the odd lane its sin planes (rows past n carry zero codes)
@@ -689,6 +692,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         }
                     }
                 }
+                if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 6] = clock64();
                 umma::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) umma::mbar_arrive(bar_tempty);
@@ -709,9 +713,11 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             umma::fence_proxy_async();
             umma::named_bar_sync(1, UMMA_EPI_THREADS);
             if (et == 0) {
-                if (sys) __threadfence_system(); else __threadfence();       // cumulative over the CTA barrier above
+                if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 7] = clock64();
+                // red.release is the fence: it is cumulative over the CTA barrier above, so every epilogue thread's stores and
+                // atomics of this pass are visible (gpu / system scope) to whoever acquires the counter
                 for (int w = 0; w < a.world; ++w) umma::red_release(a.bar[w], sys);
-                if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * 4 + 2] = clock64();
+                if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 2] = clock64();
             }
             if (flags & 1) ++e_idx;
             if (flags & 2) ++s_idx;
