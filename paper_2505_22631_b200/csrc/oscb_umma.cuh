@@ -208,21 +208,21 @@ __device__ __forceinline__ long long digits_sum(const int *D)
 
 // e2m1 stream: round(c 2^30) as ten balanced base-9 digits (d0 least significant, |d| <= 4: every digit is an e2m1 value),
 // returned as ten 4-bit e2m1 codes, digit k in bits [4k, 4k + 4)
-__device__ __forceinline__ uint32_t e2m1_of_small_int(int d)      // |d| <= 4:  0, 1, 2, 3, 4 -> codes 0, 2, 4, 5, 6; sign in bit 3
-{
-    const int m = d < 0 ? -d : d;
-    return ((0x65420u >> (4 * m)) & 0xFu) | (d < 0 ? 8u : 0u);
-}
 template <typename T> __device__ __forceinline__ uint64_t pair_codes9(T v)
 {
-    int q = (sizeof(T) == 8) ? __double2int_rn((double)v * 1073741824.0) : __float2int_rn((float)v * 1073741824.0f);
+    const int q = (sizeof(T) == 8) ? __double2int_rn((double)v * 1073741824.0) : __float2int_rn((float)v * 1073741824.0f);
+    // balanced digits d_k in [-4, 4]  <=>  plain base-9 digits e_k = d_k + 4 of u = q + sum_k 4 * 9^k = q + (9^10 - 1) / 2,
+    // and u fits 32 bits (|q| <= 2^30 < (9^10 - 1) / 2 < 2^32 - 2^30): unsigned divisions by 9, no sign cases
+    uint32_t u = (uint32_t)q + 1743392200u;
+    // e2m1 codes of d = e - 4 for e = 0 .. 8:  -4 -> 0xE, -3 -> 0xD, -2 -> 0xC, -1 -> 0xA, 0 -> 0x0, 1 -> 0x2, 2 -> 0x4, 3 -> 0x5, 4 -> 0x6
+    const uint64_t table = 0x65420ACDEull;
     uint64_t codes = 0;
 #pragma unroll
     for (int k = 0; k < UMMA_D9; ++k) {
-        int lo = q % 9;                      // sign of q
-        lo = lo > 4 ? lo - 9 : (lo < -4 ? lo + 9 : lo);
-        codes |= (uint64_t)e2m1_of_small_int(lo) << (4 * k);
-        q = (q - lo) / 9;
+        const uint32_t t = __umulhi(u, 0x38E38E39u) >> 1;         // u / 9
+        const uint32_t e = u - 9u * t;
+        codes |= ((table >> (4u * e)) & 0xFull) << (4 * k);
+        u = t;
     }
     return codes;
 }
