@@ -17,6 +17,7 @@
 #include <type_traits>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -626,11 +627,19 @@ static void run_umma(oscb_graph *g, const oscb_run_params *p, const RunPlan &rp,
         std::vector<double> en((size_t)S * Rc);
         UmmaSpec spc = umma_spec(p, rp, sc, Rc);
         spc.R_total = R;
+        const bool timing = getenv("OSCB_UMMA_TIMING") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto since = [&](std::chrono::steady_clock::time_point t0) { return std::chrono::duration<double, std::milli>(now() - t0).count(); };
+        auto t0 = now();
         UmmaSession ses(g, spc, 1, 0);
+        const double t_ctor = since(t0); t0 = now();
         ses.prepare(seeds + r0, io.p + (size_t)r0 * n);
+        const double t_prep = since(t0); t0 = now();
         ses.launch();
         ses.export_final(d_final.p + (size_t)r0 * n);
+        const double t_launch = since(t0); t0 = now();
         ses.finish(nullptr, out->best_states ? out->best_states + (size_t)r0 * n : nullptr, ev.data(), en.data());
+        if (timing) fprintf(stderr, "[umma] ctor %.2f prepare %.2f launch %.2f finish %.2f (kernel %.2f) ms\n", t_ctor, t_prep, t_launch, since(t0), ses.ms);
         ms += ses.ms;
         launches += 1;
         smem = (int64_t)ses.smem;
