@@ -223,3 +223,25 @@ def test_fp4_stream_equals_int8_stream(pkg):
         assert np.array_equal(fp4.best_states, int8.best_states)
         assert np.array_equal(fp4.best_objective, int8.best_objective)
         assert np.array_equal(fp4.energy, int8.energy)
+
+
+def test_stream_choice_reported_by_the_abi(pkg):
+    """oscb_dense_tc_stream: packed e2m1 tiles when every coupling is an e2m1 value and the call fits one launch of that
+    stream (21 B columns per replica at N = 2 -> 12 replicas; 20 + N columns at N states), int8 tiles otherwise."""
+    from paper_2505_22631_b200 import dynamics
+    g = dynamics.DeviceGraph.from_dense(0, sk_graph(256, 1))
+    try:
+        assert g.tc_stream(2, 1) == (4, 12) and g.tc_stream(2, 12) == (4, 12)
+        assert g.tc_stream(2, 13) == (8, 28) and g.tc_stream(2, 1000) == (8, 28)
+        assert g.tc_stream(3, 11) == (4, 11) and g.tc_stream(3, 12) == (8, 23)
+    finally:
+        g.close()
+    g5 = dynamics.DeviceGraph.from_dense(0, sk_graph(256, 2, (-5.0, 1.0)))       # 5 is not an e2m1 value
+    try:
+        assert g5.tc_stream(2, 1) == (8, 28)
+    finally:
+        g5.close()
+    sparse = pkg.CouplingMatrix.from_dense(sk_graph(64, 3), storage="sparse")
+    gs = dynamics.device_graph(sparse, 0)
+    with pytest.raises(ValueError):
+        gs.tc_stream(2, 1)
