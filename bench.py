@@ -336,7 +336,8 @@ def bench_dense(args, rank, world, local_rank):
             "data": "synthetic",
             "config": {"workload": label, "replicas": R, "window": window, "kernel": last.kernel, "coupling_bits": bits,
                        "replicas_per_launch": last.replicas_per_cta, "smem_bytes": last.smem_bytes, "parallelism": "one GPU",
-                       "l2": "J (n^2 bytes = %.0f MB) exceeds the 126 MB L2 and is re-read from HBM every Euler step; no flush needed" % (n * n / 1e6)},
+                       "l2": "J (%.0f MB at %d bits per coupling) exceeds the 126 MB L2 and is re-read from HBM every Euler step "
+                             "(ncu: DRAM bytes per step = the image size); no flush needed" % (n * n * bits / 8e6, bits)},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
             "gpu_launches": int(launches),
             "clocks": {"sm_mhz": clocks["sm_mhz"], "sm_max_mhz": clocks["sm_max_mhz"], "reasons": clocks["reasons"]},
