@@ -1,13 +1,13 @@
 // oscb_cluster.cuh -- latency mode of the float32 integrator: ONE replica spread over a thread-block
-// cluster of 8 SMs (the reference's default `solve` is a single replica, cli.py:143-153; at
+// cluster of 8 or 16 SMs (the reference's default `solve` is a single replica, cli.py:143-153; at
 // R = 1 the persistent kernel of oscb_resident_fast.cuh keeps a whole run on one SM).
 //
 //   * every CTA of the cluster holds a full copy of the (cos, sin) pairs of all n oscillators in
-//     shared memory, double buffered, and owns n / 8 rows of J (their CSR slice sits in its
+//     shared memory, double buffered, and owns n / CL rows of J (CL = cluster size) (their CSR slice sits in its
 //     shared memory too);
 //   * phase A of a step: a row is gathered by 8 lanes (neighbours strided over the lanes, 3 shuffle
 //     stages); phase B: one thread per row does the Euler update (SHIL, noise, wrap;
-//     dynamics.py:166-172) and stores the new pair straight into the NEXT buffer of all 8 CTAs
+//     dynamics.py:166-172) and stores the new pair straight into the NEXT buffer of all CL CTAs
 //     through distributed shared memory, while the remaining warps draw the next step's Philox
 //     noise (it does not depend on the sums, so it stays off the critical path);
 //   * one cluster barrier (arrive.release / wait.acquire) ends the step; nothing leaves the SMs.
@@ -26,7 +26,7 @@ namespace oscb {
 
 namespace cg = cooperative_groups;
 
-constexpr int CL_SIZE = 8;   // CTAs per cluster (portable maximum)
+constexpr int CL_MAX = 16;    // CTAs per cluster: 8 (portable maximum) or 16 (non-portable size, taken while 16 SMs per replica are free)
 constexpr int CL_LPR = 8;    // lanes per row
 
 struct ClusterArgs {
@@ -66,7 +66,7 @@ struct ClusterSmem {
         s.kick = take((size_t)2 * 4 * ((rows_per_cta + 3) / 4) * 4);
         s.col = take((size_t)nnz_cap * 2);
         s.w = take(weighted ? (size_t)nnz_cap * 4 : 0);
-        s.xpart = take((size_t)4 * 2 * CL_SIZE * 8);
+        s.xpart = take((size_t)4 * 2 * CL_MAX * 8);
         s.red = take((size_t)32 * 2 * 8);
         s.misc = take(64);
         s.total = o;
@@ -74,6 +74,7 @@ struct ClusterSmem {
     }
 };
 
+template <int CL_SIZE>
 __global__ void __cluster_dims__(CL_SIZE, 1, 1) __launch_bounds__(1024, 1) k_cluster_fast(const ClusterArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];

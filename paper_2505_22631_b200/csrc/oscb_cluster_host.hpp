@@ -20,7 +20,7 @@ struct ClusterShape {
     ClusterSmem lay;
 };
 
-static bool cluster_shape(const oscb_graph *g, ClusterShape *sh)
+static bool cluster_shape(const oscb_graph *g, int CL_SIZE, ClusterShape *sh)
 {
     if (g->is_dense || g->n < 64 || g->n > 65535) return false;
     const int n = (int)g->n;
@@ -45,7 +45,7 @@ static bool cluster_shape(const oscb_graph *g, ClusterShape *sh)
 // spans two 4-byte banks, so the instruction needs at least 2 wavefronts and one more for every extra hit
 // on a bank pair (column mod 16).  The order inside a row is free in float32 mode, so each instruction's 32
 // columns are picked greedily from the rows' remaining neighbours to spread over the 16 bank pairs.
-static void cluster_order_columns(const oscb_graph *g, int rows_per_cta, std::vector<int> *cols, std::vector<float> *wts)
+static void cluster_order_columns(const oscb_graph *g, int CL_SIZE, int rows_per_cta, std::vector<int> *cols, std::vector<float> *wts)
 {
     const int n = (int)g->n;
     cols->assign(g->h_indices.begin(), g->h_indices.end());
@@ -92,7 +92,7 @@ static bool cluster_applies(const oscb_graph *g, const oscb_run_params *p, int64
     if (p->precision != OSCB_PREC_F32 || p->noise_mode == OSCB_NOISE_HOST || p->variant == 1) return false;
     if (p->n_states != 2 || p->objective != OSCB_OBJ_MAXCUT) return false;
     ClusterShape sh;
-    if (!cluster_shape(g, &sh)) return false;
+    if (!cluster_shape(g, 8, &sh)) return false;
     if (sh.weighted) {
         // the piggybacked cut sums couplings in float32: exact only for small integers
         if (!g->int_weights) return false;
@@ -105,7 +105,7 @@ static bool cluster_applies(const oscb_graph *g, const oscb_run_params *p, int64
         if (worst * (double)g->n >= 16777216.0) return false;
     }
     // latency mode pays off while every replica's cluster has SMs of its own
-    return forced || R * CL_SIZE <= g->sm_count;
+    return forced || R * 8 <= g->sm_count;
 }
 
 static void run_cluster(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t cadence,
@@ -114,8 +114,35 @@ static void run_cluster(oscb_graph *g, const oscb_run_params *p, int64_t steps, 
 {
     cudaStream_t s = g->stream;
     const int n = (int)g->n, R = (int)R64;
+    // 16 CTAs per replica while at most half of the SMs are taken (R <= 4 on 148 SMs: 2.07 vs 2.26 us per step of G1; from
+    // 8 replicas on, the 16-CTA clusters are slower, 50.6 vs 45.2 ms per 20 000 steps), else the portable 8.
+    // OSCB_CLUSTER_SIZE = 8 / 16 forces.
+    int CL_SIZE = R * 32 <= g->sm_count ? 16 : 8;
+    if (const char *env = getenv("OSCB_CLUSTER_SIZE")) CL_SIZE = atoi(env) == 16 ? 16 : 8;
     ClusterShape sh;
-    OSCB_REQUIRE(cluster_shape(g, &sh), "the cluster kernel cannot hold this problem (n = %lld)", (long long)g->n);
+    if (CL_SIZE == 16) {
+        // a 16-CTA cluster has to fit one GPC: take it only if all R clusters can be resident at once
+        int resident = 0;
+        if (cluster_shape(g, 16, &sh)) {
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)(R * 16));
+            cfg.blockDim = dim3((unsigned)sh.threads);
+            cfg.dynamicSmemBytes = sh.lay.total;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 16; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            const void *f16 = (const void *)k_cluster_fast<16>;
+            if (cudaFuncSetAttribute(f16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.lay.total) != cudaSuccess ||
+                cudaFuncSetAttribute(f16, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess ||
+                cudaOccupancyMaxActiveClusters(&resident, f16, &cfg) != cudaSuccess)
+                resident = 0;
+            cudaGetLastError();
+        }
+        if (resident < R) CL_SIZE = 8;
+    }
+    OSCB_REQUIRE(cluster_shape(g, CL_SIZE, &sh), "the cluster kernel cannot hold this problem (n = %lld)", (long long)g->n);
     const int64_t S = 1 + (int64_t)sample_steps.size();
     const size_t tot = (size_t)n * R;
 
@@ -158,7 +185,7 @@ static void run_cluster(oscb_graph *g, const oscb_run_params *p, int64_t steps, 
     a.off_misc = (uint32_t)sh.lay.misc; a.smem_total = (uint32_t)sh.lay.total;
     std::vector<int> h_cols;
     std::vector<float> h_wts;
-    cluster_order_columns(g, sh.rows_per_cta, &h_cols, &h_wts);
+    cluster_order_columns(g, CL_SIZE, sh.rows_per_cta, &h_cols, &h_wts);
     DevBuf<int> d_cols(std::max<size_t>(1, h_cols.size()));
     DevBuf<float> d_wts(std::max<size_t>(1, h_wts.size()));
     d_cols.upload(h_cols.data(), h_cols.size(), s);
@@ -170,13 +197,16 @@ static void run_cluster(oscb_graph *g, const oscb_run_params *p, int64_t steps, 
     DevBuf<long long> d_dbg;
     if (getenv("OSCB_CLUSTER_TRACE")) { d_dbg.alloc(8); d_dbg.zero(s); a.dbg = d_dbg.p; }
 
-    OSCB_CUDA(cudaFuncSetAttribute(k_cluster_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.lay.total));
+    const void *fn = CL_SIZE == 16 ? (const void *)k_cluster_fast<16> : (const void *)k_cluster_fast<8>;
+    OSCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh.lay.total));
+    if (CL_SIZE > 8) OSCB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     OSCB_CUDA(cudaStreamSynchronize(s));        // the host staging vectors die after this call
     cudaEvent_t ev0, ev1;
     OSCB_CUDA(cudaEventCreate(&ev0));
     OSCB_CUDA(cudaEventCreate(&ev1));
     OSCB_CUDA(cudaEventRecord(ev0, s));
-    k_cluster_fast<<<(unsigned)(R * CL_SIZE), sh.threads, sh.lay.total, s>>>(a);
+    if (CL_SIZE == 16) k_cluster_fast<16><<<(unsigned)(R * 16), sh.threads, sh.lay.total, s>>>(a);
+    else k_cluster_fast<8><<<(unsigned)(R * 8), sh.threads, sh.lay.total, s>>>(a);
     OSCB_CUDA(cudaEventRecord(ev1, s));
     {
         cudaError_t e = cudaGetLastError();
