@@ -112,6 +112,10 @@ __device__ __forceinline__ void trig_turns_fast(float y, float &s, float &c)
 // float64 rule for every float32 in [0, 1).
 __device__ __forceinline__ uint32_t state_from_boundaries(float p, const float *bnd, int n)
 {
+    if (n == 3) {      // the 3-colouring case, without the loop
+        const uint32_t st3 = (p >= bnd[0] ? 1u : 0u) + (p >= bnd[1] ? 1u : 0u) + (p >= bnd[2] ? 1u : 0u);
+        return st3 == 3u ? 0u : st3;
+    }
     uint32_t st = 0;
     for (int k = 0; k < n; ++k) st += (p >= bnd[k]) ? 1u : 0u;
     return st == (uint32_t)n ? 0u : st;
