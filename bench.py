@@ -55,7 +55,15 @@ def load_workload(name):
     from paper_2505_22631_b200 import workloads
     from paper_2505_22631_b200.model import CouplingMatrix, SolverParams
     shape, R, tune = WORKLOADS[name]
-    n, (u, v, w), N, kind = workloads.shape_graph(shape)
+    if shape == "flat200":
+        # the reference's own generator call, generate_colorable_graph(200, 479, 3, seed=0)
+        # (problems.py:255-276; the package's port returns the reference's edge list bit for bit --
+        # tests/test_oracle_golden.py::test_flat200_graph_is_the_reference_generators)
+        from paper_2505_22631_b200 import problems
+        g = problems.generate_colorable_graph(200, 479, 3, seed=0)
+        n, (u, v, w), N, kind = g.node_count, (g.u, g.v, g.w), 3, "coloring"
+    else:
+        n, (u, v, w), N, kind = workloads.shape_graph(shape)
     J = CouplingMatrix.from_edges(n, (u, v, w))
     params = SolverParams.tuned_for(n, N, seed=0, **tune)
     return shape, J, params, kind, R
@@ -159,6 +167,55 @@ def cpu_oracle_throughput(J, params, kind, R_cpu, window, threads=None):
 
 CPU_SAMPLE_STEPS = 2048     # Euler steps of the CPU arm's bounded sample
 
+_REF = None
+
+
+def reference_package():
+    """The UNMODIFIED reference package `oscim` (numpy + numba), pip-installed once from
+    /root/reference/pkg into baseline/_ref (git-ignored, travels to the GPU box).
+    None when it (or numba) cannot be imported -- the oracle port is then the only CPU arm."""
+    global _REF
+    if _REF is None:
+        _REF = False
+        ref = ROOT / "baseline" / "_ref"
+        if (ref / "oscim").is_dir():
+            os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "oscb_numba_cache"))
+            sys.path.insert(0, str(ref))
+            try:
+                import oscim  # noqa: F401
+                _REF = oscim
+            except Exception as e:          # numba missing / broken install: say so, fall back to the port
+                print(f"bench.py: reference package not importable ({e!r}); CPU arm = oracle port", file=sys.stderr)
+            finally:
+                sys.path.remove(str(ref))
+    return _REF or None
+
+
+def reference_throughput(indptr, indices, data, n, params, kind, R_cpu, steps, workers=None):
+    """`oscim.run_replica_set` (dynamics.py:469-493) of the unmodified reference on the same CSR, parameters
+    and a fixed step count; the time is the reference's own RunResult.wall_time (dynamics.py:356, :411:
+    RNG init + integrate + scoring + trace) summed over its sequential replica groups."""
+    oscim = reference_package()
+    workers = workers or (os.cpu_count() or 1)
+    Jr = oscim.CouplingMatrix(n, np.asarray(indptr), np.asarray(indices), np.asarray(data), "sparse")
+    pr = oscim.SolverParams(K=params.K, ks_max=params.ks_max, ks_period=params.ks_period, kn=params.kn, h=params.h,
+                            t_stop=steps * params.h, n_states=params.n_states, seed=0)
+    res = oscim.run_replica_set(Jr, pr, kind, replicas=R_cpu, workers=workers)
+    assert all(r.steps_executed == steps for r in res)
+    group = oscim.dynamics._group_size(n, R_cpu)
+    dt = sum(res[k].wall_time for k in range(0, R_cpu, group))      # one wall_time per group (shared by its replicas)
+    from oscim.dynamics import resolve_workers
+    return R_cpu * len(data) * steps / dt, dt, resolve_workers(workers), group
+
+
+def reference_sample(n, nnz, R, window):
+    """(replicas, steps) of the reference's bounded sample: whole replica groups (dynamics.py:463-466: the reference
+    runs groups one after another, so its cost is linear in the replica count), ~10-20 s at ~0.15 G updates/s."""
+    group = max(1, 4_000_000 // max(1, n * 256))
+    replicas = max(1, min(R, group))
+    steps = int(min(window, max(64, 2.5e9 / (nnz * replicas))))
+    return replicas, steps
+
 
 def cpu_sample(J, R, window, scale=1.0):
     """(replicas, steps) of the CPU arm's bounded sample: ~10-20 s of work at ~80 M updates/s/core,
@@ -173,6 +230,9 @@ def cpu_sample(J, R, window, scale=1.0):
 
 
 def run_reference_arm(args, rank, world):
+    """`--impl reference`: the reference's own CPU implementation on the box's host cores -- the unmodified Python
+    package when baseline/_ref imports (kind "reference"), else the oracle port (kind "port").  The port's number
+    rides along as `cpu_baseline_port` either way."""
     if rank != 0:
         return
     shape, J, params, kind, R = load_workload(args.workload)
@@ -180,23 +240,43 @@ def run_reference_arm(args, rank, world):
     # bounded sample: many replicas (they are what the CPU threads share) x a slice of the schedule --
     # the CPU cost of an Euler step does not depend on where in the schedule it sits
     R_cpu, steps_cpu = cpu_sample(J, R, window, scale=0.5)
-    for _ in range(args.warmup):
+    for _ in range(min(1, args.warmup)):
         cpu_oracle_throughput(J, params, kind, max(1, R_cpu // 8), max(32, steps_cpu // 16))
-    t_all, upd, threads = 0.0, 0.0, 1
-    for _ in range(args.steps):
-        v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
-        t_all += dt
-        upd += R_cpu * J.nnz * steps_cpu
+    port_v, port_dt, port_threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
+    port = {"value": port_v, "unit": "updates/s", "cores": port_threads, "kind": "port",
+            "sample": f"{R_cpu} replicas x {steps_cpu} Euler steps in {port_dt:.1f} s (oracle/ C+OpenMP port of the reference)"}
+    if reference_package() is not None:
+        R_ref, steps_ref = reference_sample(J.n, J.nnz, R, window)
+        for _ in range(min(1, args.warmup)):        # numba JIT + thread pool
+            reference_throughput(J.indptr, J.indices, J.data, J.n, params, kind, min(R_ref, 2), 64)
+        t_all = upd = 0.0
+        threads = group = 1
+        for _ in range(args.steps):
+            v, dt, threads, group = reference_throughput(J.indptr, J.indices, J.data, J.n, params, kind, R_ref, steps_ref)
+            t_all += dt
+            upd += R_ref * J.nnz * steps_ref
+        kind_label = "reference"
+        sample = (f"oscim.run_replica_set (unmodified reference, numpy + numba, workers={threads}): {R_ref} replicas "
+                  f"(one group of {group}) x {steps_ref} Euler steps per step (of {R} replicas x {window} steps per GPU); "
+                  f"the reference runs its groups one after another, so its time is linear in replicas and steps")
+    else:
+        t_all, upd, threads = 0.0, 0.0, 1
+        for _ in range(args.steps):
+            v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
+            t_all += dt
+            upd += R_cpu * J.nnz * steps_cpu
+        kind_label = "port"
+        sample = (f"{R_cpu} replicas x {steps_cpu} Euler steps per step (of {R} replicas x {window} steps per GPU), "
+                  f"linear in replicas and steps")
     value = upd / t_all
-    sample = (f"{R_cpu} replicas x {steps_cpu} Euler steps per step (of {R} replicas x {window} steps per GPU), "
-              f"linear in replicas and steps")
     line = {
         "impl": "reference", "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_all / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_label(shape, J, params, R, window), "replicas_per_gpu": R, "window": window,
                    "sample": sample},
-        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": kind_label, "sample": sample},
+        "cpu_baseline_port": port,
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -418,6 +498,89 @@ def bench_dense(args, rank, world, local_rank):
         }), flush=True)
 
 
+def reference_target():
+    """0.99 x the best `best_objective` of 96 CPU-oracle replicas (numpy's noise stream, whole default schedule)
+    on the synthetic G22-shape graph -- tests/golden/fullsize_fixtures.npz, written by
+    tests/golden/make_fullsize_fixtures.py."""
+    f = ROOT / "tests" / "golden" / "fullsize_fixtures.npz"
+    if not f.exists():
+        return None
+    z = np.load(f)
+    return float(z["g22_target_best"]), int(len(z["g22_best"]))
+
+
+def time_to_target(dyn, J, params, kind, seeds, args, local_rank, phi0, R):
+    """Time-to-99 %-best-cut on the G22 shape, both arms against the SAME reference-derived target."""
+    anchor = reference_target()
+    run = lambda **kw: dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
+                                     want_phases=False, want_traces=False, **kw)
+    if anchor is None:
+        best, how_target = float(run(want_states=False).best_objective.max()), "0.99 x best cut of this GPU batch (fixture missing)"
+    else:
+        best, how_target = anchor[0], f"0.99 x best best_objective of {anchor[1]} CPU-oracle seeds (tests/golden/fullsize_fixtures.npz)"
+    target = 0.99 * best
+    hit = run(target=target, want_states=False)
+    hits = hit.first_hit_step[hit.first_hit_step >= 0]
+    first = int(hits.min()) if len(hits) else -1
+    measured = e2e_hit = None
+    if first >= 0:
+        # the solve actually stopped at the step that reaches the target: device time, and wall clock
+        # through the API with host phases in and the best states / objectives out
+        stop = max(1, first + 1)
+        for _ in range(2):
+            short = run(steps=stop, phi0=phi0)
+        t0 = time.perf_counter()
+        short = run(steps=stop, phi0=phi0)
+        e2e_hit = time.perf_counter() - t0
+        measured = short.device_ms / 1e3
+        assert float(short.best_objective.max()) >= target
+    out = {"best_cut_reference": best, "target": target, "target_from": how_target, "first_hit_step": first,
+           "steps_total": hit.steps, "seconds": measured, "e2e_seconds": e2e_hit, "gpu_best_cut": float(hit.best_objective.max()),
+           "how": "a run of first_hit_step + 1 Euler steps of all replicas: CUDA-event time of the launch, and wall clock "
+                  "of the API call with host buffers",
+           "full_run_seconds": hit.device_ms / 1e3, "replicas": R}
+    if not args.no_cpu_baseline:
+        # the CPU arm to the same target: one replica per host thread (seeds 0..T-1), best-so-far sampled every 50 steps
+        # (dynamics.py:377-384 best_trace); then the run that stops at the first sample reaching the target is timed
+        from oracle import oracle as O
+        O.build()
+        T = O.max_threads()
+        sim = lambda t_stop, stride: O.simulate(J.indptr, J.indices, J.data, K=params.K, ks_max=params.ks_max,
+                                                ks_period=params.ks_period, kn=params.kn, h=params.h, t_stop=t_stop,
+                                                n_states=params.n_states, seeds=list(range(T)), objective=kind,
+                                                trace_stride=stride, threads=T)
+        t0 = time.perf_counter()
+        full = sim(params.t_stop, 50 * params.h)
+        full_s = time.perf_counter() - t0
+        reached = np.nonzero(full.best_trace.max(axis=0) >= target)[0]
+        cpu = {"replicas": T, "cores": T, "kind": "port", "full_run_seconds": full_s, "best_cut": float(full.best_objective.max())}
+        if len(reached):
+            t_hit = float(full.trace_t[reached[0]])
+            t0 = time.perf_counter()
+            part = sim(max(t_hit, 2 * params.h), 50 * params.h)
+            cpu.update(seconds=time.perf_counter() - t0, first_hit_t=t_hit, first_hit_step=int(round(t_hit / params.h)),
+                       reached=bool(part.best_objective.max() >= target))
+        else:
+            cpu.update(seconds=None, note="target not reached by this batch within the default schedule")
+        out["cpu"] = cpu
+    return out
+
+
+def self_launch(n_ranks):
+    """Re-run this command line under torch.distributed.run with `n_ranks` local ranks.  NCCL's communicator
+    INIT lines go to stderr (NCCL_DEBUG=INFO unless the caller set it) so the rank count is visible from outside."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_ranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -433,11 +596,30 @@ def main():
     ap.add_argument("--replicas", type=int, default=0, help="override replicas per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-target", action="store_true", help="skip the time-to-99%%-best-cut run")
+    ap.add_argument("--no-parity-mode", action="store_true", help="skip the float64 sub-record of the same workload")
     args = ap.parse_args()
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        # `python bench.py --gpus N` without a launcher: become N ranks (one process per GPU, rendezvous on 127.0.0.1)
+        raise SystemExit(self_launch(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.impl == "reference" else 1)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("OSCB_BENCH_DRYRUN"):
+        # launcher check (tests/test_bench_launch.py): rendezvous only, no device work
+        import torch.distributed as dist
+        import torch
+        if world > 1:
+            dist.init_process_group("gloo")
+            t = torch.ones(1)
+            dist.all_reduce(t)
+            seen = int(t.item())
+            dist.destroy_process_group()
+        else:
+            seen = 1
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_seen": seen, "gpus_arg": args.gpus}), flush=True)
+        return
     if args.impl == "reference":
         if args.workload.startswith("SK"):
             bench_dense(args, rank, world, 0)
@@ -453,6 +635,9 @@ def main():
     backend = os.environ.get("OSCB_BENCH_BACKEND", "nccl")
     if backend != "nccl":
         local_rank = local_rank % torch.cuda.device_count()
+    elif world > torch.cuda.device_count() and "LOCAL_RANK" in os.environ:
+        raise SystemExit(f"bench.py --gpus {world}: this node has {torch.cuda.device_count()} GPU(s); "
+                         f"OSCB_BENCH_BACKEND=gloo shares one GPU between the ranks for a functional check")
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
@@ -535,7 +720,7 @@ def main():
     peaks, peak_kind = measured_peaks()
     s_phi = 4 if args.precision == "f32" else 8
     bytes_per_launch = algorithmic_bytes_per_euler_step(J, R, bool(info.unit_weights), s_phi) * window
-    if last.kernel == "resident":
+    if last.kernel in ("resident", "lowdeg", "cluster"):
         kernel_ms = dev_ms / args.steps           # one persistent launch integrates the whole window
         launch_bytes = bytes_per_launch
         launch_updates = R * J.nnz * window
@@ -549,15 +734,19 @@ def main():
     sm_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     smem_peak = 128.0 * info_sm_count * sm_mhz * 1e6 / 1e9
     smem_achieved = launch_updates * (2 * s_phi) / (kernel_ms * 1e-3) / 1e9
-    traffic = None
-    tpath = ROOT / "profiles" / "dram_traffic.json"     # written from the committed ncu --set full capture
+    kernel_name = {"resident": "k_resident_fast" if args.precision == "f32" else "k_resident",
+                   "lowdeg": "k_lowdeg"}.get(last.kernel, last.kernel)
+    # DRAM bytes per launch cannot be counted from inside an untraced run: the figure is the one transcribed from the
+    # committed `ncu --set full` capture of this exact (workload, kernel, precision, window); anything else says so
+    traffic, traffic_source = None, "not captured for this (workload, kernel, precision, window)"
+    tpath = ROOT / "profiles" / "dram_traffic.json"
     if tpath.exists():
         t = json.loads(tpath.read_text()).get(f"{args.workload}:{last.kernel}:{args.precision}:{window}")
         if t:
-            traffic = t["dram_bytes_per_launch"]
+            traffic, traffic_source = t["dram_bytes_per_launch"], t.get("source", "profiles/dram_traffic.json")
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "k_resident_fast" if last.kernel == "resident" and args.precision == "f32" else last.kernel,
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_source, "peak_kind": peak_kind,
+                "kernel": kernel_name,
                 "algorithmic_bytes_per_launch": launch_bytes, "bytes_per_update": launch_bytes / launch_updates,
                 "binding_resource": {"name": "shared-memory gather wavefronts", "achieved": smem_achieved, "peak": smem_peak,
                                      "unit": "GB/s", "frac": smem_achieved / smem_peak,
@@ -580,42 +769,44 @@ def main():
         "roofline": roofline,
     }
 
+    if rank == 0 and not args.no_parity_mode and args.precision == "f32":
+        # the same workload in the reference's own arithmetic (float64 state, the reference's operation order:
+        # dynamics.py:155-190) -- the throughput the parity mode sustains, beside the float32 headline
+        dyn.run_batch(J, params, kind, seeds, precision="f64", device=local_rank, kernel=args.kernel, steps=min(window, 256),
+                      want_phases=False, want_states=False, want_traces=False)
+        p64 = dyn.run_batch(J, params, kind, seeds, precision="f64", device=local_rank, kernel=args.kernel, steps=window,
+                            want_phases=False, want_states=False, want_traces=False)
+        b64 = algorithmic_bytes_per_euler_step(J, R, bool(info.unit_weights), 8) * window
+        ach64 = b64 / (p64.device_ms * 1e-3) / 1e9
+        line["parity_mode"] = {"precision": "f64", "value": R * J.nnz * window / (p64.device_ms * 1e-3), "unit": "updates/s",
+                               "ms_per_step": p64.device_ms, "kernel": p64.kernel, "replicas_per_cta": p64.replicas_per_cta,
+                               "frac": ach64 / peaks["hbm_gbs"], "achieved_gbs": ach64,
+                               "note": "one solve of the same workload (this rank's replicas) with precision='f64', CUDA-event time; "
+                                       "frac = algorithmic bytes at 8 B per phase / time / measured HBM peak"}
+
     if rank == 0 and not args.no_target and shape == "G22":
-        # time-to-99%-best-cut: full default schedule, target = 0.99 x best cut of this batch
-        full = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
-                             want_phases=False, want_states=False, want_traces=False)
-        best = float(full.best_objective.max())
-        hit = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
-                            target=0.99 * best, want_phases=False, want_states=False, want_traces=False)
-        hits = hit.first_hit_step[hit.first_hit_step >= 0]
-        first = int(hits.min()) if len(hits) else -1
-        measured = e2e_hit = None
-        if first >= 0:
-            # the solve actually stopped at the step that reaches the target: device time, and wall clock
-            # through the API with host phases in and the best states / objectives out
-            stop = max(1, first + 1)
-            for _ in range(2):
-                short = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
-                                      steps=stop, phi0=phi0, want_phases=False, want_traces=False)
-            t0 = time.perf_counter()
-            short = dyn.run_batch(J, params, kind, seeds, precision=args.precision, device=local_rank, kernel=args.kernel,
-                                  steps=stop, phi0=phi0, want_phases=False, want_traces=False)
-            e2e_hit = time.perf_counter() - t0
-            measured = short.device_ms / 1e3
-            assert float(short.best_objective.max()) >= 0.99 * best
-        line["time_to_99pct_best_cut"] = {
-            "best_cut": best, "target": 0.99 * best, "first_hit_step": first, "steps_total": hit.steps,
-            "seconds": measured, "e2e_seconds": e2e_hit,
-            "how": "a run of first_hit_step + 1 Euler steps of all replicas: CUDA-event time of the launch, and wall clock "
-                   "of the API call with host buffers",
-            "full_run_seconds": hit.device_ms / 1e3, "replicas": R}
+        line["time_to_99pct_best_cut"] = time_to_target(dyn, J, params, kind, seeds, args, local_rank, phi0, R)
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         R_cpu, steps_cpu = cpu_sample(J, R, window)
         v, dt, threads = cpu_oracle_throughput(J, params, kind, R_cpu, steps_cpu)
-        line["cpu_baseline"] = {"value": v, "unit": "updates/s", "cores": threads, "kind": "port",
-                                "sample": f"{R_cpu} replicas x {steps_cpu} Euler steps of the same workload in {dt:.1f} s "
-                                          f"(oracle/ C+OpenMP port of the reference; linear in replicas and steps)"}
+        port = {"value": v, "unit": "updates/s", "cores": threads, "kind": "port",
+                "sample": f"{R_cpu} replicas x {steps_cpu} Euler steps of the same workload in {dt:.1f} s "
+                          f"(oracle/ C+OpenMP port of the reference; linear in replicas and steps)"}
+        line["cpu_baseline"] = port
+        if reference_package() is not None:
+            try:
+                R_ref, steps_ref = reference_sample(J.n, J.nnz, R, window)
+                reference_throughput(J.indptr, J.indices, J.data, J.n, params, kind, min(R_ref, 2), 64)   # JIT warm-up
+                rv, rdt, rthreads, group = reference_throughput(J.indptr, J.indices, J.data, J.n, params, kind, R_ref, steps_ref)
+                line["cpu_baseline"] = {
+                    "value": rv, "unit": "updates/s", "cores": rthreads, "kind": "reference",
+                    "sample": f"oscim.run_replica_set of the unmodified reference (baseline/_ref, numpy + numba, workers={rthreads}): "
+                              f"{R_ref} replicas (one group of {group}) x {steps_ref} Euler steps of the same workload in {rdt:.1f} s; "
+                              f"groups run one after another in the reference, so linear in replicas and steps"}
+                line["cpu_baseline_port"] = port
+            except Exception as e:
+                line["cpu_baseline_reference_error"] = repr(e)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
