@@ -120,3 +120,18 @@ def test_whole_runs(oracle, golden, graph, tag, kind, replicas, stride):
 
 def test_golden_provenance(golden):
     assert str(golden["meta_oscim"]) == "0.1.0"
+
+
+def test_fullsize_fixture_reproduces(oracle):
+    """tests/golden/fullsize_fixtures.npz (the oracle's results at the benchmarked sizes) is what the oracle
+    built here produces: the first replicas of the flat200 whole-schedule fixture, bit for bit."""
+    from pathlib import Path
+    import bench
+    fix = np.load(Path(__file__).resolve().parent / "golden" / "fullsize_fixtures.npz")
+    _, J, params, kind, _ = bench.load_workload("flat200x4096")
+    seeds = [int(s) for s in fix["flat200_seeds"][:6]]
+    r = oracle.simulate(J.indptr, J.indices, J.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period,
+                        kn=params.kn, h=params.h, t_stop=params.t_stop, n_states=3, seeds=seeds, objective=kind,
+                        threads=oracle.max_threads())
+    assert np.array_equal(r.best_objective, fix["flat200_best"][:6])
+    assert float(fix["g22_target_best"]) == fix["g22_best"].max() and len(fix["g22_best"]) >= 64
