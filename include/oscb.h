@@ -58,6 +58,7 @@ extern "C" {
 #define OSCB_KERNEL_RESIDENT 2 /* persistent CTA per replica tile, phases' (cos,sin) in smem */
 #define OSCB_KERNEL_DENSE_TC 3 /* dense integer J: persistent tcgen05 int8 GEMM J*[cos|sin] digit planes */
 #define OSCB_KERNEL_CLUSTER 4  /* latency mode: one replica per 8-CTA cluster, pairs exchanged through DSMEM */
+#define OSCB_KERNEL_LOWDEG 5   /* low-degree graphs: persistent CTA per replica tile, phases in registers, pairs in smem */
 
 typedef struct oscb_graph oscb_graph;
 
@@ -224,6 +225,19 @@ int oscb_dense_tc_stream(const oscb_graph *g, int32_t n_states, int64_t R, int32
  * float32 decision-boundary table (N = 3..8), differs from the reference threshold
  * (dynamics.py:203-213); also bounds the error of the fast trig.  Must return 0 mismatches. */
 int oscb_selftest_sign_state(int device, uint64_t *mismatches);
+
+/* Host-only: the stream compiler of the low-degree persistent kernel (OSCB_KERNEL_LOWDEG; no GPU needed).  For a
+ * tile of `replicas_per_cta` replicas (a power of two <= 32), `warps` warps per CTA and `items_per_thread` quads
+ * per thread it returns the position -> quad map quad_of [warps * items_per_thread * C] (C = 32 / replicas_per_cta;
+ * >= ceil(n / 4): no quad), the component-major slot of every oscillator slot_of [n], and the ELL stream of
+ * 4-neighbour groups: offsets [4 * entries] (slot * replicas_per_cta * 8 bytes; bit 31 of a group's 4th offset marks
+ * the last group of a row when the graph is not uniform, i.e. has a row of more than 4 neighbours) and couplings
+ * [4 * entries] (padding: an all-zero pad slot, coupling 0).  Call once with NULL buffers for
+ * `entries`.  Restates the traversal of the CSR rows of dynamics.py:166-170 for that kernel. */
+int oscb_lowdeg_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, const double *weights,
+                          int32_t replicas_per_cta, int32_t warps, int32_t items_per_thread, int32_t *uniform,
+                          int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
+                          uint32_t *offsets, float *couplings, int32_t *warp_start);
 
 /* Host-only: the graph compiler of the persistent kernel (no GPU needed).  Turns a canonical CSR
  * (model.py:135-149) into the sliced-ELL neighbour stream for tiles of `replicas_per_cta`

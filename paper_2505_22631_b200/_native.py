@@ -24,8 +24,8 @@ OBJ = {"maxcut": 0, "coloring": 1}
 PREC = {"f32": 32, "f64": 64}
 NOISE_DEVICE, NOISE_HOST, NOISE_NONE = 0, 1, 2
 FUSED_MEM_BYTES = 96
-KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2, "dense-tc": 3, "cluster": 4}
-KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident", 3: "dense-tc", 4: "cluster"}
+KERNEL = {"auto": 0, "stream": 1, "resident": 2, "resident-generic": 2, "dense-tc": 3, "cluster": 4, "lowdeg": 5}
+KERNEL_NAME = {0: "auto", 1: "stream", 2: "resident", 3: "dense-tc", 4: "cluster", 5: "lowdeg"}
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC"]
@@ -96,6 +96,8 @@ SYMBOLS = {
     "oscb_resident_plan_host": (C.c_int, [C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int64), _P, _P, _P, _P]),
+    "oscb_lowdeg_plan_host": (C.c_int, [C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, _P, _P, _P, _P]),
     "oscb_run": (C.c_int, [_P, C.POINTER(RunParams), _P, C.c_int64, _P, _P, C.POINTER(RunOutputs)]),
 }
 

@@ -13,6 +13,7 @@
 #include "oscb_resident_host.hpp"
 #include "oscb_dense_host.hpp"
 #include "oscb_umma.hpp"
+#include "oscb_lowdeg.hpp"
 #include "oscb_cluster_host.hpp"
 #include <type_traits>
 
@@ -115,6 +116,11 @@ template <typename F> static int guarded(F &&f)
 }
 
 static inline unsigned blocks_for(long long total, int threads) { return (unsigned)((total + threads - 1) / threads); }
+
+void launch_initial_phases(const uint64_t *d_seeds, double *d_phi, int n, int R, cudaStream_t s)
+{
+    k_initial_phases<<<blocks_for((long long)((n + 3) / 4) * R, 128), 128, 0, s>>>(d_seeds, d_phi, n, R);
+}
 
 // dynamics.py:325-330 (Python round() == round-half-even == nearbyint in the default mode)
 static int64_t reference_cadence(int64_t n, int64_t pair_count)
@@ -1320,6 +1326,14 @@ int oscb_run(oscb_graph *g, const oscb_run_params *p, const uint64_t *seeds, int
                          "the cluster kernel takes float32, device noise, N = 2 max-cut, 64 <= n <= 65535 and unit or small integer couplings");
         if ((kernel == OSCB_KERNEL_AUTO && cluster_applies(g, p, R, false)) || kernel == OSCB_KERNEL_CLUSTER) {
             run_cluster(g, p, rp.steps, rp.cadence, rp.sample_steps, seeds, R, phi0, out);
+            return OSCB_OK;
+        }
+        if (kernel == OSCB_KERNEL_LOWDEG)
+            OSCB_REQUIRE(lowdeg_applies(g, p, R, true),
+                         "the low-degree kernel takes float32, device noise, max degree <= 16, n up to ~28000 and N = 2 max-cut on "
+                         "integer couplings or N = 3 colouring on unit couplings");
+        if ((kernel == OSCB_KERNEL_AUTO && lowdeg_applies(g, p, R, false)) || kernel == OSCB_KERNEL_LOWDEG) {
+            run_lowdeg(g, p, rp.steps, rp.cadence, rp.sample_steps, seeds, R, phi0, out);
             return OSCB_OK;
         }
         if (kernel == OSCB_KERNEL_AUTO)

@@ -88,6 +88,10 @@ struct ResidentPlan; // oscb_resident_host.hpp
 struct DensePlan;    // oscb_dense_host.hpp
 struct ShardWork;    // oscb.cu: workspace of the row-sharded dense driver
 struct UmmaPlan;     // oscb_umma.hpp: tile images of J for the tensor-core dense kernel
+struct LowdegPlan;   // oscb_lowdeg_host.hpp: slot map + ELL stream of the low-degree kernel
+
+// numpy's Philox4x64 initial phases of replicas `seeds` into phi [R][n] float64 (k_initial_phases, oscb.cu)
+void launch_initial_phases(const uint64_t *d_seeds, double *d_phi, int n, int R, cudaStream_t s);
 
 } // namespace oscb
 
@@ -113,6 +117,7 @@ struct oscb_graph {
 
     // resident-kernel plans keyed by (precision, replicas_per_cta, threads)
     std::map<uint64_t, std::shared_ptr<oscb::ResidentPlan>> plans;
+    std::map<uint64_t, std::shared_ptr<oscb::LowdegPlan>> lowdeg_plans;
     std::shared_ptr<oscb::DensePlan> dense;
     std::shared_ptr<oscb::ShardWork> shard_work;
     std::shared_ptr<oscb::UmmaPlan> umma;

@@ -15,11 +15,12 @@
 //   * a step is pass A (gather + update into the registers) | barrier | pass B (trig of the new phase, the
 //     pair stored to its slot) | barrier.  Nothing is staged through L2;
 //   * the neighbour stream is ELL with 4-neighbour groups, read straight from global memory (L2) by the lane
-//     that uses it, coalesced: {4 x u16 slot ids, 4 x f16 couplings} = 16 B per group for N = 2 (integer
-//     couplings are exact in f16; unit weights are the same stream with 1.0), 8 B for the unit-weight
-//     N = 3 colouring.  UNIFORM graphs (every row <= 4 neighbours) have exactly one group per row at an
-//     address known at compile time up to a stride -- straight-line code; otherwise a warp walks its
-//     groups with a running pointer and a "last group of the row" flag in the stream itself;
+//     that uses it, coalesced: 4 x u32 BYTE OFFSETS of the neighbours' slots (no unpacking, no address
+//     arithmetic: with one replica per CTA the offset is the LDS address) and, for N = 2, 4 x f32 couplings
+//     (unit weights are the same stream with 1.0; padding reads an all-zero slot with coupling 0).  UNIFORM
+//     graphs (every row <= 4 neighbours) have exactly one group per row at an address known at compile time up
+//     to a stride -- straight-line code; otherwise a warp walks its groups with a running pointer and a "last
+//     group of the row" flag in bit 31 of the group's fourth offset;
 //   * read-out rides on the gather of the NEXT step (as in k_resident_fast): for N = 2 the sign bit of a stored
 //     cosine is the oscillator's lattice state, and cut = (W - sum_i sigma_i sum_j w_ij sigma_j) / 4 needs one
 //     LOP3 + one FADD per neighbour; for N = 3 the low three mantissa bits of the stored cosine hold the
@@ -29,8 +30,7 @@
 //
 // Arithmetic of a step (float32, FMA-contracted) is k_resident_fast's; parity is by tolerance and distribution.
 #pragma once
-#include "oscb_resident_fast.cuh"
-#include <cuda_fp16.h>
+#include "oscb_fastmath.cuh"
 
 namespace oscb {
 
@@ -42,15 +42,16 @@ struct LowdegArgs {
     uint32_t off_cnt, off_part, off_misc;      // (the pairs start at shared offset 0)
     float hK, knsh;
     int noise_on, maximize, use_target, n_sample_steps;
-    long long step_begin, step_end, cadence, trace_stride;
+    int step_begin, step_end, cadence;
+    long long trace_stride;
     double target, w_total;
     const uint32_t *quad_of;        // [Qp] quad at a position; >= Q: none (ghost item)
-    const uint4 *stream_w;          // N = 2: {ids 0|1, ids 2|3, f16 w 0|1, f16 w 2|3}
-    const uint2 *stream_u;          // N = 3: {ids 0|1, ids 2|3}
+    const uint4 *soff;              // byte offsets of a group's four neighbour slots (replica 0 of the tile)
+    const float4 *swt;              // N = 2: their couplings
     const int *warp_start;          // looped streams: first group row of each warp
     const float *hks_table;         // [steps + 1]  h ks(step) (x2 for N = 2), float64 on the host
     const uint64_t *seeds;          // [tiles * RT]
-    const long long *sample_steps;  // global step indices after which a trace sample is taken
+    const int *sample_steps;        // global step indices after which a trace sample is taken
     float bnd[4];                   // N = 3: the float32 decision boundaries of the reference threshold rule
     double *io;                     // [R][n] phases in and out (float64, the reference's layout)
     double *best_obj, *energy, *best_trace;
@@ -59,45 +60,66 @@ struct LowdegArgs {
     unsigned long long *nonfinite;
 };
 
+// threads per CTA by items per thread: the phases of QPT quads stay in registers, so more items need more registers
+// per thread (64 / 80 / 128)
+__host__ __device__ constexpr int lowdeg_max_threads(int qpt) { return qpt <= 4 ? 1024 : (qpt <= 7 ? 768 : 512); }
+
+// x - floor(x) on the FMA/ALU pipes for |x| < 2^22 (the conversion unit is as busy as the MUFU unit here): the
+// magic-number add rounds x to the nearest integer, a compare steps it down to the floor.  Anything larger (or
+// non-finite) takes floorf.  Same value as x - floorf(x) for every x (both subtractions are exact or round once).
+__device__ __forceinline__ float frac_alu(float x)          // |x| < 2^22
+{
+    const float r = (x + 12582912.0f) - 12582912.0f;        // rint(x)
+    const float f = r - (r > x ? 1.0f : 0.0f);              // floor(x)
+    return x - f;
+}
+
 __device__ __forceinline__ float xor_sign(float w, float c)       // w * sigma(c): flip w's sign where c's sign bit is set
 {
     return __uint_as_float(__float_as_uint(w) ^ (__float_as_uint(c) & 0x80000000u));
 }
 
 // NMODE 2: OIM max-cut, integer couplings;  NMODE 3: OPM 3-colouring, unit couplings.
-template <int NMODE, int QPT, bool UNIFORM>
-__global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const LowdegArgs a)
+// RT1: one replica per CTA (a slot offset IS the shared-memory address of the pair).
+template <int NMODE, int QPT, bool UNIFORM, bool RT1>
+__global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const LowdegArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float2 *cs = reinterpret_cast<float2 *>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int r = lane & (a.RT - 1), c = lane >> a.LRT;
+    const int r = RT1 ? 0 : (lane & (a.RT - 1)), c = RT1 ? lane : (lane >> a.LRT);
     const int tile = blockIdx.x, rg = tile * a.RT + r;
     const bool live = rg < a.R_real;
-    const float2 *cs_lane = cs + r;                                  // + slot * RT
+    const unsigned char *cs_lane = smem_raw + r * 8;                 // + slot byte offset
     const int WC = a.W * a.C;
     const int pos0 = warp * a.C + c;                                 // position of item 0; item t: + t * WC
-    const uint32_t kstep = (uint32_t)a.Qp * a.RT;                    // pairs between component planes
+    const uint32_t kbytes = (uint32_t)a.Qp * a.RT * 8;               // bytes between component planes
+    const uint32_t tbytes = (uint32_t)WC * a.RT * 8;                 // bytes between the items of a thread
+    const uint32_t own0 = (uint32_t)(pos0 * a.RT + r) * 8;           // own slot of (item 0, component 0)
     int *cnt = reinterpret_cast<int *>(smem_raw + a.off_cnt);
     double *part = reinterpret_cast<double *>(smem_raw + a.off_part);
     double *best_s = reinterpret_cast<double *>(smem_raw + a.off_misc);
     int *improved_s = reinterpret_cast<int *>(smem_raw + a.off_misc + a.RT * 8);
+    auto pair_at = [&](uint32_t off) -> float2 {
+        return *reinterpret_cast<const float2 *>((RT1 ? smem_raw : cs_lane) + off);
+    };
 
     // ---- prologue: the thread's items ------------------------------------------------------------
-    uint32_t qid[QPT];
+    // the quad of item t: its position itself on uniform graphs (natural order), else looked up (L1/L2) when needed
+    auto quad = [&](int t) -> uint32_t { return UNIFORM ? (uint32_t)(pos0 + t * WC) : __ldg(a.quad_of + pos0 + t * WC); };
     float phi[QPT][4];
 #pragma unroll
     for (int t = 0; t < QPT; ++t) {
-        qid[t] = a.quad_of[pos0 + t * WC];
+        const uint32_t q = quad(t);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t i = 4u * qid[t] + k;
-            phi[t][k] = (qid[t] < (uint32_t)a.Q && i < (uint32_t)a.n && live) ? (float)a.io[(size_t)rg * a.n + i] : 0.0f;
+            const uint32_t i = 4u * q + k;
+            phi[t][k] = (q < (uint32_t)a.Q && i < (uint32_t)a.n && live) ? (float)a.io[(size_t)rg * a.n + i] : 0.0f;
         }
     }
     const uint64_t seed = a.seeds[rg];
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
-    for (int i = tid; i < OSCB_LD_PADS * a.RT; i += blockDim.x) cs[(size_t)4 * kstep + i] = make_float2(0.0f, 0.0f);
+    for (int i = tid; i < OSCB_LD_PADS * a.RT; i += blockDim.x)
+        reinterpret_cast<float2 *>(smem_raw + (size_t)4 * kbytes)[i] = make_float2(0.0f, 0.0f);
     if (tid < a.RT) {
         best_s[tid] = a.best_obj[tile * a.RT + tid];
         improved_s[tid] = 0;
@@ -108,77 +130,75 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
     auto pass_b = [&]() {
 #pragma unroll
         for (int t = 0; t < QPT; ++t) {
-            float2 *own = cs + (size_t)(pos0 + t * WC) * a.RT + r;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 float s, co;
-                trig_turns_fast(phi[t][k], s, co);
+                trig_turns_direct(phi[t][k], s, co);
                 if (NMODE == 3) {
                     const float p = phi[t][k];
                     const uint32_t oh = (p >= a.bnd[0] && p < a.bnd[1]) ? 2u : ((p >= a.bnd[1] && p < a.bnd[2]) ? 4u : 1u);
                     co = __uint_as_float((__float_as_uint(co) & ~7u) | oh);
                 }
-                own[(size_t)k * kstep] = make_float2(co, s);
+                *reinterpret_cast<float2 *>(smem_raw + own0 + t * tbytes + k * kbytes) = make_float2(co, s);
             }
         }
     };
     pass_b();
     __syncthreads();
 
-    const uint4 *sw = a.stream_w + ((size_t)(UNIFORM ? warp * 4 : a.warp_start[warp]) * a.C + c);
-    const uint2 *su = a.stream_u + ((size_t)(UNIFORM ? warp * 4 : a.warp_start[warp]) * a.C + c);
+    const size_t first_row = UNIFORM ? (size_t)warp * 4 : (size_t)a.warp_start[warp];
+    const uint4 *so = a.soff + first_row * a.C + c;
+    const float4 *sw = a.swt + first_row * a.C + c;
     const int W4C = a.W * 4 * a.C;
 
     // what the state now in shared memory still owes: a cadence score, or a trace sample (column >= 0)
     bool pending = true;
     int pending_col = 0;                 // the t = 0 sample (dynamics.py:385)
-    long long pending_label = -1;
+    int pending_label = -1;
     int sample_cur = 0;
     while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < a.step_begin) ++sample_cur;
-    long long next_sample = sample_cur < a.n_sample_steps ? a.sample_steps[sample_cur] : -1;
-    int cmod = a.cadence > 0 ? (int)(a.step_begin % a.cadence) : 1;
+    int next_sample = sample_cur < a.n_sample_steps ? a.sample_steps[sample_cur] : -1;
+    int cmod = a.cadence > 0 ? a.step_begin % a.cadence : 1;
 
     // ---- pass A ------------------------------------------------------------------------------------
     // MODE 0: update only; 1: + read-out count; 2: + read-out count + energy; 3: count + energy, no update
-    auto pass_a = [&](auto mode_tag, long long step, float hks) {
+    auto pass_a = [&](auto mode_tag, int step, float hks) {
         constexpr int MODE = decltype(mode_tag)::value;
         float S = 0.0f;          // N = 2: sum_i sigma_i sum_j w_ij sigma_j (exact integer in float32)
         uint32_t same = 0;       // N = 3: equal-state neighbours
         double en = 0.0;         // (22 passes per run carry it)
-        const uint4 *pw = sw;
-        const uint2 *pu = su;
-        uint4 curw = make_uint4(0, 0, 0, 0);
-        uint2 curu = make_uint2(0, 0);
+        bool bad = false;
+        const uint4 *po = so;
+        const float4 *pw = sw;
+        uint4 cur_o = make_uint4(0, 0, 0, 0);
+        float4 cur_w = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!UNIFORM) {
-            if (NMODE == 2) curw = *pw; else curu = *pu;
+            cur_o = *po;
+            if (NMODE == 2) cur_w = *pw;
         }
 #pragma unroll
         for (int t = 0; t < QPT; ++t) {
             float z[4] = {0.f, 0.f, 0.f, 0.f};
             if (MODE != 3 && a.noise_on)
-                normals4_fast(philox4x32_10(make_uint4(qid[t], (uint32_t)step, (uint32_t)(step >> 32), 0x6F736362u), key),
-                              z[0], z[1], z[2], z[3]);
-            const float2 *own_p = cs_lane + (size_t)(pos0 + t * WC) * a.RT;
+                normals4_fast(philox4x32_10(make_uint4(quad(t), (uint32_t)step, 0u, 0x6F736362u), key), z[0], z[1], z[2], z[3]);
             float ynew[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const float2 own = own_p[(size_t)k * kstep];
+                const float2 own = *reinterpret_cast<const float2 *>(smem_raw + own0 + t * tbytes + k * kbytes);
                 const uint32_t ownmask = NMODE == 3 ? (__float_as_uint(own.x) & 7u) : 0u;
                 float2 sum = make_float2(0.f, 0.f);
                 float tsig = 0.f;
                 uint32_t eq = 0;
-                auto group = [&](uint32_t ix, uint32_t iy, uint32_t wx, uint32_t wy) {
-                    const float2 v0 = cs_lane[ix & 0xffffu], v1 = cs_lane[ix >> 16];
-                    const float2 v2 = cs_lane[iy & 0xffffu], v3 = cs_lane[UNIFORM ? (iy >> 16) : ((iy >> 16) & 0x7fffu)];
+                auto group = [&](const uint4 o, const float4 w) {
+                    const float2 v0 = pair_at(o.x), v1 = pair_at(o.y), v2 = pair_at(o.z);
+                    const float2 v3 = pair_at(UNIFORM ? o.w : (o.w & 0x7fffffffu));
                     if (NMODE == 2) {
-                        const float2 w01 = __half22float2(*reinterpret_cast<const __half2 *>(&wx));
-                        const float2 w23 = __half22float2(*reinterpret_cast<const __half2 *>(&wy));
-                        sum = __ffma2_rn(make_float2(w01.x, w01.x), v0, sum);
-                        sum = __ffma2_rn(make_float2(w01.y, w01.y), v1, sum);
-                        sum = __ffma2_rn(make_float2(w23.x, w23.x), v2, sum);
-                        sum = __ffma2_rn(make_float2(w23.y, w23.y), v3, sum);
+                        sum = __ffma2_rn(make_float2(w.x, w.x), v0, sum);
+                        sum = __ffma2_rn(make_float2(w.y, w.y), v1, sum);
+                        sum = __ffma2_rn(make_float2(w.z, w.z), v2, sum);
+                        sum = __ffma2_rn(make_float2(w.w, w.w), v3, sum);
                         if (MODE >= 1)
-                            tsig += (xor_sign(w01.x, v0.x) + xor_sign(w01.y, v1.x)) + (xor_sign(w23.x, v2.x) + xor_sign(w23.y, v3.x));
+                            tsig += (xor_sign(w.x, v0.x) + xor_sign(w.y, v1.x)) + (xor_sign(w.z, v2.x) + xor_sign(w.w, v3.x));
                     } else {
                         sum = __fadd2_rn(sum, __fadd2_rn(__fadd2_rn(v0, v1), __fadd2_rn(v2, v3)));
                         if (MODE >= 1)
@@ -187,24 +207,18 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
                     }
                 };
                 if (UNIFORM) {
-                    if (NMODE == 2) { const uint4 e = sw[(size_t)t * W4C + k * a.C]; group(e.x, e.y, e.z, e.w); }
-                    else            { const uint2 e = su[(size_t)t * W4C + k * a.C]; group(e.x, e.y, 0, 0); }
+                    const int e = t * W4C + k * a.C;
+                    group(__ldcg(so + e), NMODE == 2 ? __ldcg(sw + e) : make_float4(0.f, 0.f, 0.f, 0.f));
                 } else {
                     bool last;
                     do {
-                        if (NMODE == 2) {
-                            const uint4 e = curw;
-                            pw += a.C;
-                            curw = *pw;
-                            last = (e.y >> 31) != 0;
-                            group(e.x, e.y, e.z, e.w);
-                        } else {
-                            const uint2 e = curu;
-                            pu += a.C;
-                            curu = *pu;
-                            last = (e.y >> 31) != 0;
-                            group(e.x, e.y, 0, 0);
-                        }
+                        const uint4 o = cur_o;
+                        const float4 w = cur_w;
+                        po += a.C;
+                        cur_o = *po;
+                        if (NMODE == 2) { pw += a.C; cur_w = *pw; }
+                        last = (int)o.w < 0;
+                        group(o, w);
                     } while (!last);
                 }
                 if (MODE >= 1) {
@@ -216,20 +230,40 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
                     const float acc = own.y * sum.x - own.x * sum.y;                 // dynamics.py:170
                     const float shil = NMODE == 2 ? own.y * own.x : own.y * (3.0f - 4.0f * own.y * own.y);
                     const float x = fmaf(a.hK, acc, fmaf(-hks, shil, fmaf(a.knsh, z[k], phi[t][k])));
-                    const float w = x - floorf(x);                                   // dynamics.py:172
-                    ynew[k] = (w >= 1.0f) ? 0.0f : w;
+                    ynew[k] = x;
                 }
             }
             if (MODE != 3) {
-                const float chk = (ynew[0] + ynew[1]) + (ynew[2] + ynew[3]);     // NaN iff some x was not finite
-                if (!(chk == chk) && live) {
+                // wrap (dynamics.py:172): one range check per quad; a huge or non-finite x takes floorf
+                const float big = fmaxf(fmaxf(fabsf(ynew[0]), fabsf(ynew[1])), fmaxf(fabsf(ynew[2]), fabsf(ynew[3])));
+                const float any = (ynew[0] + ynew[1]) + (ynew[2] + ynew[3]);     // NaN iff some x is NaN (fmaxf drops NaNs)
+                if (big < 4194304.0f && any == any) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (!(ynew[k] == ynew[k])) flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)rg, 4u * qid[t] + k);
+                    for (int k = 0; k < 4; ++k) {
+                        const float w = frac_alu(ynew[k]);
+                        ynew[k] = (w >= 1.0f) ? 0.0f : w;
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const float w = ynew[k] - floorf(ynew[k]);
+                        ynew[k] = (w >= 1.0f) ? 0.0f : w;
+                    }
                 }
+                const float chk = (ynew[0] + ynew[1]) + (ynew[2] + ynew[3]);     // NaN iff some x was not finite
+                bad = bad || !(chk == chk);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) phi[t][k] = ynew[k];
             }
+        }
+        if (MODE != 3 && bad && live) {
+            // a non-finite x leaves a NaN phase behind: name the first ones (dynamics.py:276-283)
+#pragma unroll
+            for (int t = 0; t < QPT; ++t)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (!(phi[t][k] == phi[t][k]) && quad(t) < (uint32_t)a.Q)
+                        flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)rg, 4u * quad(t) + k);
         }
         if (MODE >= 1) {
             // read-out of the state that was in shared memory during this pass
@@ -267,16 +301,16 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
                 // the pairs in shared memory still are the scored state: its lattice states -> best_states
 #pragma unroll
                 for (int t = 0; t < QPT; ++t) {
-                    if (qid[t] < (uint32_t)a.Q) {
-                        const float2 *own_p = cs_lane + (size_t)(pos0 + t * WC) * a.RT;
+                    const uint32_t q = quad(t);
+                    if (q < (uint32_t)a.Q) {
                         uint32_t packed = 0;
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            const uint32_t bits = __float_as_uint(own_p[(size_t)k * kstep].x);
+                            const uint32_t bits = __float_as_uint(reinterpret_cast<const float2 *>(smem_raw + own0 + t * tbytes + k * kbytes)->x);
                             const uint32_t st = NMODE == 2 ? (bits >> 31) : ((bits & 7u) >> 1);
                             packed |= st << (8 * k);
                         }
-                        *reinterpret_cast<uint32_t *>(a.best_states + (size_t)rg * a.n4 + 4u * qid[t]) = packed;
+                        *reinterpret_cast<uint32_t *>(a.best_states + (size_t)rg * a.n4 + 4u * q) = packed;
                     }
                 }
             }
@@ -289,7 +323,7 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
 
     // ---- time loop ---------------------------------------------------------------------------------
 #pragma unroll 1
-    for (long long step = a.step_begin; step < a.step_end; ++step) {
+    for (int step = a.step_begin; step < a.step_end; ++step) {
         const float hks = __ldg(a.hks_table + (step - a.step_begin));
         if (!pending) {
             pass_a(M0{}, step, hks);
@@ -304,7 +338,7 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
         __syncthreads();
         const bool is_sample = step == next_sample;
         const bool cadence_hit = a.cadence > 0 && cmod == 0;
-        cmod = (cmod + 1 == (int)a.cadence) ? 0 : cmod + 1;
+        cmod = (cmod + 1 == a.cadence) ? 0 : cmod + 1;
         if (is_sample) {
             pending = true;
             pending_col = 1 + sample_cur;
@@ -322,12 +356,14 @@ __global__ void __launch_bounds__(QPT > 5 ? 512 : 1024, 1) k_lowdeg(const Lowdeg
     if (tid < a.RT) a.best_obj[tile * a.RT + tid] = best_s[tid];
     if (live) {
 #pragma unroll
-        for (int t = 0; t < QPT; ++t)
+        for (int t = 0; t < QPT; ++t) {
+            const uint32_t q = quad(t);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const uint32_t i = 4u * qid[t] + k;
-                if (qid[t] < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)rg * a.n + i] = (double)phi[t][k];
+                const uint32_t i = 4u * q + k;
+                if (q < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)rg * a.n + i] = (double)phi[t][k];
             }
+        }
     }
 }
 

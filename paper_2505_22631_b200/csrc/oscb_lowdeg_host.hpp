@@ -1,0 +1,402 @@
+// oscb_lowdeg_host.hpp -- host side of k_lowdeg (oscb_lowdeg.cuh): which graphs it takes, the tile shape
+// (replicas per CTA, warps, items per thread), the component-major slot map + ELL neighbour stream, and the
+// launcher.  See the kernel header for the design.
+#pragma once
+#include "oscb_host.hpp"
+#include "oscb_lowdeg.cuh"
+#include "oscb_lowdeg.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <limits>
+#include <numeric>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+namespace oscb {
+
+struct LowdegShape {
+    int RT = 1, LRT = 0, C = 32, W = 1, QPT = 1, Q = 0, Qp = 0;
+    bool uniform = true;
+    size_t smem = 0;
+    double cost = 0.0;
+};
+
+// pure host result of the stream compiler (also exported to the CPU-side tests)
+struct LowdegStreamHost {
+    std::vector<uint32_t> quad_of;      // [Qp]
+    std::vector<uint32_t> slot_of;      // [n] slot of oscillator i (component-major)
+    std::vector<uint32_t> off;          // 4 per group entry: byte offset slot * RT * 8 (bit 31 of the 4th: last group of the row, looped form)
+    std::vector<float> wt;              // 4 per group entry: couplings (0 for padding)
+    std::vector<int> warp_start;        // looped form: first group row of each warp
+    int group_rows = 0;                 // group rows (of C entries) without the prefetch pad
+    int64_t real = 0;
+    std::vector<int64_t> warp_groups;   // group rows per warp (work balance)
+};
+
+struct LowdegPlan {
+    LowdegShape sh;
+    int nmode = 2;
+    double w_total = 0.0;
+    DevBuf<uint32_t> quad_of;
+    DevBuf<uint4> soff;
+    DevBuf<float4> swt;
+    DevBuf<int> warp_start;
+};
+
+static size_t lowdeg_smem_bytes(const LowdegShape &s, uint32_t *off_cnt, uint32_t *off_part, uint32_t *off_misc)
+{
+    size_t o = ((size_t)4 * s.Qp + OSCB_LD_PADS) * s.RT * 8;
+    auto take = [&](size_t bytes) { size_t at = o; o += (bytes + 15) & ~(size_t)15; return at; };
+    const size_t c = take((size_t)s.RT * 4), p = take((size_t)s.W * s.RT * 8), m = take((size_t)s.RT * 12 + 16);
+    if (off_cnt) *off_cnt = (uint32_t)c;
+    if (off_part) *off_part = (uint32_t)p;
+    if (off_misc) *off_misc = (uint32_t)m;
+    return o;
+}
+
+// Quads in the order their positions are dealt.  Uniform graphs keep the natural order (lattice-like graphs then
+// gather from neighbouring slots); otherwise quads are sorted by the group counts of their four rows so that
+// the C quads sharing a warp-instruction need the same number of groups, and the chunks of C are dealt to the
+// warps round-robin (the per-warp stream lengths stay within a few groups of each other).
+static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, const double *wts, const LowdegShape &s,
+                                  bool weighted_stream, LowdegStreamHost *out)
+{
+    const int Q = s.Q, Qp = s.Qp, C = s.C, W = s.W, QPT = s.QPT, RT = s.RT;
+    auto deg = [&](int i) { return i < n ? indptr[i + 1] - indptr[i] : 0; };
+    auto groups = [&](int i) { return std::max(1, (deg(i) + 3) / 4); };
+    std::vector<int> order(Q);
+    std::iota(order.begin(), order.end(), 0);
+    if (!s.uniform) {
+        std::vector<std::array<int, 4>> key(Q);
+        for (int q = 0; q < Q; ++q) key[q] = {groups(4 * q), groups(4 * q + 1), groups(4 * q + 2), groups(4 * q + 3)};
+        std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key[x] > key[y]; });
+    }
+    // chunk j of C quads -> warp-row (t, w)
+    out->quad_of.assign(Qp, 0xFFFFFFFFu);
+    const int chunks = (Q + C - 1) / C;
+    OSCB_REQUIRE(chunks <= W * QPT, "internal: lowdeg tile shape too small");
+    for (int j = 0; j < chunks; ++j) {
+        int t = j / W, w = j % W;
+        if (!s.uniform && (t & 1)) w = W - 1 - w;                       // boustrophedon: balance the sorted chunks
+        for (int c = 0; c < C && j * C + c < Q; ++c) out->quad_of[(size_t)(t * W + w) * C + c] = (uint32_t)order[j * C + c];
+    }
+    out->slot_of.assign(n, 0);
+    for (int pos = 0; pos < Qp; ++pos) {
+        const uint32_t q = out->quad_of[pos];
+        if (q >= (uint32_t)Q) continue;
+        for (int k = 0; k < 4; ++k)
+            if (4 * (int)q + k < n) out->slot_of[4 * q + k] = (uint32_t)(k * Qp + pos);
+    }
+    auto pad_off = [&](int c) { return (uint32_t)(((uint32_t)4 * Qp + (c % OSCB_LD_PADS)) * RT * 8); };
+    out->off.clear();
+    out->wt.clear();
+    out->real = 0;
+    out->warp_start.assign(W, 0);
+    out->warp_groups.assign(W, 0);
+    // one group entry of slot c: neighbours [4 g, 4 g + 4) of row i
+    auto emit = [&](int i, int g, int c, bool last) {
+        for (int u = 0; u < 4; ++u) {
+            const int e = (i >= 0 && i < n) ? indptr[i] + 4 * g + u : -1;
+            const bool real = e >= 0 && e < indptr[i + 1];
+            uint32_t o = real ? (uint32_t)(out->slot_of[indices[e]] * RT * 8) : pad_off(c);
+            if (u == 3 && last) o |= 0x80000000u;
+            out->off.push_back(o);
+            out->wt.push_back(real ? (wts ? (float)wts[e] : 1.0f) : 0.0f);
+            if (real) ++out->real;
+        }
+    };
+    auto row_of = [&](int t, int w, int c, int k) -> int {
+        const uint32_t q = out->quad_of[(size_t)(t * W + w) * C + c];
+        return q < (uint32_t)Q && 4 * (int)q + k < n ? 4 * (int)q + k : -1;
+    };
+    if (s.uniform) {
+        // [t][w][k][c], one group per row
+        for (int t = 0; t < QPT; ++t)
+            for (int w = 0; w < W; ++w)
+                for (int k = 0; k < 4; ++k)
+                    for (int c = 0; c < C; ++c) emit(row_of(t, w, c, k), 0, c, false);
+        out->group_rows = QPT * W * 4;
+        for (int w = 0; w < W; ++w) out->warp_groups[w] = (int64_t)QPT * 4;
+    } else {
+        // per warp: t, k, g in the order the kernel walks them
+        int rows = 0;
+        for (int w = 0; w < W; ++w) {
+            out->warp_start[w] = rows;
+            for (int t = 0; t < QPT; ++t)
+                for (int k = 0; k < 4; ++k) {
+                    int G = 1;
+                    for (int c = 0; c < C; ++c) {
+                        const int i = row_of(t, w, c, k);
+                        if (i >= 0) G = std::max(G, groups(i));
+                    }
+                    for (int g = 0; g < G; ++g) {
+                        for (int c = 0; c < C; ++c) emit(row_of(t, w, c, k), g, c, g == G - 1);
+                        ++rows;
+                    }
+                }
+            out->warp_groups[w] = rows - out->warp_start[w];
+        }
+        out->group_rows = rows;
+        for (int c = 0; c < C; ++c) emit(-1, 0, c, true);       // the prefetch pad row
+    }
+    (void)weighted_stream;
+}
+
+// is this run one for k_lowdeg at all?
+static bool lowdeg_kind(const oscb_graph *g, const oscb_run_params *p, int *nmode)
+{
+    if (g->is_dense || p->precision != OSCB_PREC_F32 || p->noise_mode == OSCB_NOISE_HOST || p->variant == 1) return false;
+    if (g->n < 4 || g->nnz == 0) return false;
+    if (p->n_states == 2 && p->objective == OSCB_OBJ_MAXCUT) {
+        if (!g->unit_weights) {
+            if (!g->int_weights) return false;
+            double tot = 0.0, mx = 0.0;
+            for (double w : g->h_w) { tot += std::fabs(w); mx = std::max(mx, std::fabs(w)); }
+            if (mx > 65536.0 || tot >= 8388608.0) return false;       // float32 / int32 sums of couplings stay exact
+        } else if ((double)g->nnz >= 8388608.0) return false;
+        *nmode = 2;
+        return true;
+    }
+    if (p->n_states == 3 && p->objective == OSCB_OBJ_COLORING && g->unit_weights) {
+        *nmode = 3;
+        return true;
+    }
+    return false;
+}
+
+static const int kLowdegQpt[] = {1, 2, 4, 5, 7, 10};
+
+// the tile shape with the lowest estimated time; false when the kernel does not apply
+static bool choose_lowdeg_shape(const oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced, LowdegShape *out)
+{
+    int nmode;
+    if (!lowdeg_kind(g, p, &nmode)) return false;
+    // low degree: the instruction count per row is what matters; k_resident_fast wins from ~degree 10 on
+    if (g->max_degree > 16) return false;
+    if (!forced && (double)g->nnz / (double)g->n > 8.0) return false;
+    const bool uniform = g->max_degree <= 4;
+    const int Q = (int)((g->n + 3) / 4);
+    double best = std::numeric_limits<double>::infinity();
+    bool found = false;
+    // OSCB_LOWDEG_RT / OSCB_LOWDEG_QPT pin the tile shape (tuning experiments)
+    int want_rt = p->replicas_per_cta, want_qpt = 0;
+    if (const char *e = getenv("OSCB_LOWDEG_RT")) { if (want_rt <= 0) want_rt = atoi(e); }
+    if (const char *e = getenv("OSCB_LOWDEG_QPT")) want_qpt = atoi(e);
+    for (int l = 5; l >= 0; --l) {
+        const int RT = 1 << l;
+        if (want_rt > 0 && RT != want_rt) continue;
+        if (want_rt <= 0 && RT > 1 && RT / 2 >= R) continue;      // do not pad a tile more than 2x
+        const int C = 32 / RT;
+        const int rows = (Q + C - 1) / C;
+        for (int QPT : kLowdegQpt) {
+            if (want_qpt > 0 && QPT != want_qpt) continue;
+            const int maxW = lowdeg_max_threads(QPT) / 32;
+            const int W = (rows + QPT - 1) / QPT;
+            if (W > maxW || W < 1) continue;
+            LowdegShape s;
+            s.RT = RT; s.LRT = l; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = uniform;
+            s.smem = lowdeg_smem_bytes(s, nullptr, nullptr, nullptr);
+            if (s.smem > (size_t)g->smem_optin) continue;
+            // work of one CTA in warp-rows (idle lanes and ghost items included), CTAs resident per SM, and the
+            // busiest SM's share of the tiles
+            const int64_t tiles = (R + RT - 1) / RT;
+            const int by_smem = (int)std::max<size_t>(1, ((size_t)g->smem_optin + 1024) / (s.smem + 1024));
+            const int by_threads = std::max(1, 2048 / (W * 32));
+            const int cps = std::min({by_smem, by_threads, 32});
+            const int64_t slots = (int64_t)g->sm_count * cps;
+            const int64_t waves = (tiles + slots - 1) / slots;
+            const int64_t per_sm = std::min<int64_t>(cps, (tiles + g->sm_count - 1) / g->sm_count);
+            double pad = 1.0;                                    // looped streams pad rows to the widest of C quads
+            if (!uniform) pad = 1.0 + 0.04 * (C - 1);
+            // few resident warps cannot hide the shared-memory and MUFU latencies
+            const double warps_resident = (double)per_sm * W;
+            const double occ = warps_resident >= 16 ? 1.0 : std::sqrt(16.0 / warps_resident);
+            s.cost = (double)waves * (double)per_sm * (double)W * QPT * pad * occ;
+            if (s.cost < best - 1e-9) { best = s.cost; *out = s; found = true; }
+        }
+    }
+    return found;
+}
+
+static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegShape &s, int nmode)
+{
+    const uint64_t key = (1ull << 63) | ((uint64_t)s.RT << 40) | ((uint64_t)s.W << 24) | ((uint64_t)s.QPT << 8) | (uint64_t)nmode;
+    auto it = g->lowdeg_plans.find(key);
+    if (it != g->lowdeg_plans.end()) return it->second;
+    auto plan = std::make_shared<LowdegPlan>();
+    plan->sh = s;
+    plan->nmode = nmode;
+    LowdegStreamHost h;
+    compile_lowdeg_stream((int)g->n, g->h_indptr.data(), g->h_indices.data(), g->unit_weights ? nullptr : g->h_w.data(), s,
+                          nmode == 2, &h);
+    OSCB_REQUIRE(h.real == g->nnz, "internal: lowdeg plan lost neighbours (%lld of %lld)", (long long)h.real, (long long)g->nnz);
+    double wt = 0.0;
+    for (int64_t e = 0; e < g->nnz; ++e) wt += g->unit_weights ? 1.0 : g->h_w[e];
+    plan->w_total = wt;
+    cudaStream_t st = g->stream;
+    plan->quad_of.alloc(h.quad_of.size());
+    plan->quad_of.upload(h.quad_of.data(), h.quad_of.size(), st);
+    const size_t entries = h.off.size() / 4;
+    plan->soff.alloc(entries);
+    plan->soff.upload(reinterpret_cast<const uint4 *>(h.off.data()), entries, st);
+    if (nmode == 2) {
+        plan->swt.alloc(entries);
+        plan->swt.upload(reinterpret_cast<const float4 *>(h.wt.data()), entries, st);
+    }
+    plan->warp_start.alloc(h.warp_start.size());
+    plan->warp_start.upload(h.warp_start.data(), h.warp_start.size(), st);
+    OSCB_CUDA(cudaStreamSynchronize(st));
+    g->lowdeg_plans[key] = plan;
+    return plan;
+}
+
+bool lowdeg_applies(const oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced)
+{
+    LowdegShape s;
+    return choose_lowdeg_shape(g, p, R, forced, &s);
+}
+
+template <int NMODE, bool UNIFORM, bool RT1>
+static void launch_lowdeg(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles)
+{
+    auto go = [&](auto kernel) {
+        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem));
+        kernel<<<tiles, s.W * 32, s.smem, g->stream>>>(a);
+    };
+    switch (s.QPT) {
+    case 1: go(k_lowdeg<NMODE, 1, UNIFORM, RT1>); break;
+    case 2: go(k_lowdeg<NMODE, 2, UNIFORM, RT1>); break;
+    case 4: go(k_lowdeg<NMODE, 4, UNIFORM, RT1>); break;
+    case 5: go(k_lowdeg<NMODE, 5, UNIFORM, RT1>); break;
+    case 7: go(k_lowdeg<NMODE, 7, UNIFORM, RT1>); break;
+    case 10: go(k_lowdeg<NMODE, 10, UNIFORM, RT1>); break;
+    default: OSCB_REQUIRE(false, "internal: no lowdeg instantiation for %d items per thread", s.QPT);
+    }
+}
+
+void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t cadence,
+                       const std::vector<long long> &sample_steps, const uint64_t *seeds, int64_t R64, const double *phi0,
+                       oscb_run_outputs *out)
+{
+    cudaStream_t s = g->stream;
+    const int n = (int)g->n, R = (int)R64;
+    LowdegShape sh;
+    int nmode = 2;
+    OSCB_REQUIRE(lowdeg_kind(g, p, &nmode) && choose_lowdeg_shape(g, p, R, true, &sh),
+                 "the low-degree kernel takes float32, device noise, max degree <= 16 and N = 2 max-cut on integer couplings "
+                 "or N = 3 colouring on unit couplings");
+    auto plan = get_lowdeg_plan(g, sh, nmode);
+    const int RT = sh.RT, tiles = (R + RT - 1) / RT, R_pad = tiles * RT, n4 = 4 * sh.Q;
+    const int maximize = p->objective == OSCB_OBJ_MAXCUT;
+    const int64_t S = 1 + (int64_t)sample_steps.size();
+    const size_t tot = (size_t)n * R;
+
+    DevBuf<double> d_io(tot);
+    std::vector<uint64_t> h_seeds(R_pad, 0);
+    std::copy(seeds, seeds + R, h_seeds.begin());
+    DevBuf<uint64_t> d_seeds(R_pad);
+    d_seeds.upload(h_seeds.data(), R_pad, s);
+    DevBuf<double> d_best(R_pad), d_energy((size_t)R_pad * S), d_btrace((size_t)R_pad * S);
+    DevBuf<uint8_t> d_best_states((size_t)R_pad * n4);
+    DevBuf<long long> d_first(R_pad);
+    DevBuf<int> d_samples(std::max<size_t>(1, sample_steps.size()));
+    std::vector<double> h_best(R_pad, maximize ? -std::numeric_limits<double>::infinity() : std::numeric_limits<double>::infinity());
+    std::vector<long long> h_first(R_pad, -1);
+    std::vector<int> h_samples(sample_steps.begin(), sample_steps.end());
+    for (auto &v : h_samples) v += (int)p->first_step;
+    d_best.upload(h_best.data(), R_pad, s);
+    d_first.upload(h_first.data(), R_pad, s);
+    d_samples.upload(h_samples.data(), h_samples.size(), s);
+    d_best_states.zero(s);
+    const unsigned long long none = ~0ull;
+    OSCB_CUDA(cudaMemcpyAsync(g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    if (phi0) d_io.upload(phi0, tot, s);
+    else launch_initial_phases(d_seeds.p, d_io.p, n, R, s);
+
+    // h * ks(step) (x2 for N = 2, where the SHIL term is 2 s c) for every step, in the reference's float64
+    std::vector<float> hks((size_t)steps + 1);
+    const double scale = p->h * (p->n_states == 2 ? 2.0 : 1.0);
+    for (int64_t k = 0; k <= steps; ++k)
+        hks[(size_t)k] = (float)(scale * ks_value(p->ks_max, p->ks_period, (double)(p->first_step + k) * p->h));
+    DevBuf<float> d_hks(hks.size());
+    d_hks.upload(hks.data(), hks.size(), s);
+
+    LowdegArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = n; a.Q = sh.Q; a.Qp = sh.Qp; a.RT = RT; a.LRT = sh.LRT; a.C = sh.C; a.W = sh.W; a.R_real = R; a.n4 = n4;
+    lowdeg_smem_bytes(sh, &a.off_cnt, &a.off_part, &a.off_misc);
+    a.hK = (float)(p->h * p->K);
+    a.knsh = (float)(p->kn * std::sqrt(p->h));
+    a.noise_on = (p->noise_mode == OSCB_NOISE_DEVICE && p->kn != 0.0) ? 1 : 0;
+    a.maximize = maximize; a.use_target = p->use_target; a.n_sample_steps = (int)sample_steps.size();
+    a.step_begin = (int)p->first_step; a.step_end = (int)(p->first_step + steps); a.cadence = (int)cadence; a.trace_stride = S;
+    a.target = p->target_objective; a.w_total = plan->w_total;
+    a.quad_of = plan->quad_of.p; a.soff = plan->soff.p; a.swt = plan->swt.p; a.warp_start = plan->warp_start.p;
+    a.hks_table = d_hks.p; a.seeds = d_seeds.p; a.sample_steps = d_samples.p;
+    if (nmode == 3) fast_state_boundaries(3, a.bnd);
+    a.io = d_io.p; a.best_obj = d_best.p; a.energy = d_energy.p; a.best_trace = d_btrace.p; a.best_states = d_best_states.p;
+    a.first_hit = d_first.p; a.nonfinite = g->d_nonfinite.p;
+
+    cudaEvent_t ev0, ev1;
+    OSCB_CUDA(cudaEventCreate(&ev0));
+    OSCB_CUDA(cudaEventCreate(&ev1));
+    OSCB_CUDA(cudaStreamSynchronize(s));        // the host staging vectors above must outlive their copies
+    OSCB_CUDA(cudaEventRecord(ev0, s));
+    auto by_shape = [&](auto nm) {
+        constexpr int NM = decltype(nm)::value;
+        if (sh.uniform && RT == 1) launch_lowdeg<NM, true, true>(g, a, sh, tiles);       // (RT1 only with the straight-line stream)
+        else if (sh.uniform) launch_lowdeg<NM, true, false>(g, a, sh, tiles);
+        else launch_lowdeg<NM, false, false>(g, a, sh, tiles);
+    };
+    if (nmode == 2) by_shape(std::integral_constant<int, 2>{}); else by_shape(std::integral_constant<int, 3>{});
+    OSCB_CUDA(cudaEventRecord(ev1, s));
+    {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            set_error("oscb_run(lowdeg): kernel launch failed: %s (tiles %d, threads %d, smem %zu)", cudaGetErrorString(e), tiles,
+                      sh.W * 32, sh.smem);
+            throw OscbFail{OSCB_ECUDA};
+        }
+    }
+    if (out->final_phases) d_io.download(out->final_phases, tot, s);
+    if (out->best_states)
+        OSCB_CUDA(cudaMemcpy2DAsync(out->best_states, (size_t)n, d_best_states.p, (size_t)n4, (size_t)n, (size_t)R,
+                                    cudaMemcpyDeviceToHost, s));
+    if (out->best_objective) d_best.download(out->best_objective, R, s);
+    std::vector<double> h_energy, h_btrace;
+    if (out->energy) { h_energy.resize((size_t)R * S); d_energy.download(h_energy.data(), h_energy.size(), s); }
+    if (out->best_trace) { h_btrace.resize((size_t)R * S); d_btrace.download(h_btrace.data(), h_btrace.size(), s); }
+    if (out->first_hit_step) d_first.download(h_first.data(), R, s);
+    unsigned long long flag = none;
+    OSCB_CUDA(cudaMemcpyAsync(&flag, g->d_nonfinite.p, sizeof(flag), cudaMemcpyDeviceToHost, s));
+    OSCB_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    OSCB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    for (int r = 0; r < R; ++r)
+        for (int64_t k = 0; k < S; ++k) {
+            if (out->energy) out->energy[(size_t)r * out->max_samples + k] = h_energy[(size_t)r * S + k];
+            if (out->best_trace) out->best_trace[(size_t)r * out->max_samples + k] = h_btrace[(size_t)r * S + k];
+        }
+    if (out->first_hit_step)
+        for (int r = 0; r < R; ++r) out->first_hit_step[r] = h_first[r];
+    out->device_ms = ms;
+    out->kernel_launches = 1;
+    out->kernel_used = OSCB_KERNEL_LOWDEG;
+    out->replicas_per_cta = RT;
+    out->smem_bytes = (int64_t)sh.smem;
+    if (flag != none) {
+        out->nonfinite[2] = (int64_t)(flag >> 36);
+        out->nonfinite[0] = (int64_t)((flag >> 20) & 0xFFFFull);
+        out->nonfinite[1] = (int64_t)(flag & 0xFFFFFull);
+        set_error("non-finite phase for oscillator %lld (replica row %lld) after step %lld; parameters are numerically unstable",
+                  (long long)out->nonfinite[1], (long long)out->nonfinite[0], (long long)out->nonfinite[2]);
+        throw OscbFail{OSCB_ENONFINITE};
+    }
+}
+
+} // namespace oscb

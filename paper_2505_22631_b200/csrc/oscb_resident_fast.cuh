@@ -29,6 +29,7 @@
 //   x   = phi + hK acc - h ks shil + kn sqrt(h) xi ;  phi' = x - floor(x)           (dynamics.py:171-172)
 #pragma once
 #include "oscb_resident.cuh"
+#include "oscb_fastmath.cuh"
 #include <string.h>
 
 namespace oscb {
@@ -64,61 +65,6 @@ __device__ __forceinline__ float4 lds_f4(uint32_t addr)
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
     return v;
-}
-
-// four standard normals from one Philox block, MUFU Box-Muller (same draw -> same normal as
-// normals4(float) up to ~1e-6)
-__device__ __forceinline__ void normals4_fast(uint4 x, float &z0, float &z1, float &z2, float &z3)
-{
-    const float inv32 = 2.3283064365386963e-10f;
-    const float u0 = fminf(fmaf((float)x.x, inv32, 0.5f * inv32), 1.0f);
-    const float u1 = fminf(fmaf((float)x.z, inv32, 0.5f * inv32), 1.0f);
-    float r0, r1;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(-1.3862943611198906f * __log2f(u0)));
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(-1.3862943611198906f * __log2f(u1)));
-    // angle 2 pi v, v in [0, 1): fold to [-pi, pi) first, where the MUFU approximations are tightest
-    const float v0 = (float)x.y * inv32, v1 = (float)x.w * inv32;
-    const float a0 = 6.283185307179586f * (v0 - (v0 >= 0.5f ? 1.0f : 0.0f));
-    const float a1 = 6.283185307179586f * (v1 - (v1 >= 0.5f ? 1.0f : 0.0f));
-    z0 = r0 * __cosf(a0); z1 = r0 * __sinf(a0);
-    z2 = r1 * __cosf(a1); z3 = r1 * __sinf(a1);
-}
-
-// (sin, cos) of 2 pi y for a phase y in [0, 1), in ~17 instructions instead of sincospif's ~32:
-// exact reduction to a quarter turn (4y - rint(4y) is exact), the two MUFU approximations on
-// |angle| <= pi/4 (abs. error ~4e-7, about the rounding of float32 near 1), quadrant fix-up by
-// swap / sign flips.  The SIGN BIT of the cosine is then set from the exact comparison
-// 0.25 < y < 0.75, i.e. it IS the N = 2 lattice state of the reference (dynamics.py:203-213; ties
-// at 0.25 / 0.75 -> state 0), also when the approximate magnitude underflows to zero: -0 carries
-// state 1.  Consumers read the state from the bit, never from "c < 0".
-__device__ __forceinline__ void trig_turns_fast(float y, float &s, float &c)
-{
-    const float t = 4.0f * y;
-    const float qf = rintf(t);
-    const float ang = (t - qf) * 1.5707963267948966f;
-    const float sr = __sinf(ang), cr = __cosf(ang);
-    const int qi = (int)qf;
-    const bool odd = qi & 1;
-    const float s0 = odd ? cr : sr, c0 = odd ? sr : cr;
-    s = __uint_as_float(__float_as_uint(s0) ^ ((uint32_t)(qi & 2) << 30));
-    const uint32_t state = (y > 0.25f && y < 0.75f) ? 0x80000000u : 0u;
-    c = __uint_as_float((__float_as_uint(c0) & 0x7FFFFFFFu) | state);
-}
-
-// Lattice state of a float32 phase for any N (dynamics.py:203-213): the reference rule is a step
-// function of the phase, so it is evaluated as "how many decision boundaries lie at or below p";
-// the boundaries are found on the host by bisection over float32 with the reference's own float64
-// expression (fast_state_boundaries), and oscb_selftest_sign_state checks the table against the
-// float64 rule for every float32 in [0, 1).
-__device__ __forceinline__ uint32_t state_from_boundaries(float p, const float *bnd, int n)
-{
-    if (n == 3) {      // the 3-colouring case, without the loop
-        const uint32_t st3 = (p >= bnd[0] ? 1u : 0u) + (p >= bnd[1] ? 1u : 0u) + (p >= bnd[2] ? 1u : 0u);
-        return st3 == 3u ? 0u : st3;
-    }
-    uint32_t st = 0;
-    for (int k = 0; k < n; ++k) st += (p >= bnd[k]) ? 1u : 0u;
-    return st == (uint32_t)n ? 0u : st;
 }
 
 // Everything the kernel needs, precomputed on the host so that the hot loops read constants
@@ -172,6 +118,10 @@ __global__ void k_selftest_sign_state(unsigned long long *mismatches)
         float s_ref, c_ref;
         sincospif(2.0f * p, &s_ref, &c_ref);
         if (!(fabsf(s - s_ref) <= 2e-6f && fabsf(co - c_ref) <= 2e-6f)) ++bad;
+        // the direct form (k_lowdeg): same state bit, same error bound
+        trig_turns_direct(p, s, co);
+        if ((__float_as_uint(co) >> 31) != (uint32_t)threshold_state((double)p, 2)) ++bad;
+        if (!(fabsf(s - s_ref) <= 2e-6f && fabsf(co - c_ref) <= 2e-6f)) ++bad;
     }
     if (bad) atomicAdd(mismatches, bad);
 }
@@ -188,30 +138,6 @@ __global__ void k_selftest_boundaries(int n_states, FastArgs a, unsigned long lo
         if (state_from_boundaries(p, a.bnd, a.n_bnd) != (uint32_t)threshold_state((double)p, n_states)) ++bad;
     }
     if (bad) atomicAdd(mismatches, bad);
-}
-
-// Decision boundaries of the reference threshold rule on float32 phases: bnd[k] = the smallest
-// float32 in [k/N, (k+1)/N] whose state is (k + 1) % N.  Inside that interval the state is k below
-// the boundary and (k + 1) % N from it on (both distances are monotone in p), so a
-// bisection over the float32 bit patterns with the float64 rule itself finds it exactly.
-inline void fast_state_boundaries(int n_states, float *bnd)
-{
-    for (int k = 0; k < n_states; ++k) {
-        uint32_t lo, hi;                 // state(lo) == k, state(hi) == (k + 1) % N
-        float flo = (float)((double)k / n_states), fhi = k + 1 == n_states ? 0.99999994f : (float)((double)(k + 1) / n_states);
-        memcpy(&lo, &flo, 4);
-        memcpy(&hi, &fhi, 4);
-        const int next = (k + 1) % n_states;
-        // make sure the bracket ends are on the right sides (float rounding of k/N can land either way)
-        auto st = [&](uint32_t bits) { float f; memcpy(&f, &bits, 4); return threshold_state((double)f, n_states); };
-        while (st(lo) != k) --lo;
-        while (st(hi) != next) hi = hi + 1 < 0x3F800000u ? hi + 1 : hi - 2;   // (the last interval ends below 1.0)
-        while (hi - lo > 1) {
-            const uint32_t mid = lo + (hi - lo) / 2;
-            if (st(mid) == k) lo = mid; else hi = mid;
-        }
-        memcpy(&bnd[k], &hi, 4);
-    }
 }
 
 // shared-memory layout of the float32 kernel; filled into FastArgs by the host
