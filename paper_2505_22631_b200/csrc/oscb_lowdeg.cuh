@@ -170,6 +170,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
         bool bad = false;
         const uint4 *po = so;
         const float4 *pw = sw;
+        const int stride = a.C;
         uint4 cur_o = make_uint4(0, 0, 0, 0);
         float4 cur_w = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!UNIFORM) {
@@ -211,13 +212,16 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
                     group(__ldcg(so + e), NMODE == 2 ? __ldcg(sw + e) : make_float4(0.f, 0.f, 0.f, 0.f));
                 } else {
                     bool last;
+#pragma unroll 2
                     do {
                         const uint4 o = cur_o;
                         const float4 w = cur_w;
-                        po += a.C;
+                        po += stride;
                         cur_o = *po;
-                        if (NMODE == 2) { pw += a.C; cur_w = *pw; }
-                        last = (int)o.w < 0;
+                        if (NMODE == 2) { pw += stride; cur_w = *pw; }
+                        // (the flag is the same in all lanes: the vote tells the compiler so -- a uniform branch, no
+                        // reconvergence bookkeeping around every row)
+                        last = __any_sync(0xffffffffu, (int)o.w < 0);
                         group(o, w);
                     } while (!last);
                 }
