@@ -89,7 +89,9 @@ typedef struct oscb_run_params {
     double target_objective;
     int64_t first_step;                         /* global index of the first step (restart)   */
     int32_t replicas_per_cta;                   /* 0 auto; resident kernel tile width         */
-    int32_t variant;                            /* 0 auto; 1 = generic resident kernel even where the specialised float32 one applies */
+    int32_t variant;                            /* 0 auto; 1 = generic resident kernel even where the specialised float32 one applies;
+                                                   dense tensor-core runs: 8 = stream J as int8, 4 = as packed e2m1 (the ranks of a
+                                                   row-sharded run must all pass the same value -- connect checks it)            */
 } oscb_run_params;
 
 typedef struct oscb_run_outputs {
@@ -123,6 +125,11 @@ int oscb_pool_trim(void);
 
 int oscb_graph_create_csr(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
                           const double *data, oscb_graph **out);
+/* Dense couplings.  Integer couplings |J| <= 127 on 128-row aligned shards also get the tile images of the
+ * tensor-core kernel (OSCB_KERNEL_DENSE_TC), whose sums are exact integers while the accumulators hold them: the
+ * int8 stream needs max_i sum_j |J_ij| * 128 < 2^31, the packed e2m1 stream (every coupling in {0, +-1, +-2, +-3,
+ * +-4, +-6}) max_i sum_j |J_ij| * 4 < 2^24.  A graph that breaks a bound is kept off that stream (it then runs on
+ * the SIMT dense kernels), never rounded silently. */
 int oscb_graph_create_dense(int device, int64_t n, const double *J, int64_t row_begin,
                             int64_t row_end, oscb_graph **out);
 int oscb_graph_destroy(oscb_graph *g);

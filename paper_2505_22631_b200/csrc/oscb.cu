@@ -567,6 +567,7 @@ static UmmaSpec umma_spec(const oscb_run_params *p, const RunPlan &rp, const Umm
     sp.flags = sc.flags.data();
     sp.n_events = (long long)sc.event_step.size();
     sp.n_samples = rp.n_samples;
+    sp.force_stream = (p->variant == 8 || p->variant == 4) ? p->variant : 0;
     return sp;
 }
 
@@ -825,7 +826,7 @@ int oscb_graph_create_dense(int device, int64_t n, const double *J, int64_t row_
         // J holds rows [row_begin, row_end) of the full matrix, row-major, n columns each
         build_dense(g.get(), J);
         // integer couplings on 128-row aligned shards also get the tile images of the tensor-core kernel
-        if (g->dense->kind == DENSE_I8 && row_begin % 128 == 0 && (row_end % 128 == 0 || row_end == n))
+        if (g->dense->kind == DENSE_I8 && g->dense->tc_exact && row_begin % 128 == 0 && (row_end % 128 == 0 || row_end == n))
             g->umma = umma_build_plan(g->dense->J8.p, n, g->dense->n_pad, row_begin, row_end, g->dense->fp4_ok, g->stream);
         *out = g.release();
         return OSCB_OK;
@@ -1051,8 +1052,9 @@ int oscb_dense_fused_create(oscb_graph *shard, const oscb_run_params *p, int64_t
         OSCB_REQUIRE(p->kernel == OSCB_KERNEL_AUTO || p->kernel == OSCB_KERNEL_DENSE_TC, "fused dense runs use the tensor-core kernel");
         OSCB_REQUIRE(umma_applies(shard, p), "fused dense runs are N = 2 max-cut (integer couplings) or N-state colouring (unit couplings), device noise");
         OSCB_REQUIRE(p->precision == OSCB_PREC_F32 || p->precision == OSCB_PREC_F64, "unknown precision %d", p->precision);
-        OSCB_REQUIRE(R >= 1 && R <= umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R, p->n_states)), "fused dense runs take 1..%d replicas per session",
-                     umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R, p->n_states)));
+        const int force = (p->variant == 8 || p->variant == 4) ? p->variant : 0;
+        OSCB_REQUIRE(R >= 1 && R <= umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R, p->n_states, force)), "fused dense runs take 1..%d replicas per session",
+                     umma_max_replicas(p->n_states, umma_uses_fp4(*shard->umma, (int)R, p->n_states, force)));
         OSCB_REQUIRE(p->h > 0.0 && std::isfinite(p->h) && p->ks_period > 0.0, "bad h / ks_period");
         OSCB_REQUIRE(p->steps > 0 || (p->t_stop > 0.0 && std::isfinite(p->t_stop)), "t_stop must be finite and > 0");
         bind_device(shard);

@@ -15,7 +15,7 @@
 //     neighbour's lattice state, see oscb_resident_fast.cuh); the per-CTA partial cuts are
 //     exchanged through DSMEM on the same barrier, and every CTA keeps the same best-so-far.
 //
-// Same arithmetic as k_resident_fast (float32, trig_turns_fast, normals4_fast, the same
+// Same arithmetic as k_resident_fast (float32, trig_turns_direct, normals4_fast, the same
 // (seed, step, oscillator) noise); the summation order over a row differs, so the two agree to
 // rounding, like any two float32 tile shapes.
 #pragma once
@@ -119,7 +119,7 @@ __global__ void __cluster_dims__(CL_SIZE, 1, 1) __launch_bounds__(1024, 1) k_clu
         const double *src = a.phi_io + (size_t)(live ? replica : 0) * a.n;
         for (int i = tid; i < a.n_al; i += NT) {
             float s = 0.f, c = 0.f;
-            if (i < a.n) trig_turns_fast((float)src[i], s, c);
+            if (i < a.n) trig_turns_direct((float)src[i], s, c);
             cs[i] = make_float2(c, s);
             cs[a.n_al + i] = make_float2(0.f, 0.f);
         }
@@ -327,7 +327,7 @@ __global__ void __cluster_dims__(CL_SIZE, 1, 1) __launch_bounds__(1024, 1) k_clu
                 if (!(fabsf(x) < INFINITY) && live) flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)replica, (uint32_t)i);
                 phi_s[rl] = y;
                 float s2, c2;
-                trig_turns_fast(y, s2, c2);
+                trig_turns_direct(y, s2, c2);
                 const float2 np = make_float2(c2, s2);
 #pragma unroll
                 for (int r = 0; r < CL_SIZE; ++r) cluster.map_shared_rank(nxt, r)[i] = np;   // DSMEM: the next buffer of every CTA

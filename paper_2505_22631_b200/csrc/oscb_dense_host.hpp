@@ -13,6 +13,8 @@ enum DenseKind { DENSE_I8 = 0, DENSE_F = 1 };
 struct DensePlan {
     int kind = DENSE_F;
     int n_pad = 0;
+    double max_abs_rowsum = 0.0; // max_i sum_j |J_ij| over the handle's rows
+    bool tc_exact = false;       // int32 accumulation of the int8 digit-plane GEMM cannot overflow
     bool fp4_ok = false;         // every coupling of the shard's rows is in {0, +-1, +-2, +-3, +-4, +-6} (e2m1 values)
     DevBuf<int8_t> J8;
     DevBuf<float> J32;
@@ -26,14 +28,17 @@ static void build_dense(oscb_graph *g, const double *J)
     const int n_pad = (int)((n + 3) / 4 * 4);
     bool unit = true, integral = true, small = true, fp4 = true;
     int64_t nnz = 0, pairs = 0, maxdeg = 0;
+    double max_abs_rowsum = 0.0;
     for (int64_t q = 0; q < rows; ++q) {
         const int64_t i = g->row_begin + q;
         int64_t d = 0;
+        double abs_row = 0.0;
         for (int64_t j = 0; j < n; ++j) {
             const double v = J[q * n + j];
             OSCB_REQUIRE(std::isfinite(v), "non-finite coupling at (%lld, %lld)", (long long)i, (long long)j);
             OSCB_REQUIRE(i != j || v == 0.0, "coupling diagonal must be zero");
             { const double m = std::fabs(v); if (!(m == 0.0 || m == 1.0 || m == 2.0 || m == 3.0 || m == 4.0 || m == 6.0)) fp4 = false; }
+            abs_row += std::fabs(v);
             if (v != 0.0) {
                 ++d;
                 if (j > i) ++pairs;
@@ -44,6 +49,7 @@ static void build_dense(oscb_graph *g, const double *J)
         }
         nnz += d;
         maxdeg = std::max(maxdeg, d);
+        max_abs_rowsum = std::max(max_abs_rowsum, abs_row);
     }
     g->nnz = nnz;
     g->pairs = pairs;
@@ -52,7 +58,13 @@ static void build_dense(oscb_graph *g, const double *J)
     g->int_weights = integral;
     auto plan = std::make_shared<DensePlan>();
     plan->n_pad = n_pad;
-    plan->fp4_ok = fp4;
+    // The tensor-core kernel's sums are EXACT integers only while the accumulators hold them: the int8 stream adds
+    // products |J * digit| <= 128 |J| into int32, the e2m1 stream products <= 4 |J| into float32 (exact below 2^24).
+    // A row whose |J| sum breaks the bound keeps the graph off that stream (n < ~131k at |J| = 127, n < ~1M at |J| = 1
+    // for int8; n < ~4.2M at |J| = 1 for e2m1) and the run falls back to the SIMT dense path.
+    plan->max_abs_rowsum = max_abs_rowsum;
+    plan->tc_exact = max_abs_rowsum * 128.0 < 2147483648.0;
+    plan->fp4_ok = fp4 && max_abs_rowsum * 4.0 < 16777216.0;
     cudaStream_t s = g->stream;
     const size_t elems = (size_t)rows * n_pad;
     if (integral && small) {

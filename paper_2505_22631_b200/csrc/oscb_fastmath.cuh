@@ -1,5 +1,5 @@
 // oscb_fastmath.cuh -- float32 building blocks shared by the persistent throughput kernels (k_resident_fast,
-// k_lowdeg): MUFU Box-Muller, the quarter-turn trig with the N = 2 lattice state in the cosine's sign bit, and
+// k_lowdeg, k_cluster_fast): MUFU Box-Muller, the MUFU trig with the N = 2 lattice state in the cosine's sign bit, and
 // the reference threshold rule as a table of float32 decision boundaries.
 #pragma once
 #include "oscb_device.cuh"
@@ -24,32 +24,15 @@ __device__ __forceinline__ void normals4_fast(uint4 x, float &z0, float &z1, flo
     z2 = r1 * __cosf(a1); z3 = r1 * __sinf(a1);
 }
 
-// (sin, cos) of 2 pi y for a phase y in [0, 1), in ~17 instructions instead of sincospif's ~32:
-// exact reduction to a quarter turn (4y - rint(4y) is exact), the two MUFU approximations on
-// |angle| <= pi/4 (abs. error ~4e-7, about the rounding of float32 near 1), quadrant fix-up by
-// swap / sign flips.  The SIGN BIT of the cosine is then set from the exact comparison
-// 0.25 < y < 0.75, i.e. it IS the N = 2 lattice state of the reference (dynamics.py:203-213; ties
-// at 0.25 / 0.75 -> state 0), also when the approximate magnitude underflows to zero: -0 carries
-// state 1.  Consumers read the state from the bit, never from "c < 0".
-__device__ __forceinline__ void trig_turns_fast(float y, float &s, float &c)
-{
-    const float t = 4.0f * y;
-    const float qf = rintf(t);
-    const float ang = (t - qf) * 1.5707963267948966f;
-    const float sr = __sinf(ang), cr = __cosf(ang);
-    const int qi = (int)qf;
-    const bool odd = qi & 1;
-    const float s0 = odd ? cr : sr, c0 = odd ? sr : cr;
-    s = __uint_as_float(__float_as_uint(s0) ^ ((uint32_t)(qi & 2) << 30));
-    const uint32_t state = (y > 0.25f && y < 0.75f) ? 0x80000000u : 0u;
-    c = __uint_as_float((__float_as_uint(c0) & 0x7FFFFFFFu) | state);
-}
-
-// The same pair without the quarter-turn reduction: u = y - rint(y) (y in [0, 1)) is exact and lies in [-1/2, 1/2], so the angle
-// 2 pi u is inside [-pi, pi], the interval on which the MUFU sine and cosine are specified (abs. error 2^-21.4 and
-// 2^-21.2, i.e. the same ~4e-7 the quarter-turn form reaches) -- 11 instructions instead of ~20.  The cosine's sign bit
-// is again forced from the exact comparison 0.25 < y < 0.75, written as |y - 1/2| < 1/4 (y - 1/2 is exact on
-// [1/4, 1) and can only round towards -1/4 below it).  oscb_selftest_sign_state checks both over every float32.
+// (sin, cos) of 2 pi y for a phase y in [0, 1), in ~11 instructions instead of sincospif's ~32: u = y - rint(y) is
+// exact and lies in [-1/2, 1/2], so the angle 2 pi u is inside [-pi, pi], the interval on which the MUFU sine and
+// cosine are specified (abs. error 2^-21.4 and 2^-21.2, ~4e-7: about the rounding of float32 near 1).  (Round 1 reduced
+// to a quarter turn first and fixed the quadrant up afterwards: ~20 instructions for the same error bound.)
+// The SIGN BIT of the cosine is then set from the exact comparison 0.25 < y < 0.75, written as |y - 1/2| < 1/4
+// (y - 1/2 is exact on [1/4, 1) and can only round towards -1/4 below it), i.e. it IS the N = 2 lattice state of
+// the reference (dynamics.py:203-213; ties at 0.25 / 0.75 -> state 0), also when the approximate magnitude
+// underflows to zero: -0 carries state 1.  Consumers read the state from the bit, never from "c < 0".
+// oscb_selftest_sign_state checks bit and values over every float32 in [0, 1).
 __device__ __forceinline__ void trig_turns_direct(float y, float &s, float &c)
 {
     const float a = 6.283185307179586f * (y - (y > 0.5f ? 1.0f : 0.0f));      // y - rint(y), on the ALU

@@ -12,7 +12,7 @@
 //   * N = 2 (OIM / max-cut, NMODE == 2): the SHIL harmonic is 2 s c, and scoring costs one
 //     LEA.HI per gather on the step AFTER a scored step: with c_j = cospi(2 phi_j) already in
 //     a register, its SIGN BIT is the lattice state of j (0.25 < phi < 0.75, dynamics.py:203-213;
-//     trig_turns_fast sets the bit from that exact comparison, and oscb_selftest_sign_state checks
+//     trig_turns_direct sets the bit from that exact comparison, and oscb_selftest_sign_state checks
 //     it over every float in [0, 1)).  A row contributes deg - neg or neg differing neighbours depending on its own
 //     state; the tile sum is twice the cut.  Trace samples and the first/last state still go
 //     through the explicit scoring pass;
@@ -111,16 +111,12 @@ __global__ void k_selftest_sign_state(unsigned long long *mismatches)
          q += (unsigned long long)gridDim.x * blockDim.x) {
         const float p = __uint_as_float((uint32_t)q);
         float s, co;
-        trig_turns_fast(p, s, co);
+        trig_turns_direct(p, s, co);
         const uint32_t by_sign = __float_as_uint(co) >> 31;
         if (by_sign != (uint32_t)threshold_state((double)p, 2)) ++bad;
         // and the values themselves stay within the MUFU error of the exact ones
         float s_ref, c_ref;
         sincospif(2.0f * p, &s_ref, &c_ref);
-        if (!(fabsf(s - s_ref) <= 2e-6f && fabsf(co - c_ref) <= 2e-6f)) ++bad;
-        // the direct form (k_lowdeg): same state bit, same error bound
-        trig_turns_direct(p, s, co);
-        if ((__float_as_uint(co) >> 31) != (uint32_t)threshold_state((double)p, 2)) ++bad;
         if (!(fabsf(s - s_ref) <= 2e-6f && fabsf(co - c_ref) <= 2e-6f)) ++bad;
     }
     if (bad) atomicAdd(mismatches, bad);
@@ -281,7 +277,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
         for (int i = tid; i < a.nRT; i += NT) {
             const float p = slab[i];
             float s, co;
-            trig_turns_fast(p, s, co);
+            trig_turns_direct(p, s, co);
             cs[i] = make_float2(co, s);
             if (PHI_SMEM) phis[i] = p;
         }
@@ -628,7 +624,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     float s2[RPL], c2[RPL];
 #pragma unroll
                     for (int e = 0; e < RPL; ++e) {
-                        trig_turns_fast(y[e], s2[e], c2[e]);
+                        trig_turns_direct(y[e], s2[e], c2[e]);
                     }
                     if (RPL == 2) *reinterpret_cast<float4 *>(stage_g + iRT) = make_float4(c2[0], s2[0], c2[RPL - 1], s2[RPL - 1]);
                     else stage_g[iRT] = make_float2(c2[0], s2[0]);
@@ -676,7 +672,7 @@ __global__ void __launch_bounds__(1024, 1) k_resident_fast(const FastArgs a)
                     float s[RPL], co[RPL];
 #pragma unroll
                     for (int e = 0; e < RPL; ++e) {
-                        trig_turns_fast(p[e], s[e], co[e]);
+                        trig_turns_direct(p[e], s[e], co[e]);
                     }
                     if (RPL == 2)
                         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(pair_addr<3>(iRT, cs32)), "f"(co[0]), "f"(s[0]),

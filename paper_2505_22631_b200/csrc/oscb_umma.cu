@@ -46,8 +46,15 @@ static inline size_t round256(size_t x) { return (x + 255) & ~(size_t)255; }
 // A side: 24.5 us per Euler step of SK 16384 at R = 1 against 41.8 us for the HBM-bound int8 stream.  It needs 21 B
 // columns per replica instead of 9, so a launch takes at most 12 replicas; up to there it is ahead (R = 12: 44.6 vs 47.3 us).
 // OSCB_UMMA_FP4 = 0 / 1 forces the choice.
-bool umma_uses_fp4(const UmmaPlan &plan, int R, int n_states)
+bool umma_uses_fp4(const UmmaPlan &plan, int R, int n_states, int force_stream)
 {
+    // a row-sharded run agrees on ONE stream for all ranks (every rank writes digits into every peer's B image, so
+    // the layouts must match): the caller passes the agreed choice and the process-local environment is not consulted
+    if (force_stream == 8) return false;
+    if (force_stream == 4) {
+        OSCB_REQUIRE(plan.fp4_ok && R <= umma_max_replicas(n_states, true), "the packed e2m1 stream was requested but this shard / replica count cannot take it");
+        return true;
+    }
     if (!plan.fp4_ok) return false;
     if (const char *env = getenv("OSCB_UMMA_FP4")) return atoi(env) == 1;
     return R <= umma_max_replicas(n_states, true);      // the whole call fits one launch of the e2m1 stream (N = 2: 12)
@@ -66,6 +73,7 @@ struct UmmaSession::Impl {
     void *peer_base[kUmmaMaxWorld] = {};
     bool peer_ipc[kUmmaMaxWorld] = {};
     bool connected = false;
+    int32_t stream_sig() const { return (int32_t)((a.fp4 & 1) | ((a.NB & 0x1FF) << 1) | ((a.dcols & 0x3F) << 10) | ((a.ktiles & 0x7FFF) << 16)); }
     DevBuf<unsigned char> phi[2];
     DevBuf<uint64_t> d_seeds;
     DevBuf<uint8_t> d_flags, d_best;
@@ -88,7 +96,7 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
     try {
         OSCB_REQUIRE(g && g->umma, "handle has no tensor-core plan (integer couplings |J| <= 127 on 128-row aligned shards)");
         OSCB_REQUIRE(spec.n_states >= 2 && spec.n_states <= 16, "tensor-core dense path takes N = 2..16 states");
-        const bool want_fp4 = umma_uses_fp4(*g->umma, spec.R_total > 0 ? spec.R_total : spec.R, spec.n_states);
+        const bool want_fp4 = umma_uses_fp4(*g->umma, spec.R_total > 0 ? spec.R_total : spec.R, spec.n_states, spec.force_stream);
         OSCB_REQUIRE(spec.R >= 1 && spec.R <= umma_max_replicas(spec.n_states, want_fp4),
                      "tensor-core dense path takes 1..%d replicas per launch at N = %d", umma_max_replicas(spec.n_states, want_fp4), spec.n_states);
         OSCB_REQUIRE(world >= 1 && world <= kUmmaMaxWorld && rank >= 0 && rank < world, "bad world / rank %d / %d", world, rank);
@@ -108,7 +116,7 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.tile_end = plan.tile_end;
         a.R = spec.R;
         // couplings representable in e2m1 stream as packed 4-bit codes through the TMA unpack path when few replicas share the launch
-        a.fp4 = umma_uses_fp4(plan, spec.R_total > 0 ? spec.R_total : spec.R, spec.n_states) ? 1 : 0;
+        a.fp4 = umma_uses_fp4(plan, spec.R_total > 0 ? spec.R_total : spec.R, spec.n_states, spec.force_stream) ? 1 : 0;
         a.A_fp4 = plan.A_fp4.p;
         a.ktiles = a.fp4 ? (plan.n + UMMA_K4 - 1) / UMMA_K4 : plan.tiles;
         a.dcols = a.fp4 ? 2 * UMMA_D9 : 8;
@@ -204,6 +212,7 @@ void UmmaSession::export_mem(UmmaExchange *out) const
     out->device = m->g->device;
     out->pid = (int32_t)getpid();
     out->grid = grid;
+    out->stream_sig = m->stream_sig();
 }
 
 void UmmaSession::connect(const UmmaExchange *all)
@@ -214,6 +223,13 @@ void UmmaSession::connect(const UmmaExchange *all)
         const UmmaExchange &x = all[w];
         OSCB_REQUIRE(x.bytes == m->xbytes, "rank %d exchange block is %llu bytes, expected %zu (replicas / schedule differ?)", w,
                      (unsigned long long)x.bytes, m->xbytes);
+        // at R = 1 the int8 and the e2m1 images have the SAME size, so the byte count alone would let a rank whose
+        // shard holds a coupling outside {0, +-1, +-2, +-3, +-4, +-6} (int8 digits) corrupt its peers' e2m1 planes
+        OSCB_REQUIRE(x.stream_sig == m->stream_sig(),
+                     "rank %d streams J as %s (B image signature 0x%x) but rank %d as %s (0x%x): every rank of a row-sharded run "
+                     "must use the same stream -- agree on it before create (dense_fused.run_dense_fused does; RunParams.variant 8 / 4)",
+                     w, (x.stream_sig & 1) ? "packed e2m1" : "int8", (unsigned)x.stream_sig, m->rank, m->a.fp4 ? "packed e2m1" : "int8",
+                     (unsigned)m->stream_sig());
         if (w == m->rank) m->a.cta_offset = (int)total;
         total += (unsigned)x.grid;
         if (w == m->rank) continue;

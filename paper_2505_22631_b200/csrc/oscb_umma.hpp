@@ -25,7 +25,7 @@ inline int umma_max_replicas(int n_states, bool fp4 = false)
 {
     return std::min(kUmmaMaxReplicas, 256 / ((fp4 ? 20 : 8) + (n_states == 2 ? 1 : n_states)));
 }
-bool umma_uses_fp4(const UmmaPlan &plan, int R, int n_states);   // the packed e2m1 stream for a call of R replicas in all (see oscb_umma.cu)
+bool umma_uses_fp4(const UmmaPlan &plan, int R, int n_states, int force_stream = 0);   // the packed e2m1 stream for a call of R replicas in all (see oscb_umma.cu)
 constexpr int kUmmaMaxWorld = 8;
 
 // what one rank of a row-sharded run publishes about its exchange block (the memory its peers
@@ -37,13 +37,14 @@ struct UmmaExchange {
     int32_t device;
     int32_t pid;
     int32_t grid;            // CTAs this rank launches
-    int32_t reserved;
+    int32_t stream_sig;      // layout of the B image this rank reads and WRITES INTO ITS PEERS: (fp4, B rows, digit columns, K tiles)
 };
 
 // schedule and parameters of one run of <= kUmmaMaxReplicas replicas
 struct UmmaSpec {
     int R = 1;
     int R_total = 0;                    // replicas of the whole call (several launches): picks the stream; 0 = R
+    int force_stream = 0;               // 0: by plan / OSCB_UMMA_FP4; 8: the int8 stream; 4: the packed e2m1 stream (must be possible)
     int precision = OSCB_PREC_F32;
     int noise_on = 1;
     int n_states = 2, maximize = 1;     // N = 2 max-cut, or N-state colouring (unit couplings)

@@ -40,7 +40,8 @@ class FusedDenseRank:
 
     def __init__(self, J_rows: np.ndarray, n: int, row_begin: int, row_end: int, device: int, params: SolverParams,
                  R: int, pair_count: int, world: int, rank: int, *, precision: str = "f32", steps: Optional[int] = None,
-                 trace_stride: Optional[float] = None, noise_off: bool = False, first_step: int = 0, graph=None):
+                 trace_stride: Optional[float] = None, noise_off: bool = False, first_step: int = 0, graph=None,
+                 stream_bits: int = 0):
         self.n, self.row_begin, self.row_end, self.device = n, row_begin, row_end, device
         self.R, self.world, self.rank = R, world, rank
         self.own_graph = graph is None
@@ -69,6 +70,9 @@ class FusedDenseRank:
         p.steps = self.nsteps if steps is not None else 0
         p.trace_stride = stride
         p.first_step = int(first_step)
+        if stream_bits not in (0, 4, 8):
+            raise ValueError("stream_bits must be 0 (this shard's own choice), 4 (packed e2m1) or 8 (int8)")
+        p.variant = int(stream_bits)               # the stream all ranks agreed on (agree_stream); 0 = this shard's own choice
         self.handle = C.c_void_p()
         rc = nat.lib().oscb_dense_fused_create(self.graph, C.byref(p), R, pair_count, world, rank, C.byref(self.handle))
         if rc != nat.OK:
@@ -149,6 +153,22 @@ class FusedDenseRank:
                            int(o.replicas_per_cta), int(o.smem_bytes), wall)
 
 
+def shard_stream_bits(graph, n_states: int, R: int) -> int:
+    """Bits per coupling this shard would stream on its own for a call of R replicas: 4 (packed e2m1: every coupling of
+    THESE rows in {0, +-1, +-2, +-3, +-4, +-6} and R small enough) or 8 (int8)."""
+    bits, per = C.c_int32(0), C.c_int32(0)
+    rc = nat.lib().oscb_dense_tc_stream(graph, n_states, R, C.byref(bits), C.byref(per))
+    if rc != nat.OK:
+        _raise(rc, "oscb_dense_tc_stream")
+    return int(bits.value)
+
+
+def agree_stream(local_bits: Sequence[int]) -> int:
+    """The stream of a row-sharded run: every rank writes phase digits into every peer's B image, so all ranks must use
+    ONE layout -- packed e2m1 only if every shard can take it, else int8 everywhere."""
+    return 4 if all(b == 4 for b in local_bits) else 8
+
+
 def assemble(parts: Sequence[BatchResult]) -> BatchResult:
     """Concatenate the ranks' row slices (rank order) into the result of the whole graph."""
     p0 = parts[0]
@@ -165,9 +185,21 @@ def run_fused_in_process(shards: Sequence[tuple], n: int, params: SolverParams, 
     one GPU when every rank's CTAs fit on it together).  shards = [(J_rows, row_begin, row_end,
     device), ...] in rank order."""
     world = len(shards)
-    ranks = [FusedDenseRank(J, n, rb, re, dev, params, len(seeds), pair_count, world, r, **kw)
-             for r, (J, rb, re, dev) in enumerate(shards)]
+    ranks: List[FusedDenseRank] = []
+    graphs = []
     try:
+        # upload the shards first and agree on one stream for all of them
+        for J, rb, re, dev in shards:
+            h = C.c_void_p()
+            rc = nat.lib().oscb_graph_create_dense(dev, n, nat.ptr(np.ascontiguousarray(J, dtype=np.float64)), rb, re, C.byref(h))
+            if rc != nat.OK:
+                _raise(rc, "oscb_graph_create_dense")
+            graphs.append(h)
+        bits = agree_stream([shard_stream_bits(h, params.n_states, len(seeds)) for h in graphs]) if world > 1 else 0
+        for r, (J, rb, re, dev) in enumerate(shards):
+            rk = FusedDenseRank(None, n, rb, re, dev, params, len(seeds), pair_count, world, r, graph=graphs[r], stream_bits=bits, **kw)
+            rk.own_graph = False
+            ranks.append(rk)
         blobs = [rk.export() for rk in ranks]
         for rk in ranks:
             rk.connect(blobs)
@@ -179,6 +211,8 @@ def run_fused_in_process(shards: Sequence[tuple], n: int, params: SolverParams, 
     finally:
         for rk in ranks:
             rk.close()
+        for h in graphs:
+            nat.lib().oscb_graph_destroy(h)
 
 
 def run_dense_fused(J_rows: Optional[np.ndarray], n: int, row_begin: int, row_end: int, params: SolverParams,
@@ -199,10 +233,25 @@ def run_dense_fused(J_rows: Optional[np.ndarray], n: int, row_begin: int, row_en
     keep_graph = graph is not None
     out: List[BatchResult] = []
     try:
+        if graph is None:
+            h = C.c_void_p()
+            rc = nat.lib().oscb_graph_create_dense(device, n, nat.ptr(np.ascontiguousarray(J_rows, dtype=np.float64)), row_begin,
+                                                   row_end, C.byref(h))
+            if rc != nat.OK:
+                _raise(rc, "oscb_graph_create_dense")
+            graph = h
         for r0 in range(0, len(seeds), MAX_REPLICAS):
             chunk = list(seeds[r0:r0 + MAX_REPLICAS])
-            rk = FusedDenseRank(J_rows, n, row_begin, row_end, device, params, len(chunk), pair_count, world, rank,
-                                graph=graph, **kw)
+            bits = 0
+            if world > 1:
+                # one stream for all ranks: e2m1 only if EVERY shard's couplings allow it (the OSCB_UMMA_FP4 environment of
+                # a single process must not split the ranks either)
+                mine_bits = shard_stream_bits(graph, params.n_states, len(seeds))
+                all_bits: List[Optional[int]] = [None] * world
+                dist.all_gather_object(all_bits, mine_bits, group=group)
+                bits = agree_stream(all_bits)
+            rk = FusedDenseRank(None, n, row_begin, row_end, device, params, len(chunk), pair_count, world, rank,
+                                graph=graph, stream_bits=bits, **kw)
             rk.own_graph = False
             graph = rk.graph
             try:

@@ -305,7 +305,9 @@ def phase_drift(J: CouplingMatrix, phi: PhaseState, i: int, K: float, ks_t: floa
         raise ValueError(f"dimension mismatch: coupling n={J.n} vs phases n={phi.n}")
     # a small h keeps the move inside (-0.5, 0.5) so the wrap can be undone exactly
     lo, hi = int(J.indptr[i]), int(J.indptr[i + 1])
-    bound = K * float(np.abs(J.data[lo:hi]).sum()) + abs(ks_t)
+    bound = abs(K) * float(np.abs(J.data[lo:hi]).sum()) + abs(ks_t)      # |drift| <= bound, also for K < 0
+    if not math.isfinite(bound):
+        raise ValueError("K, ks_t and the couplings must be finite")
     h = 2.0 ** -math.ceil(math.log2(max(bound, 1.0)) + 2)
     out = _step_raw(J, phi.phases[None, :], None, K, ks_t, h, 0.0, n_states, "f64", device)[0]
     d = out[i] - phi.phases[i]

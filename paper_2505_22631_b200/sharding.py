@@ -17,11 +17,12 @@ from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .dynamics import (BatchResult, RunResult, _results_from_batch, _validate_run_args, replica_seed,
+from .dynamics import (BatchResult, RunResult, _default_device, _results_from_batch, _validate_run_args, replica_seed,
                        resolve_workers, run_batch)
 from .model import CouplingMatrix, SolverParams
 
 Runner = Callable[..., BatchResult]
+MAX_REPLICAS_PER_CALL = 65536          # oscb_run's limit (include/oscb.h)
 
 
 def shard_bounds(replicas: int, world: int, rank: int) -> Tuple[int, int]:
@@ -50,9 +51,14 @@ def run_replica_block(J: CouplingMatrix, params: SolverParams, objective: str, r
     start, stop = shard_bounds(replicas, world, rank)
     if stop == start:
         return []
-    seeds = [replica_seed(params.seed, r) for r in range(start, stop)]
-    b = (runner or run_batch)(J, params, objective, seeds, **run_kw)
-    return _results_from_batch(J, params, objective, b, start)
+    # oscb_run takes at most 65536 replicas per call: chunk the block like run_replica_set does
+    out: List[RunResult] = []
+    for lo in range(start, stop, MAX_REPLICAS_PER_CALL):
+        hi = min(stop, lo + MAX_REPLICAS_PER_CALL)
+        seeds = [replica_seed(params.seed, r) for r in range(lo, hi)]
+        b = (runner or run_batch)(J, params, objective, seeds, **run_kw)
+        out.extend(_results_from_batch(J, params, objective, b, lo))
+    return out
 
 
 def best_of(results: Sequence[RunResult], objective: str) -> Optional[RunResult]:
@@ -84,7 +90,9 @@ def run_replicas_sharded(J: CouplingMatrix, params: SolverParams, objective: str
         return local
     # (objective, replica index) per rank; ranks without replicas send a sentinel
     worst = -np.inf if objective == "maxcut" else np.inf
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    # the GPU this rank computes on (OSCB_DEVICE / LOCAL_RANK, or the caller's `device`), not torch's current device:
+    # without a set_device every rank's "cuda" would be cuda:0 and NCCL would see one GPU twice
+    dev = torch.device("cuda", int(run_kw.get("device", _default_device()) or 0)) if dist.get_backend() == "nccl" else "cpu"
     mine_t = torch.tensor([local.best_objective if local else worst, float(local.replica_index) if local else -1.0],
                           dtype=torch.float64, device=dev)
     gathered = [torch.zeros_like(mine_t) for _ in range(world)]

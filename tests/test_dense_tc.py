@@ -245,3 +245,33 @@ def test_stream_choice_reported_by_the_abi(pkg):
     gs = dynamics.device_graph(sparse, 0)
     with pytest.raises(ValueError):
         gs.tc_stream(2, 1)
+
+
+def test_fused_ranks_agree_on_one_stream(pkg):
+    """A coupling outside {0, +-1, +-2, +-3, +-4, +-6} in ONE rank's rows only (its diagonal block) makes that shard an
+    int8 shard while its peer could stream packed e2m1.  At R = 1 both exchange blocks have the same size, so the ranks
+    used to connect and corrupt each other's B images silently.  Now (a) the driver agrees on one stream before create
+    and the run equals the single-handle run bit for bit, and (b) ranks created with different streams refuse to connect."""
+    from paper_2505_22631_b200 import dense_fused
+    n = 512
+    J = sk_graph(n, 9)
+    J[300, 301] = J[301, 300] = 5.0            # only in rank 1's diagonal block
+    Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.2, h=0.01, t_stop=0.6, seed=7)
+    want = pkg.run_batch(Jd, params, "maxcut", [7], kernel="dense-tc")
+    shards = [(J[0:256], 0, 256, 0), (J[256:512], 256, 512, 0)]
+    got = dense_fused.run_fused_in_process(shards, n, params, [7], pair_count=n * (n - 1) // 2)
+    assert np.array_equal(got.final_phases, want.final_phases) and np.array_equal(got.best_objective, want.best_objective)
+    assert np.array_equal(got.best_states, want.best_states) and np.array_equal(got.energy, want.energy)
+    # (b) the shards' own choices differ ...
+    ranks = [dense_fused.FusedDenseRank(Jr, n, a, b, 0, params, 1, n * (n - 1) // 2, 2, r) for r, (Jr, a, b, _) in enumerate(shards)]
+    try:
+        assert dense_fused.shard_stream_bits(ranks[0].graph, 2, 1) == 4 and dense_fused.shard_stream_bits(ranks[1].graph, 2, 1) == 8
+        assert dense_fused.agree_stream([4, 8]) == 8 and dense_fused.agree_stream([4, 4]) == 4
+        blobs = [rk.export() for rk in ranks]
+        assert len(blobs[0]) == len(blobs[1])
+        with pytest.raises(ValueError, match="same stream"):          # ... and connect says so instead of corrupting
+            ranks[0].connect(blobs)
+    finally:
+        for rk in ranks:
+            rk.close()

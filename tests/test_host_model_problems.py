@@ -227,3 +227,26 @@ def test_generator_plants_a_proper_colouring():
     with pytest.raises(ValueError):
         prob.generate_colorable_graph(4, 100, 2, seed=0)
     assert prob.parse_gset(prob.write_gset(g)) == g
+
+
+def test_coupling_matrix_pickles_and_copies_with_a_device_cache():
+    """The reference's CouplingMatrix is plain arrays and pickles (model.py:124-150); here the cached device handles
+    (ctypes pointers) must not get in the way once a J has been solved with."""
+    import copy
+    import pickle
+    from paper_2505_22631_b200.model import CouplingMatrix
+    J = CouplingMatrix.from_edges(5, [(0, 1, 1.0), (1, 2, -2.0), (3, 4, 0.5)])
+    J.pairs()
+
+    class FakeHandle:                      # stands in for dynamics.DeviceGraph (holds a ctypes c_void_p)
+        def __init__(self):
+            import ctypes
+            self.handle = ctypes.c_void_p(1234)
+    J._device = {0: FakeHandle()}
+    for K in (pickle.loads(pickle.dumps(J)), copy.deepcopy(J), copy.copy(J)):
+        assert K.n == 5 and K.storage_kind == J.storage_kind
+        assert np.array_equal(K.indptr, J.indptr) and np.array_equal(K.indices, J.indices) and np.array_equal(K.data, J.data)
+        assert K._device is None
+        assert not K.data.flags.writeable
+    D = CouplingMatrix.from_dense(np.array([[0, 1.0], [1.0, 0]]), storage="dense")
+    assert np.array_equal(pickle.loads(pickle.dumps(D)).to_dense(), D.to_dense())
