@@ -449,12 +449,26 @@ def bench_dense(args, rank, world, local_rank):
     pairs = n * (n - 1) // 2
     phi0 = dyn._initial_phases_host(local_rank, seeds, n)
 
+    nccl_backend = None
+    if args.exchange == "nccl":
+        from paper_2505_22631_b200 import dense_sharded
+        if (n // world) * world != n:
+            raise SystemExit("--exchange nccl needs n divisible by the rank count")
+        rows = n // world
+        lo, hi = rank * rows, (rank + 1) * rows
+        g.close()
+        nccl_backend = dense_sharded.CudaDenseShard(workloads.sk_dense(n)[lo:hi].astype(np.float64), n, lo, hi, local_rank, args.precision)
+
     def one():
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        res = dense_fused.run_dense_fused(None, n, lo, hi, params, seeds, device=local_rank, pair_count=pairs, phi0=phi0,
-                                          graph=g.handle, precision=args.precision, steps=window)
+        if nccl_backend is not None:
+            run = dense_sharded.run_dense_sharded(nccl_backend, params, "maxcut", seeds, pair_count=pairs, phi0=phi0, steps=window)
+            res = run.batch
+        else:
+            res = dense_fused.run_dense_fused(None, n, lo, hi, params, seeds, device=local_rank, pair_count=pairs, phi0=phi0,
+                                              graph=g.handle, precision=args.precision, steps=window)
         torch.cuda.synchronize()
         return time.perf_counter() - t0, res
 
@@ -477,7 +491,8 @@ def bench_dense(args, rank, world, local_rank):
     # per GPU: its shard of J once per Euler step and session (sessions of <= 28 replicas; one of <= 12 streams e2m1 tiles)
     sessions = [min(dense_fused.MAX_REPLICAS, R - r0) for r0 in range(0, R, dense_fused.MAX_REPLICAS)]
     chunks = len(sessions)
-    bytes_step = sum((hi - lo) * n * g.tc_stream(2, r)[0] // 8 for r in sessions) + 2 * R * n * s_phi
+    bytes_step = (sum((hi - lo) * n * g.tc_stream(2, r)[0] // 8 for r in sessions) if nccl_backend is None      # (int8 J on the SIMT path)
+                  else (hi - lo) * n) + 2 * R * n * s_phi
     achieved = bytes_step * window * args.steps / dev_s / 1e9
     if rank == 0:
         print(json.dumps({
@@ -485,7 +500,8 @@ def bench_dense(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.precision + " epilogue, int8 x int8 -> int32 tensor-core sums", "data": "synthetic",
             "config": {"workload": label + f"; J row-sharded over {world} GPUs, phase digits pushed to the peers from inside the kernel every Euler step",
-                       "replicas": R, "window": window, "kernel": "dense-tc", "parallelism": f"row-shard x{world}",
+                       "replicas": R, "window": window, "kernel": "dense-tc" if nccl_backend is None else "dense-sharded (SIMT step + ncclAllGather)",
+                       "exchange": args.exchange, "parallelism": f"row-shard x{world}",
                        "l2": "a J shard below ~100 MB (n=16384 at 4+ GPUs) stays L2 resident between Euler steps; the roofline below still charges it to HBM"},
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": int(8 * R * n + 8 * R),
                     "d2h_bytes_per_step": int(9 * R * (hi - lo) + 8 * R * 4),
@@ -595,6 +611,10 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "resident"])
     ap.add_argument("--replicas", type=int, default=0, help="override replicas per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="row-sharded dense runs (SK<n>x<R> under torchrun): 'fused' = phase digits pushed into the peers' B images "
+                         "from inside the persistent tensor-core kernel; 'nccl' = the baseline it replaces, one SIMT step launch + "
+                         "ncclAllGather of the phase slices per Euler step (dense_sharded.py)")
     ap.add_argument("--no-target", action="store_true", help="skip the time-to-99%%-best-cut run")
     ap.add_argument("--no-parity-mode", action="store_true", help="skip the float64 sub-record of the same workload")
     args = ap.parse_args()

@@ -13,6 +13,7 @@ import argparse
 import csv
 import io
 import json
+import os
 import sys
 from pathlib import Path
 from typing import Dict, List, Optional
@@ -194,20 +195,43 @@ def cmd_sweep(args) -> int:
         n_k, n_s = (int(x) for x in args.grid.lower().split("x"))
     except ValueError:
         raise UsageError(f"--grid must look like RxC with integers, got {args.grid!r}") from None
-    workers = resolve_workers(args.workers)
+    resolve_workers(args.workers)
     J = inst.coupling()
+    # all cells are independent replicas of one graph: they run as ONE batched workload -- concurrently on the GPU and,
+    # under a torch.distributed launch (WORLD_SIZE > 1), sharded over the ranks (sweep.py); rank 0 writes the table
+    from . import sweep as sw
+    over = {k: getattr(args, k) for k in TUNABLES if getattr(args, k, None) is not None}
+    labels, cells = sw.grid_cells(inst.graph.node_count, inst.n_states, args.seed, _axis(k_lo, k_hi, n_k), _axis(s_lo, s_hi, n_s), over)
+    group = _maybe_init_process_group()
+    try:
+        objs = sw.run_cells_sharded(J, cells, inst.kind, args.replicas, **_gpu_kwargs(args))
+    finally:
+        if group:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if objs is None:
+        return EXIT_OK                                # not rank 0
     lines = [SWEEP_HEADER]
-    for K in _axis(k_lo, k_hi, n_k):
-        for ks_max in _axis(s_lo, s_hi, n_s):
-            params = _tuned(args, inst.graph.node_count, inst.n_states, args.seed, {"K": K, "ks_max": ks_max})
-            scores = []
-            for res in run_replica_set(J, params, inst.kind, replicas=args.replicas, workers=workers, **_gpu_kwargs(args)):
-                final = threshold_phases(res.final_phases, params.n_states)
-                scores.append(100.0 * cut_value(inst.graph, final) / args.reference if inst.kind == "maxcut"
-                              else 100.0 * coloring_conflicts(inst.graph, final)[1])
-            lines.append(f"{K!r},{ks_max!r},{float(np.mean(scores))!r}")
+    m = inst.graph.edge_count
+    for (K, ks_max), obj in zip(labels, objs):
+        scores = 100.0 * obj / args.reference if inst.kind == "maxcut" else 100.0 * ((1.0 - obj / m) if m else np.ones_like(obj))
+        lines.append(f"{K!r},{ks_max!r},{float(np.mean(scores))!r}")
     _emit("\n".join(lines) + "\n", args.out)
     return EXIT_OK
+
+
+def _maybe_init_process_group() -> bool:
+    """Under torchrun (WORLD_SIZE > 1) join the default process group -- NCCL with GPUs, gloo otherwise (or when
+    OSCB_BENCH_BACKEND says so).  Returns True when this call created it."""
+    if int(os.environ.get("WORLD_SIZE", "1")) <= 1:
+        return False
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized():
+        return False
+    backend = os.environ.get("OSCB_BENCH_BACKEND", "nccl" if torch.cuda.is_available() else "gloo")
+    dist.init_process_group(backend)
+    return True
 
 
 def cmd_scaling(args) -> int:

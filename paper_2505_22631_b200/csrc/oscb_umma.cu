@@ -77,6 +77,8 @@ struct UmmaSession::Impl {
     DevBuf<unsigned char> phi[2];
     DevBuf<uint64_t> d_seeds;
     DevBuf<uint8_t> d_flags, d_best;
+    DevBuf<unsigned long long> d_timeout;
+    int watchdog_ms = 20000;
     DevBuf<long long> d_trace;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     size_t tsize = 4;
@@ -171,6 +173,14 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         a.best_states = m->d_best.p;
         a.nonfinite = g->d_nonfinite.p;
         a.trace = nullptr;
+        m->d_timeout.alloc(1);
+        a.timeout_flag = m->d_timeout.p;
+        if (const char *e = getenv("OSCB_UMMA_WATCHDOG_MS")) m->watchdog_ms = std::max(1, atoi(e));
+        {
+            int khz = 0;
+            OSCB_CUDA(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->device));
+            a.watchdog_cycles = (long long)m->watchdog_ms * (long long)std::max(khz, 100000);     // ms x cycles per ms
+        }
         OSCB_CUDA(cudaEventCreate(&m->ev0));
         OSCB_CUDA(cudaEventCreate(&m->ev1));
     } catch (...) {
@@ -268,6 +278,7 @@ void UmmaSession::prepare(const uint64_t *seeds, const double *d_phi0)
     m->d_flags.upload(m->flags.data(), (size_t)a.passes, s);
     const unsigned long long none = ~0ull;
     OSCB_CUDA(cudaMemcpyAsync(m->g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    OSCB_CUDA(cudaMemcpyAsync(m->d_timeout.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
     if (const char *trace_path = getenv("OSCB_UMMA_TRACE")) {     // debug: per-CTA timeline of the first passes
         (void)trace_path;
         m->d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * UMMA_TRACE_SLOTS);
@@ -333,8 +344,16 @@ void UmmaSession::finish(double *h_final_rows, uint8_t *h_best_rows, long long *
         OSCB_CUDA(cudaMemcpy2DAsync(h_best_rows, (size_t)nrows, m->d_best.p, (size_t)a.ld_phi, (size_t)nrows, (size_t)R,
                                     cudaMemcpyDeviceToHost, s));
     OSCB_CUDA(cudaMemcpyAsync(&nonfinite, m->g->d_nonfinite.p, sizeof(nonfinite), cudaMemcpyDeviceToHost, s));
+    unsigned long long timed_out = ~0ull;
+    OSCB_CUDA(cudaMemcpyAsync(&timed_out, m->d_timeout.p, sizeof(timed_out), cudaMemcpyDeviceToHost, s));
     OSCB_CUDA(cudaStreamSynchronize(s));
     OSCB_CUDA(cudaEventElapsedTime(&ms, m->ev0, m->ev1));
+    if (timed_out != ~0ull) {
+        set_error("dense tensor-core run abandoned: rank %d waited more than %d ms at Euler step %llu for the other CTAs / ranks "
+                  "of the step barrier (a peer rank never launched, died, or OSCB_UMMA_WATCHDOG_MS is too short); results are invalid",
+                  m->rank, m->watchdog_ms, timed_out);
+        throw OscbFail{OSCB_ECUDA};
+    }
     if (h_energy)
         for (long long k = 0; k < S; ++k)
             for (int r = 0; r < R; ++r) {

@@ -90,6 +90,8 @@ struct UmmaArgs {
     uint8_t *best_states;     // [R][ld_phi]
     unsigned long long *nonfinite;
     long long *trace;         // debug timeline [cta][UMMA_TRACE_PASSES][4] in SM clocks, or null
+    unsigned long long *timeout_flag;  // first pass at which some CTA of this rank gave up waiting for the step barrier (0: none)
+    long long watchdog_cycles;         // SM clocks a producer waits for the other CTAs / ranks before it gives up
 };
 
 namespace umma {
@@ -483,6 +485,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             };
             const int per_pass_i = (int)per_pass;
             const int pre = per_pass_i < stages ? per_pass_i : stages;
+            bool dead = false;
             for (long long pass = 0; pass < a.passes; ++pass) {
                 const uint8_t *Bsrc = a.B_img[pass & 1][a.rank];
                 int start = 0;
@@ -490,7 +493,19 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     for (int j = 0; j < pre; ++j) issue_a(ca);                  // J does not depend on the step: run ahead
                     const unsigned int target = a.ctas_total * (unsigned int)pass;
                     if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 3] = clock64();
-                    while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
+                    if (!dead) {
+                        // watchdog: a peer rank that never launched (or died) must not hang this GPU.  After the
+                        // deadline the run is abandoned -- the flag makes finish() fail -- and the kernel free-runs
+                        // through its remaining passes without waiting, so it terminates.
+                        const long long t_wait = clock64();
+                        while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) {
+                            if (clock64() - t_wait > a.watchdog_cycles) {
+                                dead = true;
+                                atomicMin(a.timeout_flag, (unsigned long long)pass);
+                                break;
+                            }
+                        }
+                    }
                     if (a.trace && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 0] = clock64();
                     umma::fence_proxy_async();
                     for (int j = 0; j < pre; ++j) issue_b(cb, Bsrc);
@@ -725,7 +740,13 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         // the last pass scored the final phases: wait for every rank's totals, then keep the states
         if (et == 0) {
             const unsigned int target = a.ctas_total * (unsigned int)a.passes;
-            while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) { }
+            const long long t_wait = clock64();
+            while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) {
+                if (clock64() - t_wait > a.watchdog_cycles) {        // (same watchdog as the producer's)
+                    atomicMin(a.timeout_flag, (unsigned long long)a.passes);
+                    break;
+                }
+            }
         }
         umma::named_bar_sync(1, UMMA_EPI_THREADS);
         if ((a.flags[a.passes - 1] & 1) && et < R) {

@@ -275,3 +275,30 @@ def test_fused_ranks_agree_on_one_stream(pkg):
     finally:
         for rk in ranks:
             rk.close()
+
+
+def test_watchdog_abandons_a_run_whose_peer_never_arrives(pkg, monkeypatch):
+    """The producers spin on the step barrier of ALL ranks.  A peer that never launches used to hang the GPU; now the
+    wait has a deadline (OSCB_UMMA_WATCHDOG_MS, default 20 s): the kernel free-runs to its end and finish() fails."""
+    from paper_2505_22631_b200 import dense_fused
+    monkeypatch.setenv("OSCB_UMMA_WATCHDOG_MS", "200")
+    n = 512
+    J = sk_graph(n, 3)
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.2, h=0.01, t_stop=0.3, seed=1)
+    ranks = [dense_fused.FusedDenseRank(J[a:b], n, a, b, 0, params, 2, n * (n - 1) // 2, 2, r) for r, (a, b) in enumerate(((0, 256), (256, 512)))]
+    try:
+        blobs = [rk.export() for rk in ranks]
+        for rk in ranks:
+            rk.connect(blobs)
+        for rk in ranks:
+            rk.prepare([1, 2])
+        ranks[0].launch()                      # rank 1 never launches
+        with pytest.raises(RuntimeError, match="abandoned"):
+            ranks[0].finish()
+    finally:
+        for rk in ranks:
+            rk.close()
+    # the device is fine afterwards: the same ranks run to completion when both launch
+    shards = [(J[0:256], 0, 256, 0), (J[256:512], 256, 512, 0)]
+    ok = dense_fused.run_fused_in_process(shards, n, params, [1, 2], pair_count=n * (n - 1) // 2)
+    assert ok.steps == 30 and ok.final_phases.shape == (2, n)

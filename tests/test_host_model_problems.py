@@ -250,3 +250,44 @@ def test_coupling_matrix_pickles_and_copies_with_a_device_cache():
         assert not K.data.flags.writeable
     D = CouplingMatrix.from_dense(np.array([[0, 1.0], [1.0, 0]]), storage="dense")
     assert np.array_equal(pickle.loads(pickle.dumps(D)).to_dense(), D.to_dense())
+
+
+def test_vectorised_parsers_equal_the_strict_ones_and_keep_the_errors():
+    """The array path of parse_gset / parse_dimacs_col (problems.py:108-147, :159-202) returns exactly what the
+    line-by-line parser returns on well-formed input, at scale, and every malformed input still raises the reference's
+    error class with its line number (the strict parser takes over)."""
+    import time
+    from paper_2505_22631_b200 import problems as P, workloads
+    u, v, w = workloads.random_gnm(3000, 200_000, seed=4, weights=(1.0, -1.0, 2.5))
+    g = P.Graph(3000, u, v, w)
+    text = P.write_gset(g)
+    t0 = time.perf_counter(); fast = P.parse_gset(text); t_fast = time.perf_counter() - t0
+    t0 = time.perf_counter(); slow = P._parse_gset_strict(text); t_slow = time.perf_counter() - t0
+    for a in ("u", "v", "w"):
+        assert np.array_equal(getattr(fast, a), getattr(slow, a)) and np.array_equal(getattr(fast, a), getattr(g, a))
+    assert P._fast_gset(text) is not None and t_fast < t_slow
+    unweighted = "\n".join(["5 3", "", "1 2", " 4 5 ", "2 3"]) + "\n"
+    assert np.array_equal(P.parse_gset(unweighted).w, np.ones(3)) and P._fast_gset(unweighted) is not None
+    col = P.write_dimacs_col(g) + "e 2 1\ne 1 2\n" + "c trailing comment\n"
+    fd, sd = P.parse_dimacs_col(col), P._parse_dimacs_col_strict(col)
+    assert P._fast_dimacs(col) is not None
+    assert np.array_equal(fd.u, sd.u) and np.array_equal(fd.v, sd.v) and fd.edge_count == sd.edge_count
+    bad = {
+        "3 1\n1 1\n": P.SelfLoopError, "3 2\n1 2\n2 1\n": P.DuplicateEdgeError, "3 1\n1 4\n": P.EdgeIndexError,
+        "3 2\n1 2\n": P.HeaderMismatchError, "3 1\n1 x\n": P.MalformedLineError, "3 1\n1.0 2\n": P.MalformedLineError,
+        "": P.MissingHeaderError, "3 2\n1 2\n1 3 1.5\n": None,       # mixed 2- / 3-token lines are legal
+    }
+    for text_bad, err in bad.items():
+        assert P._fast_gset(text_bad) is None
+        if err is None:
+            assert P.parse_gset(text_bad).edge_count == 2
+        else:
+            with pytest.raises(err) as ei:
+                P.parse_gset(text_bad)
+            if err not in (P.HeaderMismatchError, P.MissingHeaderError):
+                assert ei.value.line == (3 if err is P.DuplicateEdgeError else 2)
+    for text_bad, err in {"p edge 3 1\ne 1 1\n": P.SelfLoopError, "e 1 2\np edge 3 1\n": P.MissingHeaderError,
+                          "p edge 3 1\nx 1 2\n": P.UnknownDirectiveError, "p edge 3 1\ne 1 9\n": P.EdgeIndexError}.items():
+        assert P._fast_dimacs(text_bad) is None
+        with pytest.raises(err):
+            P.parse_dimacs_col(text_bad)
