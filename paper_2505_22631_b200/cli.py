@@ -76,7 +76,9 @@ def _report(inst, params: SolverParams, result, replicas: int, workers: int, ref
     return {"instance": inst.source_name, "problem": inst.kind, "n": inst.graph.node_count, "edges": inst.graph.edge_count,
             "params": {f: getattr(params, f) for f in fields}, "replicas": replicas, "workers": workers,
             "best_objective": result.best_objective, "satisfied_fraction": satisfied, "reference": reference,
-            "accuracy_pct": accuracy, "wall_time_s": result.wall_time, "steps": result.steps_executed, "seed": params.seed}
+            "accuracy_pct": accuracy, "wall_time_s": result.wall_time, "steps": result.steps_executed, "seed": params.seed,
+            # (beyond the reference's report: the arithmetic of this run -- float32 is this package's default)
+            "precision": getattr(result, "precision", "f32")}
 
 
 def _emit(text: str, out: Optional[str]) -> None:

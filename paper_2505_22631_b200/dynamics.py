@@ -178,6 +178,10 @@ class RunResult:
     steps_executed: int
     objective_kind: str
     replica_index: int = 0
+    # not in the reference's RunResult: the arithmetic this result was computed in -- "f32" (throughput mode, the
+    # DEFAULT of this package) or "f64" (the reference's own arithmetic) -- and the kernel that ran
+    precision: str = "f32"
+    kernel: str = ""
 
 
 # ---------------------------------------------------------------------------
@@ -406,6 +410,7 @@ class BatchResult:
     replicas_per_cta: int
     smem_bytes: int
     wall_time: float
+    precision: str = "f32"
 
 
 def _objective_cadence_for(n: int, pair_count: int) -> int:
@@ -496,7 +501,7 @@ def run_batch(J: CouplingMatrix, params: SolverParams, objective: str, seeds: Se
                        en[:, :S].copy() if en is not None else np.zeros((R, 0)),
                        bt[:, :S].copy() if bt is not None else np.zeros((R, 0)),
                        first, int(o.steps_executed), float(o.device_ms), int(o.kernel_launches),
-                       nat.KERNEL_NAME.get(int(o.kernel_used), "?"), int(o.replicas_per_cta), int(o.smem_bytes), wall)
+                       nat.KERNEL_NAME.get(int(o.kernel_used), "?"), int(o.replicas_per_cta), int(o.smem_bytes), wall, prec)
 
 
 def _objective_from_states(states_row: np.ndarray, iu, jv, w, kind: str) -> float:
@@ -532,6 +537,8 @@ def _results_from_batch(J: CouplingMatrix, params: SolverParams, objective: str,
             steps_executed=b.steps,
             objective_kind=objective,
             replica_index=first_index + r,
+            precision=b.precision,
+            kernel=b.kernel,
         ))
     return out
 

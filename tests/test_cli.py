@@ -7,7 +7,8 @@ import numpy as np
 import pytest
 
 REPORT_KEYS = {"instance", "problem", "n", "edges", "params", "replicas", "workers", "best_objective",
-               "satisfied_fraction", "reference", "accuracy_pct", "wall_time_s", "steps", "seed"}
+               "satisfied_fraction", "reference", "accuracy_pct", "wall_time_s", "steps", "seed",
+               "precision"}          # the reference's keys (cli.py:94-126) + the arithmetic of the run
 PARAM_KEYS = {"K", "ks_max", "ks_period", "kn", "h", "t_stop", "n_states", "seed", "batch_size"}
 
 
@@ -57,6 +58,7 @@ def test_solve_triangle_maxcut_report(capsys, files):
     report = json.loads(out)
     assert report["best_objective"] == 2.0 and report["problem"] == "maxcut"
     assert set(report) == REPORT_KEYS and set(report["params"]) == PARAM_KEYS
+    assert report["precision"] == "f32"              # the package default, stated in the report
     assert report["steps"] == 3000 and report["replicas"] == 4
 
 
