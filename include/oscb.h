@@ -217,6 +217,10 @@ int oscb_dense_fused_connect(oscb_fused *f, const void *all /* [world * OSCB_FUS
 int oscb_dense_fused_prepare(oscb_fused *f, const uint64_t *seeds /* [R] */, const double *phi0 /* [R, n] or NULL */);
 int oscb_dense_fused_launch(oscb_fused *f);
 int oscb_dense_fused_finish(oscb_fused *f, oscb_run_outputs *out);
+/* CTAs this rank's persistent kernel launches and how many of them share one 128-row tile of J (split-K: a rank that
+ * owns few row tiles splits each tile's K range over SMs / tiles CTAs; the partial sums meet in a global int32
+ * accumulator, so the results do not depend on it). */
+int oscb_dense_fused_grid(const oscb_fused *f, int32_t *ctas, int32_t *splits);
 int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows);
 int oscb_dense_fused_destroy(oscb_fused *f);
 /* What a tensor-core dense run of R replicas on this handle streams: bits per coupling of the J

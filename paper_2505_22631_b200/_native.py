@@ -90,6 +90,7 @@ SYMBOLS = {
     "oscb_dense_fused_launch": (C.c_int, [_P]),
     "oscb_dense_fused_finish": (C.c_int, [_P, C.POINTER(RunOutputs)]),
     "oscb_dense_fused_rows": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "oscb_dense_fused_grid": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "oscb_dense_fused_destroy": (C.c_int, [_P]),
     "oscb_dense_tc_stream": (C.c_int, [_P, C.c_int32, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "oscb_selftest_sign_state": (C.c_int, [C.c_int, C.POINTER(C.c_uint64)]),

@@ -1155,6 +1155,16 @@ int oscb_dense_fused_finish(oscb_fused *f, oscb_run_outputs *out)
     });
 }
 
+int oscb_dense_fused_grid(const oscb_fused *f, int32_t *ctas, int32_t *splits)
+{
+    return guarded([&]() -> int {
+        OSCB_REQUIRE(f && ctas && splits, "NULL argument");
+        *ctas = f->session->grid;
+        *splits = f->session->splits;
+        return OSCB_OK;
+    });
+}
+
 int oscb_dense_fused_rows(const oscb_fused *f, int64_t *rows)
 {
     return guarded([&]() -> int {

@@ -78,6 +78,8 @@ struct UmmaSession::Impl {
     DevBuf<uint64_t> d_seeds;
     DevBuf<uint8_t> d_flags, d_best;
     DevBuf<unsigned long long> d_timeout;
+    DevBuf<int> d_acc;                      // split-K accumulator
+    DevBuf<unsigned int> d_tile_cnt;
     int watchdog_ms = 20000;
     DevBuf<long long> d_trace;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -141,6 +143,24 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         grid = std::min(lt, g->sm_count);
         if (const char *cap = getenv("OSCB_UMMA_MAX_GRID"))       // test knob: several row tiles per CTA on small graphs
             grid = std::max(1, std::min(grid, atoi(cap)));
+        // split-K: a handle that owns few row tiles (a rank of a row-sharded run: 16 of the 128 tiles of SK 16384 at 8
+        // GPUs) would keep one CTA per tile busy and leave the other SMs idle, each CTA still streaming a full-K row tile.
+        // S CTAs then share a tile, S = SMs / tiles, when the per-CTA stream of a pass is long enough to pay for the
+        // exchange of the partial sums (OSCB_UMMA_SPLITK = 1 disables, = S forces).
+        a.splits = 1;
+        if (grid == lt) {
+            int S = std::min(g->sm_count / std::max(lt, 1), a.ktiles);
+            const size_t stream = (size_t)a.ktiles * stage;       // bytes one CTA moves per pass for a whole-K row tile
+            if (S < 2 || stream < (size_t)512 * 1024) S = 1;
+            if (const char *e = getenv("OSCB_UMMA_SPLITK")) S = std::max(1, std::min({atoi(e), g->sm_count / std::max(lt, 1), a.ktiles}));
+            a.splits = S;
+            grid = lt * S;
+        }
+        splits = a.splits;
+        m->d_acc.alloc((size_t)lt * UMMA_TILE * a.NB);
+        m->d_tile_cnt.alloc((size_t)lt);
+        a.acc_g = m->d_acc.p;
+        a.tile_cnt = m->d_tile_cnt.p;
         a.ctas_total = (unsigned)grid;                            // world = 1; connect() fills in the real totals
         a.cta_offset = 0;
         a.passes = spec.steps + 1;
@@ -153,7 +173,8 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         const size_t E = (size_t)std::max<long long>(1, spec.n_events), S = (size_t)std::max<long long>(1, spec.n_samples);
         m->off_events = 256;
         m->off_en = m->off_events + round256(E * spec.R * sizeof(long long));
-        m->off_b[0] = m->off_en + round256(S * (size_t)plan.tiles * spec.R * sizeof(double));   // <= one CTA per tile, all ranks
+        // energy partials: one slot per CTA of ALL ranks (one CTA per row tile, or with split-K at most the SMs of every rank)
+        m->off_b[0] = m->off_en + round256(S * (size_t)std::max(plan.tiles, world * g->sm_count) * spec.R * sizeof(double));
         m->off_b[1] = m->off_b[0] + round256((size_t)a.ktiles * b_stage);
         m->xbytes = m->off_b[1] + round256((size_t)a.ktiles * b_stage);
         OSCB_CUDA(cudaSetDevice(g->device));
@@ -262,6 +283,15 @@ void UmmaSession::connect(const UmmaExchange *all)
         }
         m->point_rank(w, (unsigned char *)m->peer_base[w]);
     }
+    // ranks that share this GPU (virtual ranks of the tests, OSCB_BENCH_BACKEND=gloo) must be co-resident: every
+    // kernel spins on the others' arrivals
+    unsigned here = 0;
+    for (int w = 0; w < m->world; ++w)
+        if (all[w].device == m->g->device) here += (unsigned)all[w].grid;
+    OSCB_REQUIRE(here <= (unsigned)m->g->sm_count || here == (unsigned)grid,
+                 "the ranks sharing device %d launch %u CTAs in all, more than its %d SMs: their persistent kernels cannot be "
+                 "resident together (fewer ranks per GPU, or OSCB_UMMA_SPLITK=1 to keep one CTA per row tile)",
+                 m->g->device, here, m->g->sm_count);
     m->a.ctas_total = total;
     m->connected = true;
 }
@@ -279,6 +309,8 @@ void UmmaSession::prepare(const uint64_t *seeds, const double *d_phi0)
     const unsigned long long none = ~0ull;
     OSCB_CUDA(cudaMemcpyAsync(m->g->d_nonfinite.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
     OSCB_CUDA(cudaMemcpyAsync(m->d_timeout.p, &none, sizeof(none), cudaMemcpyHostToDevice, s));
+    m->d_acc.zero(s);
+    m->d_tile_cnt.zero(s);
     if (const char *trace_path = getenv("OSCB_UMMA_TRACE")) {     // debug: per-CTA timeline of the first passes
         (void)trace_path;
         m->d_trace.alloc((size_t)grid * UMMA_TRACE_PASSES * UMMA_TRACE_SLOTS);

@@ -90,6 +90,9 @@ struct UmmaArgs {
     uint8_t *best_states;     // [R][ld_phi]
     unsigned long long *nonfinite;
     long long *trace;         // debug timeline [cta][UMMA_TRACE_PASSES][4] in SM clocks, or null
+    int splits;               // split-K: CTAs sharing one row tile (1: a CTA owns whole row tiles).  > 1 only with one unit per CTA
+    int *acc_g;               // split-K: [local tiles][128][NB] int32 partial-sum accumulator (zero between passes)
+    unsigned int *tile_cnt;   // split-K: [local tiles] monotonic count of partials added
     unsigned long long *timeout_flag;  // first pass at which some CTA of this rank gave up waiting for the step barrier (0: none)
     long long watchdog_cycles;         // SM clocks a producer waits for the other CTAs / ranks before it gives up
 };
@@ -419,8 +422,19 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool sys = a.world > 1;
-    const int my_tiles = (a.tile_end - a.tile_begin - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const long long per_pass = (long long)my_tiles * a.ktiles;
+    // Work units.  splits == 1: CTA b owns row tiles b, b + grid, ... with their whole K range.  splits = S > 1 (a rank
+    // of a row-sharded run owns few row tiles, or a small graph): the grid is exactly tiles x S, CTA b integrates
+    // k-blocks [kb0, kb1) of row tile b / S; the S partial sums of a tile meet in a global int32 accumulator and the
+    // split-0 CTA of the tile runs the update.  Integer sums: the result does not depend on S.
+    const int S = a.splits;
+    const int ksplit = S > 1 ? (int)blockIdx.x % S : 0;
+    const int lt_first = S > 1 ? (int)blockIdx.x / S : (int)blockIdx.x;
+    const int lt_stride = S > 1 ? 0 : (int)gridDim.x;
+    const int kb0 = S > 1 ? (int)(((long long)ksplit * a.ktiles) / S) : 0;
+    const int kb1 = S > 1 ? (int)(((long long)(ksplit + 1) * a.ktiles) / S) : a.ktiles;
+    const bool lead = ksplit == 0;
+    const int my_tiles = S > 1 ? 1 : (a.tile_end - a.tile_begin - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const long long per_pass = (long long)my_tiles * (kb1 - kb0);
     const uint32_t stage_tx = (uint32_t)UMMA_A_STAGE + b_stage;
 
     if (threadIdx.x == 0) {
@@ -465,15 +479,15 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             struct Cursor {
                 int s; uint32_t ph; int tk, kb;
             };
-            Cursor ca{0, 0, 0, 0}, cb{0, 0, 0, 0};
+            Cursor ca{0, 0, 0, kb0}, cb{0, 0, 0, kb0};
             auto advance = [&](Cursor &c) {
                 if (++c.s == stages) { c.s = 0; c.ph ^= 1u; }
-                if (++c.kb == a.ktiles) { c.kb = 0; if (++c.tk == my_tiles) c.tk = 0; }
+                if (++c.kb == kb1) { c.kb = kb0; if (++c.tk == my_tiles) c.tk = 0; }
             };
             auto issue_a = [&](Cursor &c) {
                 umma::mbar_wait(bar_empty + 8u * c.s, c.ph ^ 1u);
                 umma::mbar_expect_tx(bar_full + 8u * c.s, stage_tx);
-                const int lt = (int)blockIdx.x + c.tk * (int)gridDim.x;
+                const int lt = lt_first + c.tk * lt_stride;
                 const uint8_t *img = FP4 ? a.A_fp4 : a.A_img;
                 umma::bulk_g2s(sA + (uint32_t)c.s * UMMA_A_STAGE, img + ((size_t)lt * a.ktiles + c.kb) * UMMA_A_STAGE, UMMA_A_STAGE,
                                bar_full + 8u * c.s);
@@ -529,15 +543,15 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                 for (int tk = 0; tk < my_tiles; ++tk) {
                     umma::mbar_wait(bar_tempty, (uint32_t)((acc_it & 1) ^ 1));
                     umma::tc_fence_after();
-                    for (int kb = 0; kb < a.ktiles; ++kb) {
+                    for (int kb = kb0; kb < kb1; ++kb) {
                         umma::mbar_wait(bar_full + 8u * s, ph);
                         umma::tc_fence_after();
                         const uint64_t ad = umma::smem_desc(sA + (uint32_t)s * UMMA_A_STAGE);
                         const uint64_t bd = umma::smem_desc(sB + (uint32_t)s * b_stage);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
-                            if (FP4) umma::mma_mxf4(tmem, ad + 2u * k, bd + 2u * k, idesc, sfa, sfb, (uint32_t)((kb | k) != 0));
-                            else umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)((kb | k) != 0));
+                            if (FP4) umma::mma_mxf4(tmem, ad + 2u * k, bd + 2u * k, idesc, sfa, sfb, (uint32_t)(((kb - kb0) | k) != 0));
+                            else umma::mma_i8(tmem, ad + 2u * k, bd + 2u * k, idesc, (uint32_t)(((kb - kb0) | k) != 0));
                         }
                         umma::tc_commit(bar_empty + 8u * s);
                         if (++s == stages) { s = 0; ph ^= 1u; }
@@ -572,11 +586,11 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
             T *phi_out = reinterpret_cast<T *>(a.phi[(pass + 1) & 1]);
             bool checked = false;
             for (int tk = 0; tk < my_tiles; ++tk) {
-                const int lt = (int)blockIdx.x + tk * (int)gridDim.x;
+                const int lt = lt_first + tk * lt_stride;
                 const int tile = a.tile_begin + lt;
                 const int rowl = lt * UMMA_TILE + rowt;
                 const int row = row0 + rowl;
-                const bool valid = row < a.n;
+                const bool valid = row < a.n && lead;          // (only the split-0 CTA of a tile updates its rows)
                 // ---- before the sums exist ----
                 T pre_p[UMMA_RPG], pre_s[UMMA_RPG], pre_c[UMMA_RPG], pre_d[UMMA_RPG];   // phase, sin, cos, h*(-ks shil) + kn xi
                 const int Wi = valid ? a.W[rowl] : 0;
@@ -612,13 +626,68 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     if (prev_scored) umma::named_bar_sync(1, UMMA_EPI_THREADS);
                     checked = true;
                 }
+                int *accrow = S > 1 ? a.acc_g + ((size_t)lt * UMMA_TILE + rowt) * a.NB : nullptr;
+                if (S > 1) {
+                    // ---- split-K: this CTA's partial sums of its K range -> the tile's global accumulator ----
+                    for (int k = 0; k < UMMA_RPG; ++k) {
+                        const int r = group + 4 * k;
+                        if (r >= R) break;
+                        const int dcols = a.dcols, sc = a.score_cols;
+                        int P[2 * UMMA_D9];
+                        if (FP4) {
+#pragma unroll
+                            for (int q4 = 0; q4 < 2 * UMMA_D9; q4 += 4) umma::tmem_ld4(tlane + (uint32_t)(2 * UMMA_D9 * r + q4), P + q4);
+                        } else {
+                            umma::tmem_ld8(tlane + (uint32_t)(8 * r), reinterpret_cast<int (&)[8]>(P));
+                        }
+                        umma::tmem_ld_wait();
+                        for (int q = 0; q < dcols; ++q)
+                            atomicAdd(accrow + dcols * r + q, FP4 ? __float2int_rn(__int_as_float(P[q])) : P[q]);
+                        for (int q = 0; q < sc; ++q) {
+                            int v;
+                            umma::tmem_ld1(tlane + (uint32_t)(dcols * R + r * sc + q), v);
+                            umma::tmem_ld_wait();
+                            atomicAdd(accrow + dcols * R + r * sc + q, FP4 ? __float2int_rn(__int_as_float(v)) : v);
+                        }
+                    }
+                    umma::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) umma::mbar_arrive(bar_tempty);          // the accumulator is free again
+                    ++acc_it;
+                    umma::named_bar_sync(1, UMMA_EPI_THREADS);
+                    if (et == 0) umma::red_release(a.tile_cnt + lt, false); // (cumulative over the CTA barrier: all partials are in)
+                    if (lead) {
+                        if (et == 0) {
+                            const unsigned int want = (unsigned int)S * (unsigned int)(pass + 1);
+                            const long long t_wait = clock64();
+                            while ((int)(umma::ld_acquire(a.tile_cnt + lt, false) - want) < 0) {
+                                if (clock64() - t_wait > a.watchdog_cycles) { atomicMin(a.timeout_flag, (unsigned long long)pass); break; }
+                            }
+                        }
+                        umma::named_bar_sync(1, UMMA_EPI_THREADS);
+                    }
+                }
+                if (S > 1 && !lead) {
+                    if ((flags & 2) && lane == 0)
+                        for (int r = group; r < R; r += 4) en_w[quad * 32 + r] = 0.0;
+                } else {
 #pragma unroll
                 for (int k = 0; k < UMMA_RPG; ++k) {
                     const int r = group + 4 * k;
                     if (r >= R) break;                       // warp uniform
                     int D[2 * UMMA_D9], Dsig = 0;
                     const int dcols = a.dcols;
-                    if (FP4) {
+                    if (S > 1) {
+                        // the tile's complete sums (already integers); zero them for the next pass -- the other splits add
+                        // again only after this pass's grid barrier, which this CTA arrives at after these stores
+                        for (int q = 0; q < dcols; ++q) { D[q] = __ldcg(accrow + dcols * r + q); __stcg(accrow + dcols * r + q, 0); }
+                        const int sc = a.score_cols;
+                        for (int q = 0; q < sc; ++q) {
+                            const int v = __ldcg(accrow + dcols * R + r * sc + q);
+                            __stcg(accrow + dcols * R + r * sc + q, 0);
+                            if (sc == 1 || q == ((flags & 1) ? threshold_state((double)pre_p[k], a.n_states) : 0)) Dsig = v;
+                        }
+                    } else if (FP4) {
 #pragma unroll
                         for (int q4 = 0; q4 < 2 * UMMA_D9; q4 += 4) umma::tmem_ld4(tlane + (uint32_t)(2 * UMMA_D9 * r + q4), D + q4);
                     } else {
@@ -626,7 +695,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     }
                     const T p = pre_p[k], si = pre_s[k], ci = pre_c[k];
                     const int st = (flags & 1) ? threshold_state((double)p, a.n_states) : 0;
-                    if (flags & 1) {
+                    if ((flags & 1) && S == 1) {
                         if (a.n_states == 2) {
                             umma::tmem_ld1(tlane + (uint32_t)(dcols * R + r), Dsig);
                         } else {
@@ -642,7 +711,7 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     umma::tmem_ld_wait();
                     if (a.trace && et == 0 && k == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 4] = clock64();
 
-                    if (FP4) {
+                    if (FP4 && S == 1) {
                         // the mxf4 accumulator is float32 holding exact integers (|sum| < 2^24): back to int
 #pragma unroll
                         for (int q4 = 0; q4 < 2 * UMMA_D9; ++q4) D[q4] = __float2int_rn(__int_as_float(D[q4]));
@@ -707,11 +776,14 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         }
                     }
                 }
+                }   // (leader / unsplit tile)
                 if (a.trace && et == 0 && pass < UMMA_TRACE_PASSES) a.trace[((long long)blockIdx.x * UMMA_TRACE_PASSES + pass) * UMMA_TRACE_SLOTS + 6] = clock64();
-                umma::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) umma::mbar_arrive(bar_tempty);
-                ++acc_it;
+                if (S == 1) {
+                    umma::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) umma::mbar_arrive(bar_tempty);
+                    ++acc_it;
+                }
                 if (flags & 2) {
                     umma::named_bar_sync(1, UMMA_EPI_THREADS);
                     if (et < R) en_acc[et] += ((en_w[et] + en_w[32 + et]) + en_w[64 + et]) + en_w[96 + et];
@@ -757,8 +829,8 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         if (a.flags[a.passes - 1] & 1) {
             const T *phi_fin = reinterpret_cast<const T *>(a.phi[(a.passes - 1) & 1]);
             for (int tk = 0; tk < my_tiles; ++tk) {
-                const int rowl = ((int)blockIdx.x + tk * (int)gridDim.x) * UMMA_TILE + rowt;
-                if (row0 + rowl < a.n)
+                const int rowl = (lt_first + tk * lt_stride) * UMMA_TILE + rowt;
+                if (row0 + rowl < a.n && lead)
                     for (int r = group; r < R; r += 4)
                         if (improved_s[r]) a.best_states[(long long)r * a.ld_phi + rowl] = (uint8_t)threshold_state((double)phi_fin[(long long)r * a.ld_phi + rowl], a.n_states);
             }

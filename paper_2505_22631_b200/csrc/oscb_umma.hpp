@@ -77,7 +77,7 @@ public:
 
     int rows() const;
     float ms = 0.f;
-    int grid = 0, stages = 0;
+    int grid = 0, stages = 0, splits = 1;      // CTAs, ring depth, CTAs sharing one row tile (split-K)
     size_t smem = 0;
     unsigned long long nonfinite = ~0ull;
 

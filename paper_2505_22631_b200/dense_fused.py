@@ -82,6 +82,9 @@ class FusedDenseRank:
         rows = C.c_int64(0)
         nat.lib().oscb_dense_fused_rows(self.handle, C.byref(rows))
         self.rows = int(rows.value)
+        ctas, splits = C.c_int32(0), C.c_int32(0)
+        nat.lib().oscb_dense_fused_grid(self.handle, C.byref(ctas), C.byref(splits))
+        self.ctas, self.splits = int(ctas.value), int(splits.value)      # CTAs of this rank's kernel; CTAs per row tile (split-K)
 
     def close(self):
         if getattr(self, "handle", None):

@@ -302,3 +302,46 @@ def test_watchdog_abandons_a_run_whose_peer_never_arrives(pkg, monkeypatch):
     shards = [(J[0:256], 0, 256, 0), (J[256:512], 256, 512, 0)]
     ok = dense_fused.run_fused_in_process(shards, n, params, [1, 2], pair_count=n * (n - 1) // 2)
     assert ok.steps == 30 and ok.final_phases.shape == (2, n)
+
+
+@pytest.mark.parametrize("splitk", ["2", "4"])
+@pytest.mark.parametrize("precision,fp4", [("f32", "1"), ("f64", "0")])
+def test_split_k_is_bit_identical(pkg, monkeypatch, splitk, precision, fp4):
+    """Split-K (S CTAs share a row tile; partial sums meet in a global int32 accumulator): integer sums do not depend
+    on S, so single-handle runs and 2- / 4-virtual-rank row-sharded runs with split-K on equal the unsplit single-handle
+    run bit for bit -- phases, states, objectives, traces, energies (noise on, both J streams)."""
+    from paper_2505_22631_b200 import dense_fused
+    n, R = 1024, 3
+    J = sk_graph(n, 12)
+    Jd = pkg.CouplingMatrix.from_dense(J, storage="dense")
+    params = pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.2, h=0.01, t_stop=0.8, seed=60)
+    seeds = [60, 61, 62]
+    monkeypatch.setenv("OSCB_UMMA_FP4", fp4)
+    monkeypatch.setenv("OSCB_UMMA_SPLITK", "1")
+    want = pkg.run_batch(Jd, params, "maxcut", seeds, precision=precision, kernel="dense-tc")
+    monkeypatch.setenv("OSCB_UMMA_SPLITK", splitk)
+    got = [pkg.run_batch(Jd, params, "maxcut", seeds, precision=precision, kernel="dense-tc")]
+    for cuts in ((0, 512, 1024), (0, 256, 512, 768, 1024)):
+        shards = [(J[a:b], a, b, 0) for a, b in zip(cuts[:-1], cuts[1:])]
+        got.append(dense_fused.run_fused_in_process(shards, n, params, seeds, pair_count=n * (n - 1) // 2, precision=precision))
+    for g in got:
+        assert g.steps == want.steps == 80
+        for f in ("final_phases", "best_states", "best_objective", "best_trace", "energy"):
+            assert np.array_equal(getattr(g, f), getattr(want, f)), f
+
+
+def test_split_k_fills_the_rank_of_an_8_gpu_run(pkg, monkeypatch):
+    """configs[4] at 8 GPUs: a rank owns 16 of the 128 row tiles of SK 16384.  One CTA per tile would leave 132 SMs idle;
+    the plan splits every tile's K range so that >= 128 CTAs are busy (asserted from the plan, as the 8-GPU node is
+    not available: `gpurun` has one GPU)."""
+    from paper_2505_22631_b200 import dense_fused, workloads
+    monkeypatch.delenv("OSCB_UMMA_SPLITK", raising=False)
+    n, world = 16384, 8
+    rows = n // world
+    J8 = workloads.sk_dense(n)[:rows].astype(np.float64)
+    params = pkg.SolverParams.tuned_for(n, 2, seed=0)
+    rk = dense_fused.FusedDenseRank(J8, n, 0, rows, 0, params, 1, n * (n - 1) // 2, world, 0, steps=4)
+    try:
+        assert rk.rows == rows and rk.splits >= 8 and rk.ctas == 16 * rk.splits >= 128
+    finally:
+        rk.close()
