@@ -151,6 +151,9 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         if (grid == lt) {
             int S = std::min(g->sm_count / std::max(lt, 1), a.ktiles);
             const size_t stream = (size_t)a.ktiles * stage;       // bytes one CTA moves per pass for a whole-K row tile
+            // (measured, one rank of SK 16384 alone on a B200, us per Euler step unsplit -> split: 2-GPU rank 20.4 -> 16.4
+            // at S = 2, 4-GPU rank 20.3 -> 12.7 at S = 4, 8-GPU rank 20.1 -> 10.3 at S = 9; the whole graph on one GPU:
+            // 25.1.  profiles/r02n_dense_rank_emulation.jsonl, tools/dense_rank_emulation.py)
             if (S < 2 || stream < (size_t)512 * 1024) S = 1;
             if (const char *e = getenv("OSCB_UMMA_SPLITK")) S = std::max(1, std::min({atoi(e), g->sm_count / std::max(lt, 1), a.ktiles}));
             a.splits = S;

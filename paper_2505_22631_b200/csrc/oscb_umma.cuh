@@ -91,7 +91,7 @@ struct UmmaArgs {
     unsigned long long *nonfinite;
     long long *trace;         // debug timeline [cta][UMMA_TRACE_PASSES][4] in SM clocks, or null
     int splits;               // split-K: CTAs sharing one row tile (1: a CTA owns whole row tiles).  > 1 only with one unit per CTA
-    int *acc_g;               // split-K: [local tiles][128][NB] int32 partial-sum accumulator (zero between passes)
+    int *acc_g;               // split-K: [local tiles][NB][128] int32 partial-sum accumulator (zero between passes)
     unsigned int *tile_cnt;   // split-K: [local tiles] monotonic count of partials added
     unsigned long long *timeout_flag;  // first pass at which some CTA of this rank gave up waiting for the step barrier (0: none)
     long long watchdog_cycles;         // SM clocks a producer waits for the other CTAs / ranks before it gives up
@@ -626,7 +626,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     if (prev_scored) umma::named_bar_sync(1, UMMA_EPI_THREADS);
                     checked = true;
                 }
-                int *accrow = S > 1 ? a.acc_g + ((size_t)lt * UMMA_TILE + rowt) * a.NB : nullptr;
+                // column-major inside the tile ([col][row]): the 32 lanes of a warp add to 32 consecutive ints, one L2 line
+                int *accrow = S > 1 ? a.acc_g + (size_t)lt * UMMA_TILE * a.NB + rowt : nullptr;
+                auto acc_at = [&](int col) -> int * { return accrow + (size_t)col * UMMA_TILE; };
                 if (S > 1) {
                     // ---- split-K: this CTA's partial sums of its K range -> the tile's global accumulator ----
                     for (int k = 0; k < UMMA_RPG; ++k) {
@@ -642,12 +644,12 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         }
                         umma::tmem_ld_wait();
                         for (int q = 0; q < dcols; ++q)
-                            atomicAdd(accrow + dcols * r + q, FP4 ? __float2int_rn(__int_as_float(P[q])) : P[q]);
+                            atomicAdd(acc_at(dcols * r + q), FP4 ? __float2int_rn(__int_as_float(P[q])) : P[q]);
                         for (int q = 0; q < sc; ++q) {
                             int v;
                             umma::tmem_ld1(tlane + (uint32_t)(dcols * R + r * sc + q), v);
                             umma::tmem_ld_wait();
-                            atomicAdd(accrow + dcols * R + r * sc + q, FP4 ? __float2int_rn(__int_as_float(v)) : v);
+                            atomicAdd(acc_at(dcols * R + r * sc + q), FP4 ? __float2int_rn(__int_as_float(v)) : v);
                         }
                     }
                     umma::tc_fence_before();
@@ -680,11 +682,12 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     if (S > 1) {
                         // the tile's complete sums (already integers); zero them for the next pass -- the other splits add
                         // again only after this pass's grid barrier, which this CTA arrives at after these stores
-                        for (int q = 0; q < dcols; ++q) { D[q] = __ldcg(accrow + dcols * r + q); __stcg(accrow + dcols * r + q, 0); }
+                        for (int q = 0; q < dcols; ++q) D[q] = __ldcg(acc_at(dcols * r + q));
+                        for (int q = 0; q < dcols; ++q) __stcg(acc_at(dcols * r + q), 0);
                         const int sc = a.score_cols;
                         for (int q = 0; q < sc; ++q) {
-                            const int v = __ldcg(accrow + dcols * R + r * sc + q);
-                            __stcg(accrow + dcols * R + r * sc + q, 0);
+                            const int v = __ldcg(acc_at(dcols * R + r * sc + q));
+                            __stcg(acc_at(dcols * R + r * sc + q), 0);
                             if (sc == 1 || q == ((flags & 1) ? threshold_state((double)pre_p[k], a.n_states) : 0)) Dsig = v;
                         }
                     } else if (FP4) {
