@@ -127,23 +127,28 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
     }
 
     // pass B: pairs of the phases in the registers -> the thread's own slots
-    auto pass_b = [&]() {
+    // `with_state`: the next pass A reads lattice states out of these pairs.  N = 2 always carries the state (it is the
+    // cosine's sign bit, three instructions); the N = 3 one-hot bits cost six and are written only when they will be read.
+    const float b0 = a.bnd[0], b1 = a.bnd[1], b2 = a.bnd[2];
+    auto pass_b = [&](bool with_state) {
 #pragma unroll
         for (int t = 0; t < QPT; ++t) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 float s, co;
                 trig_turns_direct(phi[t][k], s, co);
-                if (NMODE == 3) {
+                if (NMODE == 3 && with_state) {
                     const float p = phi[t][k];
-                    const uint32_t oh = (p >= a.bnd[0] && p < a.bnd[1]) ? 2u : ((p >= a.bnd[1] && p < a.bnd[2]) ? 4u : 1u);
+                    uint32_t oh = p >= b0 ? 2u : 1u;
+                    oh = p >= b1 ? 4u : oh;
+                    oh = p >= b2 ? 1u : oh;
                     co = __uint_as_float((__float_as_uint(co) & ~7u) | oh);
                 }
                 *reinterpret_cast<float2 *>(smem_raw + own0 + t * tbytes + k * kbytes) = make_float2(co, s);
             }
         }
     };
-    pass_b();
+    pass_b(true);
     __syncthreads();
 
     const size_t first_row = UNIFORM ? (size_t)warp * 4 : (size_t)a.warp_start[warp];
@@ -171,12 +176,6 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
         const uint4 *po = so;
         const float4 *pw = sw;
         const int stride = a.C;
-        uint4 cur_o = make_uint4(0, 0, 0, 0);
-        float4 cur_w = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!UNIFORM) {
-            cur_o = *po;
-            if (NMODE == 2) cur_w = *pw;
-        }
 #pragma unroll
         for (int t = 0; t < QPT; ++t) {
             float z[4] = {0.f, 0.f, 0.f, 0.f};
@@ -211,14 +210,14 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
                     const int e = t * W4C + k * a.C;
                     group(__ldcg(so + e), NMODE == 2 ? __ldcg(sw + e) : make_float4(0.f, 0.f, 0.f, 0.f));
                 } else {
+                    // (no software prefetch: the stream sits in L1 / L2 and the other warps cover the load; carrying the next
+                    // group in registers cost four moves per group)
                     bool last;
-#pragma unroll 2
                     do {
-                        const uint4 o = cur_o;
-                        const float4 w = cur_w;
+                        const uint4 o = __ldg(po);
+                        const float4 w = NMODE == 2 ? __ldg(pw) : make_float4(0.f, 0.f, 0.f, 0.f);
                         po += stride;
-                        cur_o = *po;
-                        if (NMODE == 2) { pw += stride; cur_w = *pw; }
+                        if (NMODE == 2) pw += stride;
                         // (the flag is the same in all lanes: the vote tells the compiler so -- a uniform branch, no
                         // reconvergence bookkeeping around every row)
                         last = __any_sync(0xffffffffu, (int)o.w < 0);
@@ -238,10 +237,11 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
                 }
             }
             if (MODE != 3) {
-                // wrap (dynamics.py:172): one range check per quad; a huge or non-finite x takes floorf
+                // wrap (dynamics.py:172).  N = 2 (the G81 shape: the MUFU / conversion unit is the busy one): on the ALU, one
+                // range check per quad, a huge or non-finite x takes floorf; N = 3: floorf (fewer instructions, the unit has room)
                 const float big = fmaxf(fmaxf(fabsf(ynew[0]), fabsf(ynew[1])), fmaxf(fabsf(ynew[2]), fabsf(ynew[3])));
                 const float any = (ynew[0] + ynew[1]) + (ynew[2] + ynew[3]);     // NaN iff some x is NaN (fmaxf drops NaNs)
-                if (big < 4194304.0f && any == any) {
+                if (NMODE == 2 && big < 4194304.0f && any == any) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const float w = frac_alu(ynew[k]);
@@ -338,10 +338,10 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
             pass_a(M2{}, step, hks);
         }
         pending = false;
-        pass_b();
-        __syncthreads();
         const bool is_sample = step == next_sample;
         const bool cadence_hit = a.cadence > 0 && cmod == 0;
+        pass_b(is_sample || cadence_hit);
+        __syncthreads();
         cmod = (cmod + 1 == a.cadence) ? 0 : cmod + 1;
         if (is_sample) {
             pending = true;
