@@ -200,11 +200,7 @@ UmmaSession::UmmaSession(oscb_graph *g, const UmmaSpec &spec, int world, int ran
         m->d_timeout.alloc(1);
         a.timeout_flag = m->d_timeout.p;
         if (const char *e = getenv("OSCB_UMMA_WATCHDOG_MS")) m->watchdog_ms = std::max(1, atoi(e));
-        {
-            int khz = 0;
-            OSCB_CUDA(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->device));
-            a.watchdog_cycles = (long long)m->watchdog_ms * (long long)std::max(khz, 100000);     // ms x cycles per ms
-        }
+        a.watchdog_ns = (long long)m->watchdog_ms * 1000000ll;      // (%globaltimer: no clock-rate query -- that one costs tens of ms)
         OSCB_CUDA(cudaEventCreate(&m->ev0));
         OSCB_CUDA(cudaEventCreate(&m->ev1));
     } catch (...) {

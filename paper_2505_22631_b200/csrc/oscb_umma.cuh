@@ -94,7 +94,7 @@ struct UmmaArgs {
     int *acc_g;               // split-K: [local tiles][NB][128] int32 partial-sum accumulator (zero between passes)
     unsigned int *tile_cnt;   // split-K: [local tiles] monotonic count of partials added
     unsigned long long *timeout_flag;  // first pass at which some CTA of this rank gave up waiting for the step barrier (0: none)
-    long long watchdog_cycles;         // SM clocks a producer waits for the other CTAs / ranks before it gives up
+    long long watchdog_ns;             // nanoseconds (%globaltimer) a CTA waits for the other CTAs / ranks before it gives up
 };
 
 namespace umma {
@@ -300,6 +300,12 @@ __device__ __forceinline__ void write_b(uint8_t *Bimg, int NB, int R, int kb, in
     }
 }
 
+__device__ __forceinline__ long long global_ns()
+{
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ unsigned int ld_acquire(const unsigned int *p, bool sys)
 {
     unsigned int v;
@@ -511,9 +517,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                         // watchdog: a peer rank that never launched (or died) must not hang this GPU.  After the
                         // deadline the run is abandoned -- the flag makes finish() fail -- and the kernel free-runs
                         // through its remaining passes without waiting, so it terminates.
-                        const long long t_wait = clock64();
+                        const long long t_wait = umma::global_ns();
                         while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) {
-                            if (clock64() - t_wait > a.watchdog_cycles) {
+                            if (umma::global_ns() - t_wait > a.watchdog_ns) {
                                 dead = true;
                                 atomicMin(a.timeout_flag, (unsigned long long)pass);
                                 break;
@@ -661,9 +667,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
                     if (lead) {
                         if (et == 0) {
                             const unsigned int want = (unsigned int)S * (unsigned int)(pass + 1);
-                            const long long t_wait = clock64();
+                            const long long t_wait = umma::global_ns();
                             while ((int)(umma::ld_acquire(a.tile_cnt + lt, false) - want) < 0) {
-                                if (clock64() - t_wait > a.watchdog_cycles) { atomicMin(a.timeout_flag, (unsigned long long)pass); break; }
+                                if (umma::global_ns() - t_wait > a.watchdog_ns) { atomicMin(a.timeout_flag, (unsigned long long)pass); break; }
                             }
                         }
                         umma::named_bar_sync(1, UMMA_EPI_THREADS);
@@ -815,9 +821,9 @@ __global__ void __launch_bounds__(UMMA_THREADS, 1) k_dense_umma(const UmmaArgs a
         // the last pass scored the final phases: wait for every rank's totals, then keep the states
         if (et == 0) {
             const unsigned int target = a.ctas_total * (unsigned int)a.passes;
-            const long long t_wait = clock64();
+            const long long t_wait = umma::global_ns();
             while ((int)(umma::ld_acquire(a.bar[a.rank], sys) - target) < 0) {
-                if (clock64() - t_wait > a.watchdog_cycles) {        // (same watchdog as the producer's)
+                if (umma::global_ns() - t_wait > a.watchdog_ns) {        // (same watchdog as the producer's)
                     atomicMin(a.timeout_flag, (unsigned long long)a.passes);
                     break;
                 }
