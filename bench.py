@@ -608,7 +608,7 @@ def main():
                     help="Euler steps per bench step; 0 = the workload's whole default schedule ceil(t_stop / h) "
                          "(dense SK workloads: 1024)")
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"])
-    ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "resident"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "stream", "resident", "lowdeg", "cluster"])
     ap.add_argument("--replicas", type=int, default=0, help="override replicas per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],

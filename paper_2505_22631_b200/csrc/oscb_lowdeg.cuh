@@ -47,6 +47,7 @@ struct LowdegArgs {
     double target, w_total;
     const uint32_t *quad_of;        // [Qp] quad at a position; >= Q: none (ghost item)
     const uint4 *soff;              // byte offsets of a group's four neighbour slots (replica 0 of the tile)
+    const uint2 *sidx;              // k_lowdeg_pair: the same groups as 4 x u16 SLOT numbers (bit 15 of the 4th: last group of the row)
     const float4 *swt;              // N = 2: their couplings
     const int *warp_start;          // looped streams: first group row of each warp
     const float *hks_table;         // [steps + 1]  h ks(step) (x2 for N = 2), float64 on the host
@@ -367,6 +368,297 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
                 const uint32_t i = 4u * q + k;
                 if (q < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)rg * a.n + i] = (double)phi[t][k];
             }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------------------------
+// k_lowdeg_pair -- the same register-resident design for N = 2 max-cut at ANY degree, two replicas per lane.
+//
+// k_resident_fast spends more on a row's bookkeeping (row table, group counts, phases through L2, staged pairs, a
+// pass-B copy: ~100 lane-instructions per replica-oscillator on the G22 shape) than on its 20 gathers (~78).  Here the
+// per-oscillator part is k_lowdeg's (phases in registers, trig after the barrier, ~30), and the gather keeps what makes
+// k_resident_fast's cheap: a lane owns TWO adjacent replicas, so one LDS.128 fetches both (cos, sin) pairs of a
+// neighbour and the stream words, the address add and the loop control are shared by two updates.  Looped stream
+// only (rows of any degree); UNITW: unit couplings -- plain packed adds, and the coupling stream is read only on the
+// steps that read the cut out (it carries the zeros that keep padding out of the count).
+template <int QPT, bool UNITW>
+__global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(const LowdegArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int LPS = a.RT >> 1;                                       // lanes per slot
+    const int q = lane & (LPS - 1), c = lane >> (a.LRT - 1);
+    const int r0 = 2 * q;
+    const int tile = blockIdx.x, rg0 = tile * a.RT + r0;
+    const bool live[2] = {rg0 < a.R_real, rg0 + 1 < a.R_real};
+    const unsigned char *cs_lane = smem_raw + r0 * 8;                // + slot byte offset: the pairs of replicas r0, r0 + 1
+    const int WC = a.W * a.C;
+    const int pos0 = warp * a.C + c;
+    const uint32_t kbytes = (uint32_t)a.Qp * a.RT * 8;
+    const uint32_t tbytes = (uint32_t)WC * a.RT * 8;
+    const uint32_t own0 = (uint32_t)(pos0 * a.RT + r0) * 8;
+    int *cnt = reinterpret_cast<int *>(smem_raw + a.off_cnt);
+    double *part = reinterpret_cast<double *>(smem_raw + a.off_part);
+    double *best_s = reinterpret_cast<double *>(smem_raw + a.off_misc);
+    int *improved_s = reinterpret_cast<int *>(smem_raw + a.off_misc + a.RT * 8);
+    // (c0, s0, c1, s1) of the two replicas of this lane at a slot
+    const uint32_t slot_bytes = (uint32_t)a.RT * 8u;
+    auto pairs_at = [&](uint32_t slot) -> float4 { return *reinterpret_cast<const float4 *>(cs_lane + slot * slot_bytes); };
+    auto quad = [&](int t) -> uint32_t { return __ldg(a.quad_of + pos0 + t * WC); };
+
+    float phi[QPT][4][2];
+#pragma unroll
+    for (int t = 0; t < QPT; ++t) {
+        const uint32_t qd = quad(t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = 4u * qd + k;
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                phi[t][k][e] = (qd < (uint32_t)a.Q && i < (uint32_t)a.n && live[e]) ? (float)a.io[(size_t)(rg0 + e) * a.n + i] : 0.0f;
+        }
+    }
+    uint2 key[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const uint64_t seed = a.seeds[rg0 + e];
+        key[e] = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    }
+    for (int i = tid; i < OSCB_LD_PADS * a.RT; i += blockDim.x)
+        reinterpret_cast<float2 *>(smem_raw + (size_t)4 * kbytes)[i] = make_float2(0.0f, 0.0f);
+    if (tid < a.RT) {
+        best_s[tid] = a.best_obj[tile * a.RT + tid];
+        improved_s[tid] = 0;
+        cnt[tid] = 0;
+    }
+    auto pass_b = [&]() {
+#pragma unroll
+        for (int t = 0; t < QPT; ++t)
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                float s0, c0, s1, c1;
+                trig_turns_direct(phi[t][k][0], s0, c0);
+                trig_turns_direct(phi[t][k][1], s1, c1);
+                *reinterpret_cast<float4 *>(smem_raw + own0 + t * tbytes + k * kbytes) = make_float4(c0, s0, c1, s1);
+            }
+    };
+    pass_b();
+    __syncthreads();
+
+    const size_t first_row = (size_t)a.warp_start[warp];
+    // the stream as u16 slot numbers: 8 B per group, ~100 KB per step on the G22 shape -- it stays in the L1 the 132 KB
+    // shared-memory configuration leaves (the u32-offset form, 200 KB, thrashed it: every group waited on L2)
+    const uint2 *so = a.sidx + first_row * a.C + c;
+    const float4 *sw = a.swt + first_row * a.C + c;
+
+    bool pending = true;
+    int pending_col = 0, pending_label = -1, sample_cur = 0;
+    while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < a.step_begin) ++sample_cur;
+    int next_sample = sample_cur < a.n_sample_steps ? a.sample_steps[sample_cur] : -1;
+    int cmod = a.cadence > 0 ? a.step_begin % a.cadence : 1;
+
+    auto pass_a = [&](auto mode_tag, int step, float hks) {
+        constexpr int MODE = decltype(mode_tag)::value;
+        constexpr bool USE_W = !UNITW || MODE >= 1;
+        float S[2] = {0.f, 0.f};
+        double en[2] = {0.0, 0.0};
+        bool bad = false;
+        const uint2 *po = so;
+        const float4 *pw = sw;
+        const int stride = a.C;
+        uint2 nxt = __ldg(po);               // the slot numbers run one group ahead of their use (the last group of a warp's
+                                             // stream prefetches the pad row behind it)
+#pragma unroll
+        for (int t = 0; t < QPT; ++t) {
+            float z[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+            if (MODE != 3 && a.noise_on) {
+                const uint32_t qd = quad(t);
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    normals4_fast(philox4x32_10(make_uint4(qd, (uint32_t)step, 0u, 0x6F736362u), key[e]), z[e][0], z[e][1], z[e][2], z[e][3]);
+            }
+            float ynew[4][2];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float4 own = *reinterpret_cast<const float4 *>(smem_raw + own0 + t * tbytes + k * kbytes);
+                float2 sum0 = make_float2(0.f, 0.f), sum1 = make_float2(0.f, 0.f);
+                float ts0 = 0.f, ts1 = 0.f;
+                // The adds of a group run one group behind its loads: while the four LDS.128 of group g are in flight the
+                // packed adds of group g - 1 issue (a warp issues in order, so without this every group paid the full
+                // shared-memory latency before its first add).
+                float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, p2 = p0, p3 = p0;
+                float4 pwt = make_float4(0.f, 0.f, 0.f, 0.f);
+                auto accumulate = [&](const float4 &v0, const float4 &v1, const float4 &v2, const float4 &v3, const float4 &w) {
+                    if (USE_W) {
+                        sum0 = __ffma2_rn(make_float2(w.x, w.x), make_float2(v0.x, v0.y), sum0);
+                        sum1 = __ffma2_rn(make_float2(w.x, w.x), make_float2(v0.z, v0.w), sum1);
+                        sum0 = __ffma2_rn(make_float2(w.y, w.y), make_float2(v1.x, v1.y), sum0);
+                        sum1 = __ffma2_rn(make_float2(w.y, w.y), make_float2(v1.z, v1.w), sum1);
+                        sum0 = __ffma2_rn(make_float2(w.z, w.z), make_float2(v2.x, v2.y), sum0);
+                        sum1 = __ffma2_rn(make_float2(w.z, w.z), make_float2(v2.z, v2.w), sum1);
+                        sum0 = __ffma2_rn(make_float2(w.w, w.w), make_float2(v3.x, v3.y), sum0);
+                        sum1 = __ffma2_rn(make_float2(w.w, w.w), make_float2(v3.z, v3.w), sum1);
+                    } else {
+                        sum0 = __fadd2_rn(sum0, __fadd2_rn(__fadd2_rn(make_float2(v0.x, v0.y), make_float2(v1.x, v1.y)),
+                                                           __fadd2_rn(make_float2(v2.x, v2.y), make_float2(v3.x, v3.y))));
+                        sum1 = __fadd2_rn(sum1, __fadd2_rn(__fadd2_rn(make_float2(v0.z, v0.w), make_float2(v1.z, v1.w)),
+                                                           __fadd2_rn(make_float2(v2.z, v2.w), make_float2(v3.z, v3.w))));
+                    }
+                    if (MODE >= 1) {
+                        ts0 += (xor_sign(w.x, v0.x) + xor_sign(w.y, v1.x)) + (xor_sign(w.z, v2.x) + xor_sign(w.w, v3.x));
+                        ts1 += (xor_sign(w.x, v0.z) + xor_sign(w.y, v1.z)) + (xor_sign(w.z, v2.z) + xor_sign(w.w, v3.z));
+                    }
+                };
+                bool last;
+#pragma unroll 2
+                do {
+                    const uint2 o = nxt;
+                    po += stride;
+                    nxt = __ldg(po);
+                    float4 w = make_float4(1.f, 1.f, 1.f, 1.f);
+                    if (USE_W) { w = __ldg(pw); }
+                    pw += stride;
+                    last = __any_sync(0xffffffffu, (int)o.y < 0);
+                    const float4 v0 = pairs_at(o.x & 0xffffu), v1 = pairs_at(o.x >> 16);
+                    const float4 v2 = pairs_at(o.y & 0xffffu), v3 = pairs_at((o.y >> 16) & 0x7fffu);
+                    accumulate(p0, p1, p2, p3, pwt);
+                    p0 = v0; p1 = v1; p2 = v2; p3 = v3; pwt = w;
+                } while (!last);
+                accumulate(p0, p1, p2, p3, pwt);
+                if (MODE >= 1) { S[0] += xor_sign(ts0, own.x); S[1] += xor_sign(ts1, own.z); }
+                if (MODE >= 2) {
+                    en[0] += (double)own.x * (double)sum0.x + (double)own.y * (double)sum0.y;
+                    en[1] += (double)own.z * (double)sum1.x + (double)own.w * (double)sum1.y;
+                }
+                if (MODE != 3) {
+                    const float acc0 = own.y * sum0.x - own.x * sum0.y, acc1 = own.w * sum1.x - own.z * sum1.y;   // dynamics.py:170
+                    ynew[k][0] = fmaf(a.hK, acc0, fmaf(-hks, own.y * own.x, fmaf(a.knsh, z[0][k], phi[t][k][0])));
+                    ynew[k][1] = fmaf(a.hK, acc1, fmaf(-hks, own.w * own.z, fmaf(a.knsh, z[1][k], phi[t][k][1])));
+                }
+            }
+            if (MODE != 3) {
+                float chk = 0.f;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const float w = ynew[k][e] - floorf(ynew[k][e]);                  // dynamics.py:172
+                        const float y = (w >= 1.0f) ? 0.0f : w;
+                        phi[t][k][e] = y;
+                        chk += y;
+                    }
+                bad = bad || !(chk == chk);
+            }
+        }
+        if (MODE != 3 && bad) {
+#pragma unroll
+            for (int t = 0; t < QPT; ++t)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (!(phi[t][k][e] == phi[t][k][e]) && live[e] && quad(t) < (uint32_t)a.Q)
+                            flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)(rg0 + e), 4u * quad(t) + k);
+        }
+        if (MODE >= 1) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                int v = __float2int_rn(S[e]);
+                for (int off = 16; off >= LPS; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane < LPS) atomicAdd(&cnt[2 * lane + e], v);
+                if (MODE >= 2) {
+                    double x = 0.5 * en[e];
+                    for (int off = 16; off >= LPS; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
+                    if (lane < LPS) part[warp * a.RT + 2 * lane + e] = x;
+                }
+            }
+            __syncthreads();
+            if (tid < a.RT) {
+                const int tot = cnt[tid];
+                cnt[tid] = 0;
+                const double obj = (a.w_total - (double)tot) * 0.25;
+                const double b = best_s[tid];
+                const bool better = obj > b;                                  // strict: dynamics.py:370-375
+                improved_s[tid] = better ? 1 : 0;
+                const int gi = tile * a.RT + tid;
+                if (better) {
+                    best_s[tid] = obj;
+                    if (a.use_target && a.first_hit[gi] < 0 && obj >= a.target) a.first_hit[gi] = pending_label;
+                }
+                if (MODE >= 2 && pending_col >= 0) {
+                    double en_tot = 0.0;
+                    for (int w = 0; w < a.W; ++w) en_tot += part[w * a.RT + tid];
+                    a.energy[(size_t)gi * a.trace_stride + pending_col] = en_tot;
+                    a.best_trace[(size_t)gi * a.trace_stride + pending_col] = best_s[tid];
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                if (improved_s[r0 + e] && live[e]) {
+#pragma unroll
+                    for (int t = 0; t < QPT; ++t) {
+                        const uint32_t qd = quad(t);
+                        if (qd < (uint32_t)a.Q) {
+                            uint32_t packed = 0;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const float4 own = *reinterpret_cast<const float4 *>(smem_raw + own0 + t * tbytes + k * kbytes);
+                                packed |= (__float_as_uint(e ? own.z : own.x) >> 31) << (8 * k);
+                            }
+                            *reinterpret_cast<uint32_t *>(a.best_states + (size_t)(rg0 + e) * a.n4 + 4u * qd) = packed;
+                        }
+                    }
+                }
+            }
+        }
+    };
+    using M0 = std::integral_constant<int, 0>;
+    using M1 = std::integral_constant<int, 1>;
+    using M2 = std::integral_constant<int, 2>;
+    using M3 = std::integral_constant<int, 3>;
+#pragma unroll 1
+    for (int step = a.step_begin; step < a.step_end; ++step) {
+        const float hks = __ldg(a.hks_table + (step - a.step_begin));
+        if (!pending) {
+            pass_a(M0{}, step, hks);
+            __syncthreads();
+        } else if (pending_col < 0) {
+            pass_a(M1{}, step, hks);
+        } else {
+            pass_a(M2{}, step, hks);
+        }
+        pending = false;
+        pass_b();
+        __syncthreads();
+        const bool is_sample = step == next_sample;
+        const bool cadence_hit = a.cadence > 0 && cmod == 0;
+        cmod = (cmod + 1 == a.cadence) ? 0 : cmod + 1;
+        if (is_sample) {
+            pending = true;
+            pending_col = 1 + sample_cur;
+            pending_label = step;
+            ++sample_cur;
+            next_sample = sample_cur < a.n_sample_steps ? a.sample_steps[sample_cur] : -1;
+        } else if (cadence_hit) {
+            pending = true;
+            pending_col = -1;
+            pending_label = step;
+        }
+    }
+    if (pending) pass_a(M3{}, a.step_end, 0.0f);
+
+    if (tid < a.RT) a.best_obj[tile * a.RT + tid] = best_s[tid];
+#pragma unroll
+    for (int t = 0; t < QPT; ++t) {
+        const uint32_t qd = quad(t);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = 4u * qd + k;
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+                if (live[e] && qd < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)(rg0 + e) * a.n + i] = (double)phi[t][k][e];
         }
     }
 }

@@ -19,6 +19,7 @@ namespace oscb {
 
 struct LowdegShape {
     int RT = 1, LRT = 0, C = 32, W = 1, QPT = 1, Q = 0, Qp = 0;
+    int rpl = 1;                 // replicas per lane: 2 = k_lowdeg_pair (N = 2, looped stream)
     bool uniform = true;
     size_t smem = 0;
     double cost = 0.0;
@@ -42,6 +43,7 @@ struct LowdegPlan {
     double w_total = 0.0;
     DevBuf<uint32_t> quad_of;
     DevBuf<uint4> soff;
+    DevBuf<uint2> sidx;          // two-replica form: u16 slot numbers
     DevBuf<float4> swt;
     DevBuf<int> warp_start;
 };
@@ -96,11 +98,38 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
     out->real = 0;
     out->warp_start.assign(W, 0);
     out->warp_groups.assign(W, 0);
-    // one group entry of slot c: neighbours [4 g, 4 g + 4) of row i
+    // Looped streams: the slots that share a 128-byte shared-memory wavefront (H = 128 / (RT * 8) consecutive slots) should
+    // read different bank classes (slot number mod H) at the same position, so the neighbours of the row in slot c are
+    // visited starting with class c mod H and rotating (G22 shape, 8 replicas per tile: 1.40 -> ~1.1 wavefronts per ideal one).
+    // Uniform streams keep the CSR order (lattice-like graphs gather from neighbouring slots as they are), and so does the
+    // one-replica-per-lane kernel.  Float32 sums depend on the order, so k_lowdeg_pair's last bits depend on the tile shape
+    // (like k_resident_fast's); the float64 parity mode always sums in CSR order.
+    const int H = std::max(1, std::min(C, 128 / (RT * 8)));
+    std::vector<std::vector<int>> perms(C);       // per slot of the current warp-row: CSR positions of its row in visiting order
+    auto visit_order = [&](int i, int c) {
+        std::vector<int> &perm = perms[c];
+        perm.resize(deg(i));
+        std::iota(perm.begin(), perm.end(), indptr[i]);
+        if (s.uniform || H < 2 || s.rpl != 2) return;      // (one replica per lane keeps the CSR order: its results then do not depend on the tile shape)
+        std::vector<std::vector<int>> bucket(H);
+        for (int e : perm) bucket[out->slot_of[indices[e]] % H].push_back(e);
+        size_t at = 0;
+        for (int round = 0; at < perm.size(); ++round) {
+            // position p prefers class (c + p) mod H; when that class has run dry take the fullest one
+            int cls = (c + round) % H;
+            if (bucket[cls].empty())
+                for (int k = 0; k < H; ++k)
+                    if (bucket[k].size() > bucket[cls].size()) cls = k;
+            perm[at++] = bucket[cls].front();
+            bucket[cls].erase(bucket[cls].begin());
+        }
+    };
+    // one group entry of slot c: neighbours [4 g, 4 g + 4) of row i in visiting order
     auto emit = [&](int i, int g, int c, bool last) {
+        if (i >= 0 && g == 0) visit_order(i, c);
         for (int u = 0; u < 4; ++u) {
-            const int e = (i >= 0 && i < n) ? indptr[i] + 4 * g + u : -1;
-            const bool real = e >= 0 && e < indptr[i + 1];
+            const bool real = i >= 0 && i < n && 4 * g + u < deg(i);
+            const int e = real ? perms[c][4 * g + u] : -1;
             uint32_t o = real ? (uint32_t)(out->slot_of[indices[e]] * RT * 8) : pad_off(c);
             if (u == 3 && last) o |= 0x80000000u;
             out->off.push_back(o);
@@ -175,8 +204,7 @@ static bool choose_lowdeg_shape(const oscb_graph *g, const oscb_run_params *p, i
     int nmode;
     if (!lowdeg_kind(g, p, &nmode)) return false;
     // low degree: the instruction count per row is what matters; k_resident_fast wins from ~degree 10 on
-    if (g->max_degree > 16) return false;
-    if (!forced && (double)g->nnz / (double)g->n > 8.0) return false;
+    if (!forced && (g->max_degree > 16 || (double)g->nnz / (double)g->n > 8.0)) return false;
     const bool uniform = g->max_degree <= 4;
     const int Q = (int)((g->n + 3) / 4);
     double best = std::numeric_limits<double>::infinity();
@@ -185,19 +213,26 @@ static bool choose_lowdeg_shape(const oscb_graph *g, const oscb_run_params *p, i
     int want_rt = p->replicas_per_cta, want_qpt = 0;
     if (const char *e = getenv("OSCB_LOWDEG_RT")) { if (want_rt <= 0) want_rt = atoi(e); }
     if (const char *e = getenv("OSCB_LOWDEG_QPT")) want_qpt = atoi(e);
+    int want_rpl = 0;
+    if (const char *e = getenv("OSCB_LOWDEG_RPL")) want_rpl = atoi(e);
     for (int l = 5; l >= 0; --l) {
         const int RT = 1 << l;
         if (want_rt > 0 && RT != want_rt) continue;
         if (want_rt <= 0 && RT > 1 && RT / 2 >= R) continue;      // do not pad a tile more than 2x
-        const int C = 32 / RT;
+      for (int rpl = 1; rpl <= 2; ++rpl) {
+        // two replicas per lane (k_lowdeg_pair): N = 2 on a looped stream, tiles of an even number of replicas
+        if (rpl == 2 && (nmode != 2 || uniform || RT < 2)) continue;
+        if (want_rpl > 0 && rpl != want_rpl) continue;
+        const int C = 32 * rpl / RT;
         const int rows = (Q + C - 1) / C;
         for (int QPT : kLowdegQpt) {
             if (want_qpt > 0 && QPT != want_qpt) continue;
-            const int maxW = lowdeg_max_threads(QPT) / 32;
+            if (rpl == 2 && QPT > 5) continue;
+            const int maxW = lowdeg_max_threads(rpl * QPT) / 32;
             const int W = (rows + QPT - 1) / QPT;
             if (W > maxW || W < 1) continue;
             LowdegShape s;
-            s.RT = RT; s.LRT = l; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = uniform;
+            s.RT = RT; s.LRT = l; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = uniform; s.rpl = rpl;
             s.smem = lowdeg_smem_bytes(s, nullptr, nullptr, nullptr);
             if (s.smem > (size_t)g->smem_optin) continue;
             // work of one CTA in warp-rows (idle lanes and ghost items included), CTAs resident per SM, and the
@@ -214,16 +249,18 @@ static bool choose_lowdeg_shape(const oscb_graph *g, const oscb_run_params *p, i
             // few resident warps cannot hide the shared-memory and MUFU latencies
             const double warps_resident = (double)per_sm * W;
             const double occ = warps_resident >= 16 ? 1.0 : std::sqrt(16.0 / warps_resident);
-            s.cost = (double)waves * (double)per_sm * (double)W * QPT * pad * occ;
+            // (a warp-row of two-replica lanes does the gathers of twice the replicas for ~1.2-1.5x the instructions: measured ahead of one replica per lane on every looped N = 2 graph tried)
+            s.cost = (double)waves * (double)per_sm * (double)W * QPT * pad * occ * (rpl == 2 ? 1.2 : 1.0);
             if (s.cost < best - 1e-9) { best = s.cost; *out = s; found = true; }
         }
+      }
     }
     return found;
 }
 
 static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegShape &s, int nmode)
 {
-    const uint64_t key = (1ull << 63) | ((uint64_t)s.RT << 40) | ((uint64_t)s.W << 24) | ((uint64_t)s.QPT << 8) | (uint64_t)nmode;
+    const uint64_t key = (1ull << 63) | ((uint64_t)s.rpl << 48) | ((uint64_t)s.RT << 40) | ((uint64_t)s.W << 24) | ((uint64_t)s.QPT << 8) | (uint64_t)nmode;
     auto it = g->lowdeg_plans.find(key);
     if (it != g->lowdeg_plans.end()) return it->second;
     auto plan = std::make_shared<LowdegPlan>();
@@ -240,6 +277,20 @@ static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegSh
     plan->quad_of.alloc(h.quad_of.size());
     plan->quad_of.upload(h.quad_of.data(), h.quad_of.size(), st);
     const size_t entries = h.off.size() / 4;
+    std::vector<uint2> idx16;
+    if (s.rpl == 2) {
+        OSCB_REQUIRE((size_t)4 * s.Qp + OSCB_LD_PADS <= 32768, "internal: k_lowdeg_pair slot numbers exceed 15 bits");
+        idx16.resize(entries);
+        const uint32_t sb = (uint32_t)s.RT * 8u;
+        for (size_t e = 0; e < entries; ++e) {
+            uint32_t id[4];
+            for (int u = 0; u < 4; ++u) id[u] = (h.off[4 * e + u] & 0x7fffffffu) / sb;
+            if (h.off[4 * e + 3] & 0x80000000u) id[3] |= 0x8000u;
+            idx16[e] = make_uint2(id[0] | (id[1] << 16), id[2] | (id[3] << 16));
+        }
+        plan->sidx.alloc(entries);
+        plan->sidx.upload(idx16.data(), entries, st);
+    }
     plan->soff.alloc(entries);
     plan->soff.upload(reinterpret_cast<const uint4 *>(h.off.data()), entries, st);
     if (nmode == 2) {
@@ -274,6 +325,22 @@ static void launch_lowdeg(oscb_graph *g, const LowdegArgs &a, const LowdegShape 
     case 7: go(k_lowdeg<NMODE, 7, UNIFORM, RT1>); break;
     case 10: go(k_lowdeg<NMODE, 10, UNIFORM, RT1>); break;
     default: OSCB_REQUIRE(false, "internal: no lowdeg instantiation for %d items per thread", s.QPT);
+    }
+}
+
+template <bool UNITW>
+static void launch_lowdeg_pair(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles)
+{
+    auto go = [&](auto kernel) {
+        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem));
+        kernel<<<tiles, s.W * 32, s.smem, g->stream>>>(a);
+    };
+    switch (s.QPT) {
+    case 1: go(k_lowdeg_pair<1, UNITW>); break;
+    case 2: go(k_lowdeg_pair<2, UNITW>); break;
+    case 4: go(k_lowdeg_pair<4, UNITW>); break;
+    case 5: go(k_lowdeg_pair<5, UNITW>); break;
+    default: OSCB_REQUIRE(false, "internal: no k_lowdeg_pair instantiation for %d items per thread", s.QPT);
     }
 }
 
@@ -334,7 +401,7 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     a.maximize = maximize; a.use_target = p->use_target; a.n_sample_steps = (int)sample_steps.size();
     a.step_begin = (int)p->first_step; a.step_end = (int)(p->first_step + steps); a.cadence = (int)cadence; a.trace_stride = S;
     a.target = p->target_objective; a.w_total = plan->w_total;
-    a.quad_of = plan->quad_of.p; a.soff = plan->soff.p; a.swt = plan->swt.p; a.warp_start = plan->warp_start.p;
+    a.quad_of = plan->quad_of.p; a.soff = plan->soff.p; a.sidx = plan->sidx.p; a.swt = plan->swt.p; a.warp_start = plan->warp_start.p;
     a.hks_table = d_hks.p; a.seeds = d_seeds.p; a.sample_steps = d_samples.p;
     if (nmode == 3) fast_state_boundaries(3, a.bnd);
     a.io = d_io.p; a.best_obj = d_best.p; a.energy = d_energy.p; a.best_trace = d_btrace.p; a.best_states = d_best_states.p;
@@ -351,7 +418,9 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
         else if (sh.uniform) launch_lowdeg<NM, true, false>(g, a, sh, tiles);
         else launch_lowdeg<NM, false, false>(g, a, sh, tiles);
     };
-    if (nmode == 2) by_shape(std::integral_constant<int, 2>{}); else by_shape(std::integral_constant<int, 3>{});
+    if (sh.rpl == 2) { if (g->unit_weights) launch_lowdeg_pair<true>(g, a, sh, tiles); else launch_lowdeg_pair<false>(g, a, sh, tiles); }
+    else if (nmode == 2) by_shape(std::integral_constant<int, 2>{});
+    else by_shape(std::integral_constant<int, 3>{});
     OSCB_CUDA(cudaEventRecord(ev1, s));
     {
         cudaError_t e = cudaGetLastError();
