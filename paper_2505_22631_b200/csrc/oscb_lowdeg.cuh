@@ -663,4 +663,5 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
     }
 }
 
+
 } // namespace oscb
