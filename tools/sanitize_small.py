@@ -5,7 +5,7 @@ import numpy as np
 import paper_2505_22631_b200 as pkg
 from paper_2505_22631_b200 import dynamics, workloads
 
-which = sys.argv[1:] or ["resident", "cluster", "stream", "dense-tc"]
+which = sys.argv[1:] or ["resident", "cluster", "stream", "dense-tc", "lowdeg", "dense-splitk"]
 u, v, w = workloads.random_gnm(128, 700, seed=1, weights=(1.0,))
 J = pkg.CouplingMatrix.from_edges(128, (u, v, w))
 p = pkg.SolverParams.tuned_for(128, 2, seed=0, t_stop=0.6)
@@ -26,4 +26,30 @@ if "dense-tc" in which:
     g = dynamics.DeviceGraph.from_dense(0, U + U.T)
     b = pkg.run_batch(None, pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.1, h=0.01, t_stop=0.3, seed=0), "maxcut", [0, 1, 2], graph=g)
     print("dense-tc", b.kernel, b.best_objective.max())
+    g.close()
+if "lowdeg" in which:
+    # straight-line stream (torus, one and several replicas per CTA), looped stream (N = 3; N = 2 = the two-replica-per-lane kernel)
+    ut, vt, wt = workloads.torus_pm1(10, 20, seed=2)
+    Jt = pkg.CouplingMatrix.from_edges(200, (ut, vt, wt))
+    pt = pkg.SolverParams.tuned_for(200, 2, seed=0, t_stop=0.4)
+    for rt in (1, 8):
+        b = pkg.run_batch(Jt, pt, "maxcut", list(range(11)), kernel="lowdeg", replicas_per_cta=rt)
+        print("lowdeg uniform rt", rt, b.kernel, b.best_objective.max())
+    us, vs, ws = workloads.random_gnm(203, 520, seed=5, weights=(1.0, -1.0, 2.0))
+    Js = pkg.CouplingMatrix.from_edges(203, (us, vs, ws))
+    for rt in (1, 4):
+        b = pkg.run_batch(Js, pkg.SolverParams.tuned_for(203, 2, seed=0, t_stop=0.4), "maxcut", list(range(9)), kernel="lowdeg", replicas_per_cta=rt)
+        print("lowdeg looped N=2 rt", rt, b.kernel, b.best_objective.max())
+    uc, vc, wc = workloads.random_gnm(203, 480, seed=6)
+    Jc = pkg.CouplingMatrix.from_edges(203, (uc, vc, wc))
+    b = pkg.run_batch(Jc, pkg.SolverParams.tuned_for(203, 3, seed=0, t_stop=0.4), "coloring", list(range(37)), kernel="lowdeg")
+    print("lowdeg looped N=3", b.kernel, b.replicas_per_cta, b.best_objective.min())
+if "dense-splitk" in which:
+    import os
+    os.environ["OSCB_UMMA_SPLITK"] = "4"
+    rng = np.random.default_rng(4)
+    U = np.triu(rng.choice(np.array([-1.0, 1.0]), size=(512, 512)), 1)
+    g = dynamics.DeviceGraph.from_dense(0, U + U.T)
+    b = pkg.run_batch(None, pkg.SolverParams(K=0.02, ks_max=1.0, ks_period=0.5, kn=0.1, h=0.01, t_stop=0.3, seed=0), "maxcut", [0, 1, 2], graph=g)
+    print("dense-tc split-K", b.kernel, b.best_objective.max())
     g.close()
