@@ -40,6 +40,7 @@ struct LowdegArgs {
     int n, Q, Qp, RT, LRT, C, W, R_real;
     int n4;                         // row pitch of best_states: 4 * Q
     uint32_t off_cnt, off_part, off_misc;      // (the pairs start at shared offset 0)
+    uint32_t off_ids, n_ids;                   // k_lowdeg_pair with its slot stream staged in shared memory: offset, entries (uint2)
     float hK, knsh;
     int noise_on, maximize, use_target, n_sample_steps;
     int step_begin, step_end, cadence;
@@ -382,7 +383,9 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
 // neighbour and the stream words, the address add and the loop control are shared by two updates.  Looped stream
 // only (rows of any degree); UNITW: unit couplings -- plain packed adds, and the coupling stream is read only on the
 // steps that read the cut out (it carries the zeros that keep padding out of the count).
-template <int QPT, bool UNITW>
+// IDS: the slot stream is staged in shared memory behind the pairs (when both fit: G22 shape, 8 replicas: 129 + 95 KB), so
+// a group's slot numbers come back in an LDS latency instead of an L1 / L2 one.
+template <int QPT, bool UNITW, bool IDS>
 __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(const LowdegArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -444,12 +447,16 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
             }
     };
     pass_b();
+    if (IDS) {
+        uint2 *dst = reinterpret_cast<uint2 *>(smem_raw + a.off_ids);
+        for (uint32_t i = tid; i < a.n_ids; i += blockDim.x) dst[i] = __ldg(a.sidx + i);
+    }
     __syncthreads();
 
     const size_t first_row = (size_t)a.warp_start[warp];
     // the stream as u16 slot numbers: 8 B per group, ~100 KB per step on the G22 shape -- it stays in the L1 the 132 KB
     // shared-memory configuration leaves (the u32-offset form, 200 KB, thrashed it: every group waited on L2)
-    const uint2 *so = a.sidx + first_row * a.C + c;
+    const uint2 *so = (IDS ? reinterpret_cast<const uint2 *>(smem_raw + a.off_ids) : a.sidx) + first_row * a.C + c;
     const float4 *sw = a.swt + first_row * a.C + c;
 
     bool pending = true;
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
         const uint2 *po = so;
         const float4 *pw = sw;
         const int stride = a.C;
-        uint2 nxt = __ldg(po);               // the slot numbers run one group ahead of their use (the last group of a warp's
+        uint2 nxt = IDS ? *po : __ldg(po);   // the slot numbers run one group ahead of their use (the last group of a warp's
                                              // stream prefetches the pad row behind it)
 #pragma unroll
         for (int t = 0; t < QPT; ++t) {
@@ -515,7 +522,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                 do {
                     const uint2 o = nxt;
                     po += stride;
-                    nxt = __ldg(po);
+                    nxt = IDS ? *po : __ldg(po);
                     float4 w = make_float4(1.f, 1.f, 1.f, 1.f);
                     if (USE_W) { w = __ldg(pw); }
                     pw += stride;

@@ -44,6 +44,7 @@ struct LowdegPlan {
     DevBuf<uint32_t> quad_of;
     DevBuf<uint4> soff;
     DevBuf<uint2> sidx;          // two-replica form: u16 slot numbers
+    size_t n_ids = 0;            // entries of sidx
     DevBuf<float4> swt;
     DevBuf<int> warp_start;
 };
@@ -290,6 +291,7 @@ static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegSh
         }
         plan->sidx.alloc(entries);
         plan->sidx.upload(idx16.data(), entries, st);
+        plan->n_ids = entries;
     }
     plan->soff.alloc(entries);
     plan->soff.upload(reinterpret_cast<const uint4 *>(h.off.data()), entries, st);
@@ -328,18 +330,18 @@ static void launch_lowdeg(oscb_graph *g, const LowdegArgs &a, const LowdegShape 
     }
 }
 
-template <bool UNITW>
-static void launch_lowdeg_pair(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles)
+template <bool UNITW, bool IDS>
+static void launch_lowdeg_pair(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles, size_t smem)
 {
     auto go = [&](auto kernel) {
-        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem));
-        kernel<<<tiles, s.W * 32, s.smem, g->stream>>>(a);
+        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kernel<<<tiles, s.W * 32, smem, g->stream>>>(a);
     };
     switch (s.QPT) {
-    case 1: go(k_lowdeg_pair<1, UNITW>); break;
-    case 2: go(k_lowdeg_pair<2, UNITW>); break;
-    case 4: go(k_lowdeg_pair<4, UNITW>); break;
-    case 5: go(k_lowdeg_pair<5, UNITW>); break;
+    case 1: go(k_lowdeg_pair<1, UNITW, IDS>); break;
+    case 2: go(k_lowdeg_pair<2, UNITW, IDS>); break;
+    case 4: go(k_lowdeg_pair<4, UNITW, IDS>); break;
+    case 5: go(k_lowdeg_pair<5, UNITW, IDS>); break;
     default: OSCB_REQUIRE(false, "internal: no k_lowdeg_pair instantiation for %d items per thread", s.QPT);
     }
 }
@@ -407,6 +409,7 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     a.io = d_io.p; a.best_obj = d_best.p; a.energy = d_energy.p; a.best_trace = d_btrace.p; a.best_states = d_best_states.p;
     a.first_hit = d_first.p; a.nonfinite = g->d_nonfinite.p;
 
+    size_t launched_smem = sh.smem;
     cudaEvent_t ev0, ev1;
     OSCB_CUDA(cudaEventCreate(&ev0));
     OSCB_CUDA(cudaEventCreate(&ev1));
@@ -418,7 +421,17 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
         else if (sh.uniform) launch_lowdeg<NM, true, false>(g, a, sh, tiles);
         else launch_lowdeg<NM, false, false>(g, a, sh, tiles);
     };
-    if (sh.rpl == 2) { if (g->unit_weights) launch_lowdeg_pair<true>(g, a, sh, tiles); else launch_lowdeg_pair<false>(g, a, sh, tiles); }
+    if (sh.rpl == 2) {
+        // the slot stream goes to shared memory when it fits behind the pairs (OSCB_LOWDEG_IDS=0: never)
+        const size_t ids_bytes = (plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15;
+        const bool want_ids = !(getenv("OSCB_LOWDEG_IDS") && atoi(getenv("OSCB_LOWDEG_IDS")) == 0);
+        const bool ids = want_ids && sh.smem + ids_bytes <= (size_t)g->smem_optin;
+        size_t smem = sh.smem;
+        if (ids) { a.off_ids = (uint32_t)sh.smem; a.n_ids = (uint32_t)plan->n_ids; smem += ids_bytes; }
+        launched_smem = smem;
+        if (ids) { if (g->unit_weights) launch_lowdeg_pair<true, true>(g, a, sh, tiles, smem); else launch_lowdeg_pair<false, true>(g, a, sh, tiles, smem); }
+        else     { if (g->unit_weights) launch_lowdeg_pair<true, false>(g, a, sh, tiles, smem); else launch_lowdeg_pair<false, false>(g, a, sh, tiles, smem); }
+    }
     else if (nmode == 2) by_shape(std::integral_constant<int, 2>{});
     else by_shape(std::integral_constant<int, 3>{});
     OSCB_CUDA(cudaEventRecord(ev1, s));
@@ -457,7 +470,7 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     out->kernel_launches = 1;
     out->kernel_used = OSCB_KERNEL_LOWDEG;
     out->replicas_per_cta = RT;
-    out->smem_bytes = (int64_t)sh.smem;
+    out->smem_bytes = (int64_t)launched_smem;
     if (flag != none) {
         out->nonfinite[2] = (int64_t)(flag >> 36);
         out->nonfinite[0] = (int64_t)((flag >> 20) & 0xFFFFull);
