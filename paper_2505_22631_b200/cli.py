@@ -282,7 +282,7 @@ def _solver_flags(p, replicas_default=1, workers_default=1, with_k=True):
 def _gpu_flags(p):
     p.add_argument("--precision", choices=("f32", "f64"), default=None, help="f32 throughput mode (default) or f64 parity mode")
     p.add_argument("--device", type=int, default=None, help="CUDA device index")
-    p.add_argument("--kernel", choices=("auto", "stream", "resident"), default="auto")
+    p.add_argument("--kernel", choices=("auto", "stream", "resident", "lowdeg", "cluster", "dense-tc"), default="auto")
 
 
 def build_parser() -> argparse.ArgumentParser:
