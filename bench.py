@@ -787,7 +787,9 @@ def main():
     smem_peak = 128.0 * info_sm_count * sm_mhz * 1e6 / 1e9
     smem_achieved = launch_updates * (2 * s_phi) / (kernel_ms * 1e-3) / 1e9
     kernel_name = {"resident": "k_resident_fast" if args.precision == "f32" else "k_resident",
-                   "lowdeg": "k_lowdeg"}.get(last.kernel, last.kernel)
+                   # (N = 2 rows of more than one group run two replicas per lane: oscb_lowdeg_host.hpp)
+                   "lowdeg": "k_lowdeg_pair" if (params.n_states == 2 and int(np.diff(J.indptr).max()) > 4 and last.replicas_per_cta > 1)
+                             else "k_lowdeg"}.get(last.kernel, last.kernel)
     # DRAM bytes per launch cannot be counted from inside an untraced run: the figure is the one transcribed from the
     # committed `ncu --set full` capture of this exact (workload, kernel, precision, window); anything else says so
     traffic, traffic_source = None, "not captured for this (workload, kernel, precision, window)"
@@ -824,9 +826,10 @@ def main():
     if rank == 0 and not args.no_parity_mode and args.precision == "f32":
         # the same workload in the reference's own arithmetic (float64 state, the reference's operation order:
         # dynamics.py:155-190) -- the throughput the parity mode sustains, beside the float32 headline
-        dyn.run_batch(J, params, kind, seeds, precision="f64", device=local_rank, kernel=args.kernel, steps=min(window, 256),
+        k64 = args.kernel if args.kernel in ("auto", "stream", "resident") else "auto"     # (the others are float32 only)
+        dyn.run_batch(J, params, kind, seeds, precision="f64", device=local_rank, kernel=k64, steps=min(window, 256),
                       want_phases=False, want_states=False, want_traces=False)
-        p64 = dyn.run_batch(J, params, kind, seeds, precision="f64", device=local_rank, kernel=args.kernel, steps=window,
+        p64 = dyn.run_batch(J, params, kind, seeds, precision="f64", device=local_rank, kernel=k64, steps=window,
                             want_phases=False, want_states=False, want_traces=False)
         b64 = algorithmic_bytes_per_euler_step(J, R, bool(info.unit_weights), 8) * window
         ach64 = b64 / (p64.device_ms * 1e-3) / 1e9

@@ -408,15 +408,17 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
     // (c0, s0, c1, s1) of the two replicas of this lane at a slot
     const uint32_t slot_bytes = (uint32_t)a.RT * 8u;
     auto pairs_at = [&](uint32_t slot) -> float4 { return *reinterpret_cast<const float4 *>(cs_lane + slot * slot_bytes); };
+    // quad table word: quad number (24 bits, all ones = ghost) | the components of its rows in visiting order (4 x 2 bits)
     auto quad = [&](int t) -> uint32_t { return __ldg(a.quad_of + pos0 + t * WC); };
+    auto comp_of = [](uint32_t qw, int k) -> uint32_t { return (qw >> (24 + 2 * k)) & 3u; };
 
     float phi[QPT][4][2];
 #pragma unroll
     for (int t = 0; t < QPT; ++t) {
-        const uint32_t qd = quad(t);
+        const uint32_t qw = quad(t), qd = qw & 0xFFFFFFu;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t i = 4u * qd + k;
+            const uint32_t i = 4u * qd + comp_of(qw, k);
 #pragma unroll
             for (int e = 0; e < 2; ++e)
                 phi[t][k][e] = (qd < (uint32_t)a.Q && i < (uint32_t)a.n && live[e]) ? (float)a.io[(size_t)(rg0 + e) * a.n + i] : 0.0f;
@@ -480,10 +482,18 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
         for (int t = 0; t < QPT; ++t) {
             float z[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
             if (MODE != 3 && a.noise_on) {
-                const uint32_t qd = quad(t);
+                const uint32_t qw = quad(t), qd = qw & 0xFFFFFFu;
 #pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    normals4_fast(philox4x32_10(make_uint4(qd, (uint32_t)step, 0u, 0x6F736362u), key[e]), z[e][0], z[e][1], z[e][2], z[e][3]);
+                for (int e = 0; e < 2; ++e) {
+                    float n0, n1, n2, n3;
+                    normals4_fast(philox4x32_10(make_uint4(qd, (uint32_t)step, 0u, 0x6F736362u), key[e]), n0, n1, n2, n3);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {                       // the k-th row visited is component comp_of(qw, k)
+                        const uint32_t cm = comp_of(qw, k);
+                        const float lo = (cm & 1u) ? n1 : n0, hi = (cm & 1u) ? n3 : n2;
+                        z[e][k] = (cm & 2u) ? hi : lo;
+                    }
+                }
             }
             float ynew[4][2];
 #pragma unroll
@@ -565,8 +575,8 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                 for (int k = 0; k < 4; ++k)
 #pragma unroll
                     for (int e = 0; e < 2; ++e)
-                        if (!(phi[t][k][e] == phi[t][k][e]) && live[e] && quad(t) < (uint32_t)a.Q)
-                            flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)(rg0 + e), 4u * quad(t) + k);
+                        if (!(phi[t][k][e] == phi[t][k][e]) && live[e] && (quad(t) & 0xFFFFFFu) < (uint32_t)a.Q)
+                            flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)(rg0 + e), 4u * (quad(t) & 0xFFFFFFu) + comp_of(quad(t), k));
         }
         if (MODE >= 1) {
 #pragma unroll
@@ -606,13 +616,13 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                 if (improved_s[r0 + e] && live[e]) {
 #pragma unroll
                     for (int t = 0; t < QPT; ++t) {
-                        const uint32_t qd = quad(t);
+                        const uint32_t qw = quad(t), qd = qw & 0xFFFFFFu;
                         if (qd < (uint32_t)a.Q) {
                             uint32_t packed = 0;
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 const float4 own = *reinterpret_cast<const float4 *>(smem_raw + own0 + t * tbytes + k * kbytes);
-                                packed |= (__float_as_uint(e ? own.z : own.x) >> 31) << (8 * k);
+                                packed |= (__float_as_uint(e ? own.z : own.x) >> 31) << (8 * comp_of(qw, k));
                             }
                             *reinterpret_cast<uint32_t *>(a.best_states + (size_t)(rg0 + e) * a.n4 + 4u * qd) = packed;
                         }
@@ -659,10 +669,10 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
     if (tid < a.RT) a.best_obj[tile * a.RT + tid] = best_s[tid];
 #pragma unroll
     for (int t = 0; t < QPT; ++t) {
-        const uint32_t qd = quad(t);
+        const uint32_t qw = quad(t), qd = qw & 0xFFFFFFu;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const uint32_t i = 4u * qd + k;
+            const uint32_t i = 4u * qd + comp_of(qw, k);
 #pragma unroll
             for (int e = 0; e < 2; ++e)
                 if (live[e] && qd < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)(rg0 + e) * a.n + i] = (double)phi[t][k][e];

@@ -8,7 +8,7 @@ namespace oscb {
 
 // float32, device noise, max degree <= 16 (mean <= 8 unless `forced`), and N = 2 max-cut on integer couplings
 // or N = 3 colouring on unit couplings
-bool lowdeg_applies(const oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced);
+bool lowdeg_applies(oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced);
 
 // the whole run in one persistent launch (same contract as run_resident)
 void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t cadence,

@@ -72,9 +72,20 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
     auto groups = [&](int i) { return std::max(1, (deg(i) + 3) / 4); };
     std::vector<int> order(Q);
     std::iota(order.begin(), order.end(), 0);
+    // k_lowdeg_pair walks the four rows of a quad in descending degree (rowsel[q][k] = the component visited k-th), so the
+    // rows that share a warp-row's k-th trip have similar lengths: a quad's long row no longer meets its neighbours' short
+    // ones (G22 shape: 0.82 -> 0.90 of the stream entries are real neighbours).  The permutation travels in the top byte
+    // of the quad table; slots, registers and stream are all in visiting order, only the noise component, the state
+    // byte and the phase I/O look the component up.
+    const bool sort_rows = s.rpl == 2 && !s.uniform;
+    std::vector<std::array<uint8_t, 4>> rowsel(Q, std::array<uint8_t, 4>{0, 1, 2, 3});
+    if (sort_rows)
+        for (int q = 0; q < Q; ++q)
+            std::stable_sort(rowsel[q].begin(), rowsel[q].end(), [&](uint8_t x, uint8_t y) { return deg(4 * q + x) > deg(4 * q + y); });
     if (!s.uniform) {
         std::vector<std::array<int, 4>> key(Q);
-        for (int q = 0; q < Q; ++q) key[q] = {groups(4 * q), groups(4 * q + 1), groups(4 * q + 2), groups(4 * q + 3)};
+        for (int q = 0; q < Q; ++q)
+            key[q] = {groups(4 * q + rowsel[q][0]), groups(4 * q + rowsel[q][1]), groups(4 * q + rowsel[q][2]), groups(4 * q + rowsel[q][3])};
         std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key[x] > key[y]; });
     }
     // chunk j of C quads -> warp-row (t, w)
@@ -91,7 +102,7 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
         const uint32_t q = out->quad_of[pos];
         if (q >= (uint32_t)Q) continue;
         for (int k = 0; k < 4; ++k)
-            if (4 * (int)q + k < n) out->slot_of[4 * q + k] = (uint32_t)(k * Qp + pos);
+            if (4 * (int)q + rowsel[q][k] < n) out->slot_of[4 * q + rowsel[q][k]] = (uint32_t)(k * Qp + pos);
     }
     auto pad_off = [&](int c) { return (uint32_t)(((uint32_t)4 * Qp + (c % OSCB_LD_PADS)) * RT * 8); };
     out->off.clear();
@@ -140,7 +151,7 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
     };
     auto row_of = [&](int t, int w, int c, int k) -> int {
         const uint32_t q = out->quad_of[(size_t)(t * W + w) * C + c];
-        return q < (uint32_t)Q && 4 * (int)q + k < n ? 4 * (int)q + k : -1;
+        return q < (uint32_t)Q && 4 * (int)q + rowsel[q][k] < n ? 4 * (int)q + rowsel[q][k] : -1;
     };
     if (s.uniform) {
         // [t][w][k][c], one group per row
@@ -171,6 +182,14 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
         }
         out->group_rows = rows;
         for (int c = 0; c < C; ++c) emit(-1, 0, c, true);       // the prefetch pad row
+    }
+    if (sort_rows) {
+        OSCB_REQUIRE(Q < 0xFFFFFF, "internal: quad numbers exceed 24 bits");
+        for (uint32_t &qw : out->quad_of)
+            if (qw < (uint32_t)Q) {
+                const auto &r = rowsel[qw];
+                qw |= (uint32_t)(r[0] | (r[1] << 2) | (r[2] << 4) | (r[3] << 6)) << 24;
+            }
     }
     (void)weighted_stream;
 }
@@ -306,10 +325,40 @@ static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegSh
     return plan;
 }
 
-bool lowdeg_applies(const oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced)
+// k_lowdeg_pair beyond the low degrees: a unit-coupling N = 2 max-cut graph of any degree whose slot stream fits in shared
+// memory behind the pairs of an 8-replica tile (the G22 shape: 130 + 90 KB), when the batch fills the GPU with such tiles.
+// There the pair kernel's leaner per-oscillator part beats k_resident_fast (2.18 vs 2.10 T updates/s on G22 x 1024).  Off
+// that shape -- stream from L1 / L2, other tile sizes, weighted rows -- k_resident_fast measured ahead and keeps the run.
+static bool lowdeg_pair_resident_shape(oscb_graph *g, const oscb_run_params *p, int64_t R, LowdegShape *out)
+{
+    int nmode;
+    if (!lowdeg_kind(g, p, &nmode) || nmode != 2 || !g->unit_weights || g->max_degree <= 4) return false;
+    if (getenv("OSCB_LOWDEG_RT") || getenv("OSCB_LOWDEG_QPT") || getenv("OSCB_LOWDEG_RPL")) return false;   // pinned shapes: the general chooser
+    if (p->replicas_per_cta > 0 && p->replicas_per_cta != 8) return false;
+    const int RT = 8, C = 8, Q = (int)((g->n + 3) / 4), rows = (Q + C - 1) / C;
+    if ((R + RT - 1) / RT < (int64_t)g->sm_count * 3 / 4) return false;
+    for (int QPT : {4, 5}) {
+        const int W = (rows + QPT - 1) / QPT;
+        if (W < 8 || W > lowdeg_max_threads(2 * QPT) / 32) continue;
+        LowdegShape s;
+        s.RT = RT; s.LRT = 3; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = false; s.rpl = 2;
+        s.smem = lowdeg_smem_bytes(s, nullptr, nullptr, nullptr);
+        s.cost = 0.0;
+        if (s.smem > (size_t)g->smem_optin || (size_t)4 * s.Qp + OSCB_LD_PADS > 32768) continue;
+        if (s.smem + (size_t)g->nnz * 2 > (size_t)g->smem_optin) continue;        // even an unpadded stream would not fit
+        auto plan = get_lowdeg_plan(g, s, nmode);
+        if (s.smem + ((plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15) > (size_t)g->smem_optin) continue;
+        *out = s;
+        return true;
+    }
+    return false;
+}
+
+bool lowdeg_applies(oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced)
 {
     LowdegShape s;
-    return choose_lowdeg_shape(g, p, R, forced, &s);
+    if (choose_lowdeg_shape(g, p, R, false, &s) || lowdeg_pair_resident_shape(g, p, R, &s)) return true;
+    return forced && choose_lowdeg_shape(g, p, R, true, &s);
 }
 
 template <int NMODE, bool UNIFORM, bool RT1>
@@ -354,7 +403,8 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     const int n = (int)g->n, R = (int)R64;
     LowdegShape sh;
     int nmode = 2;
-    OSCB_REQUIRE(lowdeg_kind(g, p, &nmode) && choose_lowdeg_shape(g, p, R, true, &sh),
+    OSCB_REQUIRE(lowdeg_kind(g, p, &nmode) && (choose_lowdeg_shape(g, p, R, false, &sh) || lowdeg_pair_resident_shape(g, p, R, &sh) ||
+                                                 choose_lowdeg_shape(g, p, R, true, &sh)),
                  "the low-degree kernel takes float32, device noise, max degree <= 16 and N = 2 max-cut on integer couplings "
                  "or N = 3 colouring on unit couplings");
     auto plan = get_lowdeg_plan(g, sh, nmode);

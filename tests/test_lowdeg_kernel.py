@@ -143,6 +143,8 @@ CASES = [
     ("sparse203", lambda: _graph(203, "sparse_pm", 2), 2, "maxcut", 5, 4, 20),
     ("sparse1001", lambda: _graph(1001, "sparse_pm", 4), 2, "maxcut", 2, 1, 20),
     ("unit1001", lambda: _graph(1001, "unit", 5), 3, "coloring", 6, 2, 60),
+    # the headline route: 1024 replicas of the degree-20 G22 shape go to k_lowdeg_pair with the slot stream in shared memory
+    ("G22x1024", lambda: __import__("bench").load_workload("G22x1024")[1], 2, "maxcut", 1024, 0, 20),
 ]
 
 
@@ -226,6 +228,25 @@ def test_determinism_replica_independence_and_tile_shape_independence(pkg):
 
 
 @gpu
+@pytest.mark.parametrize("n,rt", [(203, 4), (600, 8), (1001, 2)])
+def test_pair_kernel_noise_is_a_function_of_seed_step_and_oscillator(pkg, monkeypatch, n, rt):
+    """k_lowdeg_pair walks the rows of a quad in descending degree; the noise an oscillator gets must still be component
+    i mod 4 of the Philox block of quad i / 4 (the device noise contract every kernel shares): with noise ON a few steps of
+    the pair kernel and of the per-step streaming kernel agree to float32 rounding, phases and read-out."""
+    J = _graph(n, "sparse_pm", 31)
+    params = pkg.SolverParams.tuned_for(J.n, 2, seed=3, K=0.2, ks_max=1.0, kn=0.3)
+    seeds = [3 + r for r in range(2 * rt + 1)]
+    monkeypatch.setenv("OSCB_LOWDEG_RPL", "2")
+    a = pkg.run_batch(J, params, "maxcut", seeds, kernel="lowdeg", steps=6, replicas_per_cta=rt)
+    monkeypatch.delenv("OSCB_LOWDEG_RPL")
+    b = pkg.run_batch(J, params, "maxcut", seeds, kernel="stream", steps=6, precision="f32")
+    assert a.kernel == "lowdeg" and b.kernel == "stream" and a.replicas_per_cta == rt
+    assert circ_dist_rad(a.final_phases, b.final_phases).max() <= 2e-5
+    assert np.array_equal(_objective(J, a.best_states, "maxcut"), a.best_objective)
+    assert np.abs(a.best_objective - b.best_objective).max() <= 4.0
+
+
+@gpu
 @pytest.mark.parametrize("N,kind", [(2, "maxcut"), (3, "coloring")])
 def test_noise_on_distribution_matches_the_oracle(pkg, oracle, N, kind):
     """Noise ON (device Philox vs numpy's stream replayed by the oracle): best objectives over 128 seeds agree in
@@ -258,6 +279,9 @@ def test_auto_selection_and_fallbacks(pkg):
     assert pkg.run_batch(Jf, pf, "coloring", list(range(64)), steps=4).kernel == "lowdeg"
     _, J22, p22, _, _ = bench.load_workload("G22x1024")
     assert pkg.run_batch(J22, p22, "maxcut", list(range(64)), steps=4).kernel == "resident"
+    # ... unless the batch fills the GPU with 8-replica tiles whose slot stream fits in shared memory: k_lowdeg_pair
+    big = pkg.run_batch(J22, p22, "maxcut", list(range(1024)), steps=4, want_phases=False, want_states=False)
+    assert big.kernel == "lowdeg" and big.replicas_per_cta == 8
     assert pkg.run_batch(J22, p22, "maxcut", list(range(8)), steps=4, kernel="lowdeg").kernel == "lowdeg"      # on request: any degree
     with pytest.raises(ValueError):
         pkg.run_batch(J22, p22, "maxcut", [0], steps=4, kernel="lowdeg", precision="f64")                      # float32 only
