@@ -250,6 +250,17 @@ int oscb_lowdeg_plan_host(int64_t n, const int64_t *indptr, const int64_t *indic
                           int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
                           uint32_t *offsets, float *couplings, int32_t *warp_start);
 
+/* The same for k_lowdeg_pair, the two-replicas-per-lane form (N = 2 max-cut rows of any degree; C = 64 / replicas_per_cta
+ * slots per warp, replicas_per_cta >= 2).  On a looped stream the four rows of a quad are visited in descending degree:
+ * bits 24..31 of a quad_of word hold the component (0..3) visited 1st..4th, two bits each, bits 0..23 the quad (all ones:
+ * none), and slot_of is (visiting position) * Qp + position of the quad.  A row's neighbours -- and its padding, which may
+ * sit anywhere in the row -- are ordered so that the slots read by one quarter-warp fall in different shared-memory bank
+ * groups where the row contents allow it. */
+int oscb_lowdeg_pair_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, const double *weights,
+                               int32_t replicas_per_cta, int32_t warps, int32_t items_per_thread, int32_t *uniform,
+                               int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
+                               uint32_t *offsets, float *couplings, int32_t *warp_start);
+
 /* Host-only: the graph compiler of the persistent kernel (no GPU needed).  Turns a canonical CSR
  * (model.py:135-149) into the sliced-ELL neighbour stream for tiles of `replicas_per_cta`
  * replicas, CTAs of at most `max_threads` threads and (cos, sin) pairs of `pair_bytes` bytes.

@@ -99,6 +99,8 @@ SYMBOLS = {
                                           C.POINTER(C.c_int64), _P, _P, _P, _P]),
     "oscb_lowdeg_plan_host": (C.c_int, [C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, _P, _P, _P, _P]),
+    "oscb_lowdeg_pair_plan_host": (C.c_int, [C.c_int64, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                             C.POINTER(C.c_int64), C.POINTER(C.c_int64), _P, _P, _P, _P, _P]),
     "oscb_run": (C.c_int, [_P, C.POINTER(RunParams), _P, C.c_int64, _P, _P, C.POINTER(RunOutputs)]),
 }
 

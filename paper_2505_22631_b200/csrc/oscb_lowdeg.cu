@@ -2,10 +2,10 @@
 // host side (oscb_lowdeg_host.hpp), plus the C-ABI test hook that exposes the stream compiler to CPU tests.
 #include "oscb_lowdeg_host.hpp"
 
-extern "C" int oscb_lowdeg_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, const double *weights,
-                                     int32_t replicas_per_cta, int32_t warps, int32_t items_per_thread, int32_t *uniform,
-                                     int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
-                                     uint32_t *offsets, float *couplings, int32_t *warp_start)
+static int lowdeg_plan_host(const char *who, int rpl, int64_t n, const int64_t *indptr, const int64_t *indices, const double *weights,
+                            int32_t replicas_per_cta, int32_t warps, int32_t items_per_thread, int32_t *uniform,
+                            int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
+                            uint32_t *offsets, float *couplings, int32_t *warp_start)
 {
     using namespace oscb;
     try {
@@ -19,8 +19,9 @@ extern "C" int oscb_lowdeg_plan_host(int64_t n, const int64_t *indptr, const int
         s.RT = replicas_per_cta;
         s.LRT = 0;
         while ((1 << s.LRT) < s.RT) ++s.LRT;
-        OSCB_REQUIRE((1 << s.LRT) == s.RT && s.RT <= 32, "replicas_per_cta must be a power of two <= 32");
-        s.C = 32 / s.RT; s.W = warps; s.QPT = items_per_thread; s.Q = (int)((n + 3) / 4); s.Qp = s.W * s.QPT * s.C;
+        OSCB_REQUIRE((1 << s.LRT) == s.RT && s.RT <= 32 && s.RT >= rpl, "replicas_per_cta must be a power of two <= 32");
+        s.rpl = rpl;
+        s.C = 32 * rpl / s.RT; s.W = warps; s.QPT = items_per_thread; s.Q = (int)((n + 3) / 4); s.Qp = s.W * s.QPT * s.C;
         s.uniform = maxdeg <= 4;
         LowdegStreamHost h;
         compile_lowdeg_stream((int)n, ip.data(), ix.data(), weights, s, true, &h);
@@ -36,7 +37,25 @@ extern "C" int oscb_lowdeg_plan_host(int64_t n, const int64_t *indptr, const int
     } catch (const OscbFail &f) {
         return f.code;
     } catch (const std::exception &e) {
-        set_error("oscb_lowdeg_plan_host: %s", e.what());
+        set_error("%s: %s", who, e.what());
         return OSCB_ECUDA;
     }
+}
+
+extern "C" int oscb_lowdeg_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, const double *weights,
+                                     int32_t replicas_per_cta, int32_t warps, int32_t items_per_thread, int32_t *uniform,
+                                     int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
+                                     uint32_t *offsets, float *couplings, int32_t *warp_start)
+{
+    return lowdeg_plan_host("oscb_lowdeg_plan_host", 1, n, indptr, indices, weights, replicas_per_cta, warps, items_per_thread, uniform,
+                            group_rows, entries, quad_of, slot_of, offsets, couplings, warp_start);
+}
+
+extern "C" int oscb_lowdeg_pair_plan_host(int64_t n, const int64_t *indptr, const int64_t *indices, const double *weights,
+                                          int32_t replicas_per_cta, int32_t warps, int32_t items_per_thread, int32_t *uniform,
+                                          int64_t *group_rows, int64_t *entries, uint32_t *quad_of, uint32_t *slot_of,
+                                          uint32_t *offsets, float *couplings, int32_t *warp_start)
+{
+    return lowdeg_plan_host("oscb_lowdeg_pair_plan_host", 2, n, indptr, indices, weights, replicas_per_cta, warps, items_per_thread, uniform,
+                            group_rows, entries, quad_of, slot_of, offsets, couplings, warp_start);
 }

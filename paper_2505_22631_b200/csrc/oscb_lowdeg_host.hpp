@@ -104,45 +104,85 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
         for (int k = 0; k < 4; ++k)
             if (4 * (int)q + rowsel[q][k] < n) out->slot_of[4 * q + rowsel[q][k]] = (uint32_t)(k * Qp + pos);
     }
-    auto pad_off = [&](int c) { return (uint32_t)(((uint32_t)4 * Qp + (c % OSCB_LD_PADS)) * RT * 8); };
     out->off.clear();
     out->wt.clear();
     out->real = 0;
     out->warp_start.assign(W, 0);
     out->warp_groups.assign(W, 0);
-    // Looped streams: the slots that share a 128-byte shared-memory wavefront (H = 128 / (RT * 8) consecutive slots) should
-    // read different bank classes (slot number mod H) at the same position, so the neighbours of the row in slot c are
-    // visited starting with class c mod H and rotating (G22 shape, 8 replicas per tile: 1.40 -> ~1.1 wavefronts per ideal one).
-    // Uniform streams keep the CSR order (lattice-like graphs gather from neighbouring slots as they are), and so does the
-    // one-replica-per-lane kernel.  Float32 sums depend on the order, so k_lowdeg_pair's last bits depend on the tile shape
-    // (like k_resident_fast's); the float64 parity mode always sums in CSR order.
+    // Looped streams of k_lowdeg_pair: an LDS.128 is served a quarter-warp at a time, i.e. H = 128 / (RT * 8) consecutive
+    // slots per 128-byte wavefront, and two of them collide when their targets fall in the same bank group (slot number mod
+    // H) at different addresses.  The rows of such a group of H slots are therefore scheduled TOGETHER: at every position
+    // each row takes a neighbour from a bank group nobody else in the quarter-warp uses; a row that has none left of a free
+    // group spends one of its padding reads there instead (a row shorter than its warp-row's 4 G positions may pad
+    // anywhere, and a pad slot exists for every bank group).  G22 shape, 8 replicas per tile: 1.40 wavefronts per ideal one
+    // in CSR order, ~1.13 with each row ordered on its own, ~1.03 jointly.  Uniform streams keep the CSR order
+    // (lattice-like graphs gather from neighbouring slots as they are), and so does the one-replica-per-lane kernel, whose
+    // results then do not depend on the tile shape.  Float32 sums depend on the order, so k_lowdeg_pair's last bits depend
+    // on the tile shape (like k_resident_fast's); the float64 parity mode always sums in CSR order.
     const int H = std::max(1, std::min(C, 128 / (RT * 8)));
-    std::vector<std::vector<int>> perms(C);       // per slot of the current warp-row: CSR positions of its row in visiting order
-    auto visit_order = [&](int i, int c) {
-        std::vector<int> &perm = perms[c];
-        perm.resize(deg(i));
-        std::iota(perm.begin(), perm.end(), indptr[i]);
-        if (s.uniform || H < 2 || s.rpl != 2) return;      // (one replica per lane keeps the CSR order: its results then do not depend on the tile shape)
-        std::vector<std::vector<int>> bucket(H);
-        for (int e : perm) bucket[out->slot_of[indices[e]] % H].push_back(e);
-        size_t at = 0;
-        for (int round = 0; at < perm.size(); ++round) {
-            // position p prefers class (c + p) mod H; when that class has run dry take the fullest one
-            int cls = (c + round) % H;
-            if (bucket[cls].empty())
-                for (int k = 0; k < H; ++k)
-                    if (bucket[k].size() > bucket[cls].size()) cls = k;
-            perm[at++] = bucket[cls].front();
-            bucket[cls].erase(bucket[cls].begin());
+    const bool joint = !s.uniform && H >= 2 && s.rpl == 2;
+    // sched[c]: for every position of slot c's row in the current warp-row, a CSR entry, or -(1 + bank group) for padding
+    std::vector<std::vector<int>> sched(C);
+    auto schedule_rows = [&](const int *rows, int G) {
+        const int P = 4 * G;
+        for (int c = 0; c < C; ++c) sched[c].assign(P, -1);
+        if (!joint) {
+            for (int c = 0; c < C; ++c) {
+                const int i = rows[c], d = i >= 0 ? deg(i) : 0;
+                for (int u = 0; u < P; ++u) sched[c][u] = u < d ? indptr[i] + u : -(1 + c % OSCB_LD_PADS);
+            }
+            return;
+        }
+        for (int c0 = 0; c0 < C; c0 += H) {
+            std::vector<std::vector<std::vector<int>>> bucket(H, std::vector<std::vector<int>>(H));   // [slot][bank group] -> CSR entries, reversed
+            int left[32];
+            for (int j = 0; j < H; ++j) {
+                const int i = rows[c0 + j];
+                left[j] = i >= 0 ? deg(i) : 0;
+                if (i >= 0)
+                    for (int e = indptr[i + 1] - 1; e >= indptr[i]; --e) bucket[j][out->slot_of[indices[e]] % H].push_back(e);
+            }
+            for (int pos = 0; pos < P; ++pos) {
+                int order[32];
+                for (int j = 0; j < H; ++j) order[j] = j;
+                // rows with the least padding left choose first; position-dependent tie-break spreads the leftovers
+                std::stable_sort(order, order + H, [&](int x, int y) { return (P - pos - left[x]) < (P - pos - left[y]); });
+                uint32_t used = 0;
+                int pads[32], n_pads = 0;
+                for (int oi = 0; oi < H; ++oi) {
+                    const int j = order[oi];
+                    if (left[j] == 0) { pads[n_pads++] = j; continue; }
+                    int cls = -1;
+                    for (int k = 0; k < H; ++k) {
+                        const int cand = (j + pos + k) % H;
+                        if (!(used >> cand & 1u) && !bucket[j][cand].empty() && (cls < 0 || bucket[j][cand].size() > bucket[j][cls].size())) cls = cand;
+                    }
+                    if (cls < 0) {
+                        if (P - pos - left[j] > 0) { pads[n_pads++] = j; continue; }       // pad here, keep the neighbours for later
+                        for (int k = 0; k < H; ++k)
+                            if (!bucket[j][k].empty() && (cls < 0 || bucket[j][k].size() > bucket[j][cls].size())) cls = k;
+                    }
+                    sched[c0 + j][pos] = bucket[j][cls].back();
+                    bucket[j][cls].pop_back();
+                    --left[j];
+                    used |= 1u << cls;
+                }
+                for (int q = 0; q < n_pads; ++q) {
+                    int cls = pads[q] % H;
+                    for (int k = 0; k < H; ++k)
+                        if (!(used >> ((pads[q] + k) % H) & 1u)) { cls = (pads[q] + k) % H; break; }
+                    used |= 1u << cls;
+                    sched[c0 + pads[q]][pos] = -(1 + cls);
+                }
+            }
         }
     };
-    // one group entry of slot c: neighbours [4 g, 4 g + 4) of row i in visiting order
-    auto emit = [&](int i, int g, int c, bool last) {
-        if (i >= 0 && g == 0) visit_order(i, c);
+    // one group entry of slot c: positions [4 g, 4 g + 4) of its scheduled row
+    auto emit = [&](int g, int c, bool last) {
         for (int u = 0; u < 4; ++u) {
-            const bool real = i >= 0 && i < n && 4 * g + u < deg(i);
-            const int e = real ? perms[c][4 * g + u] : -1;
-            uint32_t o = real ? (uint32_t)(out->slot_of[indices[e]] * RT * 8) : pad_off(c);
+            const int e = sched[c][4 * g + u];
+            const bool real = e >= 0;
+            uint32_t o = real ? (uint32_t)(out->slot_of[indices[e]] * RT * 8) : (uint32_t)(((uint32_t)4 * Qp + (uint32_t)(-e - 1)) * RT * 8);
             if (u == 3 && last) o |= 0x80000000u;
             out->off.push_back(o);
             out->wt.push_back(real ? (wts ? (float)wts[e] : 1.0f) : 0.0f);
@@ -155,33 +195,41 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
     };
     if (s.uniform) {
         // [t][w][k][c], one group per row
+        std::vector<int> rows_now(C);
         for (int t = 0; t < QPT; ++t)
             for (int w = 0; w < W; ++w)
-                for (int k = 0; k < 4; ++k)
-                    for (int c = 0; c < C; ++c) emit(row_of(t, w, c, k), 0, c, false);
+                for (int k = 0; k < 4; ++k) {
+                    for (int c = 0; c < C; ++c) rows_now[c] = row_of(t, w, c, k);
+                    schedule_rows(rows_now.data(), 1);
+                    for (int c = 0; c < C; ++c) emit(0, c, false);
+                }
         out->group_rows = QPT * W * 4;
         for (int w = 0; w < W; ++w) out->warp_groups[w] = (int64_t)QPT * 4;
     } else {
         // per warp: t, k, g in the order the kernel walks them
         int rows = 0;
+        std::vector<int> rows_now(C);
         for (int w = 0; w < W; ++w) {
             out->warp_start[w] = rows;
             for (int t = 0; t < QPT; ++t)
                 for (int k = 0; k < 4; ++k) {
                     int G = 1;
                     for (int c = 0; c < C; ++c) {
-                        const int i = row_of(t, w, c, k);
+                        const int i = rows_now[c] = row_of(t, w, c, k);
                         if (i >= 0) G = std::max(G, groups(i));
                     }
+                    schedule_rows(rows_now.data(), G);
                     for (int g = 0; g < G; ++g) {
-                        for (int c = 0; c < C; ++c) emit(row_of(t, w, c, k), g, c, g == G - 1);
+                        for (int c = 0; c < C; ++c) emit(g, c, g == G - 1);
                         ++rows;
                     }
                 }
             out->warp_groups[w] = rows - out->warp_start[w];
         }
         out->group_rows = rows;
-        for (int c = 0; c < C; ++c) emit(-1, 0, c, true);       // the prefetch pad row
+        std::fill(rows_now.begin(), rows_now.end(), -1);
+        schedule_rows(rows_now.data(), 1);
+        for (int c = 0; c < C; ++c) emit(0, c, true);           // the prefetch pad row
     }
     if (sort_rows) {
         OSCB_REQUIRE(Q < 0xFFFFFF, "internal: quad numbers exceed 24 bits");
