@@ -88,6 +88,45 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
             key[q] = {groups(4 * q + rowsel[q][0]), groups(4 * q + rowsel[q][1]), groups(4 * q + rowsel[q][2]), groups(4 * q + rowsel[q][3])};
         std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key[x] > key[y]; });
     }
+    // k_lowdeg_pair: the bank group of an oscillator's slot is its quad's place in the chunk mod Hq (see the row scheduling
+    // below), and a row whose neighbours crowd into one bank group collides with its quarter-warp partners whatever their
+    // order.  Swap quads of different bank groups inside a chunk (the chunk contents, hence the padding, stay as sorted)
+    // while that evens out the rows' neighbour counts per bank group: sum over rows and groups of count^2, local search.
+    const int Hq = std::max(1, std::min(C, 128 / (RT * 8)));
+    if (sort_rows && Hq >= 2) {
+        std::vector<int> cls(Q), cnt((size_t)n * Hq, 0);
+        for (int idx = 0; idx < Q; ++idx) cls[order[idx]] = (idx % C) % Hq;
+        for (int r = 0; r < n; ++r)
+            for (int e = indptr[r]; e < indptr[r + 1]; ++e) ++cnt[(size_t)r * Hq + cls[indices[e] >> 2]];
+        // move every oscillator of quad q from bank group a to b: returns the change of the objective (the CSR is symmetric:
+        // the rows that see oscillator x are x's own neighbours)
+        auto move = [&](int q, int a, int b) {
+            long long d = 0;
+            for (int x = 4 * q; x < std::min(n, 4 * q + 4); ++x)
+                for (int e = indptr[x]; e < indptr[x + 1]; ++e) {
+                    int *c = &cnt[(size_t)indices[e] * Hq];
+                    d += 2 * (c[b] - c[a]) + 2;
+                    --c[a];
+                    ++c[b];
+                }
+            return d;
+        };
+        for (int pass = 0; pass < 6; ++pass) {
+            bool any = false;
+            for (int j0 = 0; j0 < Q; j0 += C) {
+                const int m = std::min(C, Q - j0);
+                for (int x = 0; x < m; ++x)
+                    for (int y = x + 1; y < m; ++y) {
+                        const int qa = order[j0 + x], qb = order[j0 + y], a = x % Hq, b = y % Hq;
+                        if (a == b) continue;
+                        const long long d = move(qa, a, b) + move(qb, b, a);
+                        if (d < 0) { std::swap(order[j0 + x], order[j0 + y]); any = true; }
+                        else { move(qb, a, b); move(qa, b, a); }
+                    }
+            }
+            if (!any) break;
+        }
+    }
     // chunk j of C quads -> warp-row (t, w)
     out->quad_of.assign(Qp, 0xFFFFFFFFu);
     const int chunks = (Q + C - 1) / C;
