@@ -503,9 +503,8 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                 float ts0 = 0.f, ts1 = 0.f;
                 // The adds of a group run one group behind its loads: while the four LDS.128 of group g are in flight the
                 // packed adds of group g - 1 issue (a warp issues in order, so without this every group paid the full
-                // shared-memory latency before its first add).
-                float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0, p2 = p0, p3 = p0;
-                float4 pwt = make_float4(0.f, 0.f, 0.f, 0.f);
+                // shared-memory latency before its first add).  The first group is peeled: nothing to add behind it.
+                float4 p0, p1, p2, p3, pwt = make_float4(1.f, 1.f, 1.f, 1.f);
                 auto accumulate = [&](const float4 &v0, const float4 &v1, const float4 &v2, const float4 &v3, const float4 &w) {
                     if (USE_W) {
                         sum0 = __ffma2_rn(make_float2(w.x, w.x), make_float2(v0.x, v0.y), sum0);
@@ -527,21 +526,25 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                         ts1 += (xor_sign(w.x, v0.z) + xor_sign(w.y, v1.z)) + (xor_sign(w.z, v2.z) + xor_sign(w.w, v3.z));
                     }
                 };
-                bool last;
-#pragma unroll 2
-                do {
+                // one group's loads: its slot numbers were fetched a group ahead, the next group's are fetched now
+                auto fetch = [&](float4 &v0, float4 &v1, float4 &v2, float4 &v3, float4 &w) -> bool {
                     const uint2 o = nxt;
                     po += stride;
                     nxt = IDS ? *po : __ldg(po);
-                    float4 w = make_float4(1.f, 1.f, 1.f, 1.f);
                     if (USE_W) { w = __ldg(pw); }
                     pw += stride;
-                    last = __any_sync(0xffffffffu, (int)o.y < 0);
-                    const float4 v0 = pairs_at(o.x & 0xffffu), v1 = pairs_at(o.x >> 16);
-                    const float4 v2 = pairs_at(o.y & 0xffffu), v3 = pairs_at((o.y >> 16) & 0x7fffu);
+                    v0 = pairs_at(o.x & 0xffffu); v1 = pairs_at(o.x >> 16);
+                    v2 = pairs_at(o.y & 0xffffu); v3 = pairs_at((o.y >> 16) & 0x7fffu);
+                    return __any_sync(0xffffffffu, (int)o.y < 0);
+                };
+                bool last = fetch(p0, p1, p2, p3, pwt);
+#pragma unroll 2
+                while (!last) {
+                    float4 v0, v1, v2, v3, w = make_float4(1.f, 1.f, 1.f, 1.f);
+                    last = fetch(v0, v1, v2, v3, w);
                     accumulate(p0, p1, p2, p3, pwt);
                     p0 = v0; p1 = v1; p2 = v2; p3 = v3; pwt = w;
-                } while (!last);
+                }
                 accumulate(p0, p1, p2, p3, pwt);
                 if (MODE >= 1) { S[0] += xor_sign(ts0, own.x); S[1] += xor_sign(ts1, own.z); }
                 if (MODE >= 2) {
