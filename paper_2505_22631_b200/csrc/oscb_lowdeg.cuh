@@ -48,7 +48,8 @@ struct LowdegArgs {
     double target, w_total;
     const uint32_t *quad_of;        // [Qp] quad at a position; >= Q: none (ghost item)
     const uint4 *soff;              // byte offsets of a group's four neighbour slots (replica 0 of the tile)
-    const uint2 *sidx;              // k_lowdeg_pair: the same groups as 4 x u16 SLOT numbers (bit 15 of the 4th: last group of the row)
+    const uint2 *sidx;              // k_lowdeg_pair: the same groups as 4 x u16 SLOT numbers
+    const uint32_t *row_groups;     // k_lowdeg_pair: [W][QPT] group counts of an item's four rows in visiting order, a byte each
     const float4 *swt;              // N = 2: their couplings
     const int *warp_start;          // looped streams: first group row of each warp
     const float *hks_table;         // [steps + 1]  h ks(step) (x2 for N = 2), float64 on the host
@@ -496,6 +497,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                 }
             }
             float ynew[4][2];
+            const uint32_t gcount = __ldg(a.row_groups + warp * QPT + t);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const float4 own = *reinterpret_cast<const float4 *>(smem_raw + own0 + t * tbytes + k * kbytes);
@@ -526,22 +528,24 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
                         ts1 += (xor_sign(w.x, v0.z) + xor_sign(w.y, v1.z)) + (xor_sign(w.z, v2.z) + xor_sign(w.w, v3.z));
                     }
                 };
-                // one group's loads: its slot numbers were fetched a group ahead, the next group's are fetched now
-                auto fetch = [&](float4 &v0, float4 &v1, float4 &v2, float4 &v3, float4 &w) -> bool {
+                // one group's loads: its slot numbers were fetched a group ahead, the next group's are fetched now (the last
+                // group of a warp's stream prefetches the pad row behind it)
+                auto fetch = [&](float4 &v0, float4 &v1, float4 &v2, float4 &v3, float4 &w) {
                     const uint2 o = nxt;
                     po += stride;
                     nxt = IDS ? *po : __ldg(po);
                     if (USE_W) { w = __ldg(pw); }
                     pw += stride;
                     v0 = pairs_at(o.x & 0xffffu); v1 = pairs_at(o.x >> 16);
-                    v2 = pairs_at(o.y & 0xffffu); v3 = pairs_at((o.y >> 16) & 0x7fffu);
-                    return __any_sync(0xffffffffu, (int)o.y < 0);
+                    v2 = pairs_at(o.y & 0xffffu); v3 = pairs_at(o.y >> 16);
                 };
-                bool last = fetch(p0, p1, p2, p3, pwt);
+                // the row's group count is warp-uniform and known up front: a counted loop, no vote per group
+                const int G = (int)((gcount >> (8 * k)) & 0xffu);
+                fetch(p0, p1, p2, p3, pwt);
 #pragma unroll 2
-                while (!last) {
+                for (int g = 1; g < G; ++g) {
                     float4 v0, v1, v2, v3, w = make_float4(1.f, 1.f, 1.f, 1.f);
-                    last = fetch(v0, v1, v2, v3, w);
+                    fetch(v0, v1, v2, v3, w);
                     accumulate(p0, p1, p2, p3, pwt);
                     p0 = v0; p1 = v1; p2 = v2; p3 = v3; pwt = w;
                 }

@@ -35,6 +35,7 @@ struct LowdegStreamHost {
     int group_rows = 0;                 // group rows (of C entries) without the prefetch pad
     int64_t real = 0;
     std::vector<int64_t> warp_groups;   // group rows per warp (work balance)
+    std::vector<uint32_t> row_groups;   // looped form: [W][QPT] the group counts of an item's four rows, one byte each (saturating at 255)
 };
 
 struct LowdegPlan {
@@ -47,6 +48,7 @@ struct LowdegPlan {
     size_t n_ids = 0;            // entries of sidx
     DevBuf<float4> swt;
     DevBuf<int> warp_start;
+    DevBuf<uint32_t> row_groups; // two-replica form: group counts of the rows (a byte each), [W][QPT]
 };
 
 static size_t lowdeg_smem_bytes(const LowdegShape &s, uint32_t *off_cnt, uint32_t *off_part, uint32_t *off_misc)
@@ -246,8 +248,9 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
         for (int w = 0; w < W; ++w) out->warp_groups[w] = (int64_t)QPT * 4;
     } else {
         // per warp: t, k, g in the order the kernel walks them
-        int rows = 0;
+        int rows = 0, max_groups = 0;
         std::vector<int> rows_now(C);
+        out->row_groups.assign((size_t)W * QPT, 0);
         for (int w = 0; w < W; ++w) {
             out->warp_start[w] = rows;
             for (int t = 0; t < QPT; ++t)
@@ -258,6 +261,8 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
                         if (i >= 0) G = std::max(G, groups(i));
                     }
                     schedule_rows(rows_now.data(), G);
+                    out->row_groups[(size_t)w * QPT + t] |= (uint32_t)std::min(G, 255) << (8 * k);
+                    max_groups = std::max(max_groups, G);
                     for (int g = 0; g < G; ++g) {
                         for (int c = 0; c < C; ++c) emit(g, c, g == G - 1);
                         ++rows;
@@ -266,6 +271,7 @@ static void compile_lowdeg_stream(int n, const int *indptr, const int *indices, 
             out->warp_groups[w] = rows - out->warp_start[w];
         }
         out->group_rows = rows;
+        OSCB_REQUIRE(s.rpl != 2 || max_groups <= 255, "k_lowdeg_pair takes rows of up to 1020 neighbours");
         std::fill(rows_now.begin(), rows_now.end(), -1);
         schedule_rows(rows_now.data(), 1);
         for (int c = 0; c < C; ++c) emit(0, c, true);           // the prefetch pad row
@@ -328,7 +334,7 @@ static bool choose_lowdeg_shape(const oscb_graph *g, const oscb_run_params *p, i
         if (want_rt <= 0 && RT > 1 && RT / 2 >= R) continue;      // do not pad a tile more than 2x
       for (int rpl = 1; rpl <= 2; ++rpl) {
         // two replicas per lane (k_lowdeg_pair): N = 2 on a looped stream, tiles of an even number of replicas
-        if (rpl == 2 && (nmode != 2 || uniform || RT < 2)) continue;
+        if (rpl == 2 && (nmode != 2 || uniform || RT < 2 || g->max_degree > 1020)) continue;
         if (want_rpl > 0 && rpl != want_rpl) continue;
         const int C = 32 * rpl / RT;
         const int rows = (Q + C - 1) / C;
@@ -386,18 +392,19 @@ static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegSh
     const size_t entries = h.off.size() / 4;
     std::vector<uint2> idx16;
     if (s.rpl == 2) {
-        OSCB_REQUIRE((size_t)4 * s.Qp + OSCB_LD_PADS <= 32768, "internal: k_lowdeg_pair slot numbers exceed 15 bits");
+        OSCB_REQUIRE((size_t)4 * s.Qp + OSCB_LD_PADS <= 65536, "internal: k_lowdeg_pair slot numbers exceed 16 bits");
         idx16.resize(entries);
         const uint32_t sb = (uint32_t)s.RT * 8u;
         for (size_t e = 0; e < entries; ++e) {
             uint32_t id[4];
             for (int u = 0; u < 4; ++u) id[u] = (h.off[4 * e + u] & 0x7fffffffu) / sb;
-            if (h.off[4 * e + 3] & 0x80000000u) id[3] |= 0x8000u;
             idx16[e] = make_uint2(id[0] | (id[1] << 16), id[2] | (id[3] << 16));
         }
         plan->sidx.alloc(entries);
         plan->sidx.upload(idx16.data(), entries, st);
         plan->n_ids = entries;
+        plan->row_groups.alloc(h.row_groups.size());
+        plan->row_groups.upload(h.row_groups.data(), h.row_groups.size(), st);
     }
     plan->soff.alloc(entries);
     plan->soff.upload(reinterpret_cast<const uint4 *>(h.off.data()), entries, st);
@@ -419,7 +426,7 @@ static std::shared_ptr<LowdegPlan> get_lowdeg_plan(oscb_graph *g, const LowdegSh
 static bool lowdeg_pair_resident_shape(oscb_graph *g, const oscb_run_params *p, int64_t R, LowdegShape *out)
 {
     int nmode;
-    if (!lowdeg_kind(g, p, &nmode) || nmode != 2 || !g->unit_weights || g->max_degree <= 4) return false;
+    if (!lowdeg_kind(g, p, &nmode) || nmode != 2 || !g->unit_weights || g->max_degree <= 4 || g->max_degree > 1020) return false;
     if (getenv("OSCB_LOWDEG_RT") || getenv("OSCB_LOWDEG_QPT") || getenv("OSCB_LOWDEG_RPL")) return false;   // pinned shapes: the general chooser
     if (p->replicas_per_cta > 0 && p->replicas_per_cta != 8) return false;
     const int RT = 8, C = 8, Q = (int)((g->n + 3) / 4), rows = (Q + C - 1) / C;
@@ -540,7 +547,7 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     a.maximize = maximize; a.use_target = p->use_target; a.n_sample_steps = (int)sample_steps.size();
     a.step_begin = (int)p->first_step; a.step_end = (int)(p->first_step + steps); a.cadence = (int)cadence; a.trace_stride = S;
     a.target = p->target_objective; a.w_total = plan->w_total;
-    a.quad_of = plan->quad_of.p; a.soff = plan->soff.p; a.sidx = plan->sidx.p; a.swt = plan->swt.p; a.warp_start = plan->warp_start.p;
+    a.quad_of = plan->quad_of.p; a.soff = plan->soff.p; a.sidx = plan->sidx.p; a.swt = plan->swt.p; a.warp_start = plan->warp_start.p; a.row_groups = plan->row_groups.p;
     a.hks_table = d_hks.p; a.seeds = d_seeds.p; a.sample_steps = d_samples.p;
     if (nmode == 3) fast_state_boundaries(3, a.bnd);
     a.io = d_io.p; a.best_obj = d_best.p; a.energy = d_energy.p; a.best_trace = d_btrace.p; a.best_states = d_best_states.p;
