@@ -5,7 +5,7 @@ import numpy as np
 import paper_2505_22631_b200 as pkg
 from paper_2505_22631_b200 import dynamics, workloads
 
-which = sys.argv[1:] or ["resident", "cluster", "stream", "dense-tc", "lowdeg", "dense-splitk"]
+which = sys.argv[1:] or ["resident", "cluster", "stream", "dense-tc", "lowdeg", "lowdeg-pair", "dense-splitk"]
 u, v, w = workloads.random_gnm(128, 700, seed=1, weights=(1.0,))
 J = pkg.CouplingMatrix.from_edges(128, (u, v, w))
 p = pkg.SolverParams.tuned_for(128, 2, seed=0, t_stop=0.6)
@@ -44,6 +44,24 @@ if "lowdeg" in which:
     Jc = pkg.CouplingMatrix.from_edges(203, (uc, vc, wc))
     b = pkg.run_batch(Jc, pkg.SolverParams.tuned_for(203, 3, seed=0, t_stop=0.4), "coloring", list(range(37)), kernel="lowdeg")
     print("lowdeg looped N=3", b.kernel, b.replicas_per_cta, b.best_objective.min())
+if "lowdeg-pair" in which:
+    # k_lowdeg_pair pinned: weighted and unit couplings (slot stream in shared memory), and the headline route (G22 shape,
+    # enough 8-replica tiles to fill the GPU) for a few steps
+    import os
+    os.environ["OSCB_LOWDEG_RPL"] = "2"
+    us, vs, ws = workloads.random_gnm(203, 520, seed=5, weights=(1.0, -1.0, 2.0))
+    Js = pkg.CouplingMatrix.from_edges(203, (us, vs, ws))
+    uu, vu, wu = workloads.random_gnm(301, 1500, seed=7)
+    Ju = pkg.CouplingMatrix.from_edges(301, (uu, vu, wu))
+    for name, Jp in (("weighted", Js), ("unit", Ju)):
+        for rt in (2, 8):
+            b = pkg.run_batch(Jp, pkg.SolverParams.tuned_for(Jp.n, 2, seed=0, t_stop=0.4), "maxcut", list(range(2 * rt + 1)), kernel="lowdeg", replicas_per_cta=rt)
+            print("lowdeg pair", name, "rt", rt, b.kernel, b.replicas_per_cta, b.best_objective.max())
+    del os.environ["OSCB_LOWDEG_RPL"]
+    import bench
+    _, J22, p22, kind, _ = bench.load_workload("G22x1024")
+    b = pkg.run_batch(J22, p22, kind, list(range(896)), steps=3, want_phases=False)
+    print("lowdeg pair headline route", b.kernel, b.replicas_per_cta, b.best_objective.max())
 if "dense-splitk" in which:
     import os
     os.environ["OSCB_UMMA_SPLITK"] = "4"
