@@ -50,6 +50,10 @@ struct LowdegArgs {
     const uint4 *soff;              // byte offsets of a group's four neighbour slots (replica 0 of the tile)
     const uint2 *sidx;              // k_lowdeg_pair: the same groups as 4 x u16 SLOT numbers
     const uint32_t *row_groups;     // k_lowdeg_pair: [W][QPT] group counts of an item's four rows in visiting order, a byte each
+    // k_lowdeg_pair, one window of a mixed-tile schedule (null: CTA b is tile b and runs [step_begin, step_end)):
+    const int *tile_map;            // [grid] the tile (of RT replicas) CTA b integrates ...
+    const int *tile_step;           // [grid] ... from this step on, for window_steps steps (hks_table stays indexed from step_begin)
+    int window_steps;
     const float4 *swt;              // N = 2: their couplings
     const int *warp_start;          // looped streams: first group row of each warp
     const float *hks_table;         // [steps + 1]  h ks(step) (x2 for N = 2), float64 on the host
@@ -394,7 +398,8 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
     const int LPS = a.RT >> 1;                                       // lanes per slot
     const int q = lane & (LPS - 1), c = lane >> (a.LRT - 1);
     const int r0 = 2 * q;
-    const int tile = blockIdx.x, rg0 = tile * a.RT + r0;
+    const int tile = a.tile_map ? __ldg(a.tile_map + blockIdx.x) : (int)blockIdx.x, rg0 = tile * a.RT + r0;
+    const int sb = a.tile_map ? __ldg(a.tile_step + blockIdx.x) : a.step_begin, se = a.tile_map ? sb + a.window_steps : a.step_end;
     const bool live[2] = {rg0 < a.R_real, rg0 + 1 < a.R_real};
     const unsigned char *cs_lane = smem_raw + r0 * 8;                // + slot byte offset: the pairs of replicas r0, r0 + 1
     const int WC = a.W * a.C;
@@ -462,11 +467,11 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
     const uint2 *so = (IDS ? reinterpret_cast<const uint2 *>(smem_raw + a.off_ids) : a.sidx) + first_row * a.C + c;
     const float4 *sw = a.swt + first_row * a.C + c;
 
-    bool pending = true;
+    bool pending = sb == a.step_begin;        // the read-out of the state the run starts from (a later window of a schedule: none)
     int pending_col = 0, pending_label = -1, sample_cur = 0;
-    while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < a.step_begin) ++sample_cur;
+    while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < sb) ++sample_cur;
     int next_sample = sample_cur < a.n_sample_steps ? a.sample_steps[sample_cur] : -1;
-    int cmod = a.cadence > 0 ? a.step_begin % a.cadence : 1;
+    int cmod = a.cadence > 0 ? sb % a.cadence : 1;
 
     auto pass_a = [&](auto mode_tag, int step, float hks) {
         constexpr int MODE = decltype(mode_tag)::value;
@@ -643,7 +648,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
     using M2 = std::integral_constant<int, 2>;
     using M3 = std::integral_constant<int, 3>;
 #pragma unroll 1
-    for (int step = a.step_begin; step < a.step_end; ++step) {
+    for (int step = sb; step < se; ++step) {
         const float hks = __ldg(a.hks_table + (step - a.step_begin));
         if (!pending) {
             pass_a(M0{}, step, hks);
@@ -671,7 +676,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(
             pending_label = step;
         }
     }
-    if (pending) pass_a(M3{}, a.step_end, 0.0f);
+    if (pending) pass_a(M3{}, se, 0.0f);
 
     if (tid < a.RT) a.best_obj[tile * a.RT + tid] = best_s[tid];
 #pragma unroll

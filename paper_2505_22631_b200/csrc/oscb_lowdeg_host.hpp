@@ -430,7 +430,9 @@ static bool lowdeg_pair_resident_shape(oscb_graph *g, const oscb_run_params *p, 
     if (getenv("OSCB_LOWDEG_RT") || getenv("OSCB_LOWDEG_QPT") || getenv("OSCB_LOWDEG_RPL")) return false;   // pinned shapes: the general chooser
     if (p->replicas_per_cta > 0 && p->replicas_per_cta != 8) return false;
     const int RT = 8, C = 8, Q = (int)((g->n + 3) / 4), rows = (Q + C - 1) / C;
-    if ((R + RT - 1) / RT < (int64_t)g->sm_count * 3 / 4) return false;
+    int64_t min_tiles = (int64_t)g->sm_count * 3 / 4;
+    if (const char *e = getenv("OSCB_LOWDEG_PAIR_MIN_TILES")) min_tiles = atoll(e);       // (tuning experiments)
+    if ((R + RT - 1) / RT < min_tiles) return false;
     for (int QPT : {4, 5}) {
         const int W = (rows + QPT - 1) / QPT;
         if (W < 8 || W > lowdeg_max_threads(2 * QPT) / 32) continue;
@@ -446,6 +448,66 @@ static bool lowdeg_pair_resident_shape(oscb_graph *g, const oscb_run_params *p, 
         return true;
     }
     return false;
+}
+
+// The tile decomposition quantises the work of a batch: 1024 replicas are 128 tiles of 8, one per SM, and 20 SMs of a B200
+// idle (a 7-replica tile costs what an 8-replica one costs).  A 4-replica tile advances a step in ~0.6 of the time of an
+// 8-replica one, so a + b = all SMs tiles with 8a + 4b = R keep every SM busy if the replicas take turns in the fast lane:
+// the run is cut into windows; in a window F = b / 2 "octets" (groups of 8 replicas) run as two 4-replica tiles for steps4
+// steps while the other a run as 8-replica tiles for steps8 < steps4 steps, the fast set rotates, and after `windows`
+// windows every octet has been fast `turns` times: (windows - turns) * steps8 + turns * steps4 = steps for all of them.
+// Phases, best states and traces live in global memory between windows; the noise is a function of (seed, step, oscillator)
+// and the schedule of the step number, so a replica's trajectory is the one of an unbroken run up to the float32 summation
+// order of the tile shape it happens to be in (which differs between shapes anyway).
+struct MixedTiles {
+    LowdegShape s4;
+    int tiles8 = 0, tiles4 = 0, fast_octets = 0, windows = 0, turns = 0;
+    int64_t steps8 = 0, steps4 = 0;
+};
+
+static bool plan_mixed_tiles(oscb_graph *g, const oscb_run_params *p, const LowdegShape &s8, int64_t R, int64_t steps, MixedTiles *m)
+{
+    if (const char *e = getenv("OSCB_LOWDEG_MIXED")) { if (atoi(e) == 0) return false; }
+    if (s8.rpl != 2 || s8.RT != 8 || !g->unit_weights || R % 8 != 0 || p->replicas_per_cta > 0) return false;
+    const int64_t sms = g->sm_count, octets = R / 8;
+    if (octets >= sms || R < 4 * sms) return false;                 // one tile of 8 per SM fills the GPU / tiles of 4 alone do
+    const int64_t F = sms - octets;                                 // a = octets - F tiles of 8, b = 2 F tiles of 4: a + b = sms
+    if (F < 1 || octets - F < 1) return false;
+    int64_t gg = octets, x = F;
+    while (x) { const int64_t t = gg % x; gg = x; x = t; }
+    const int64_t windows = octets / gg, turns = F / gg;
+    int64_t min_window = 256;
+    if (const char *e = getenv("OSCB_LOWDEG_MIXED_MIN_WINDOW")) min_window = std::max<long long>(1, atoll(e));     // (tests)
+    if (windows > 64 || steps < windows * min_window) return false;
+    // the 4-replica tile shape: 16 quads per warp, slot stream in shared memory like the 8-replica one
+    LowdegShape s4;
+    const int C = 16, rows = (s8.Q + C - 1) / C;
+    bool found = false;
+    for (int QPT : {4, 2, 5}) {
+        const int W = (rows + QPT - 1) / QPT;
+        if (W < 4 || W > lowdeg_max_threads(2 * QPT) / 32) continue;
+        s4.RT = 4; s4.LRT = 2; s4.C = C; s4.W = W; s4.QPT = QPT; s4.Q = s8.Q; s4.Qp = W * QPT * C; s4.uniform = false; s4.rpl = 2;
+        s4.smem = lowdeg_smem_bytes(s4, nullptr, nullptr, nullptr);
+        if (s4.smem > (size_t)g->smem_optin || (size_t)4 * s4.Qp + OSCB_LD_PADS > 65536) continue;
+        auto plan4 = get_lowdeg_plan(g, s4, 2);
+        if (s4.smem + ((plan4->n_ids * sizeof(uint2) + 15) & ~(size_t)15) > (size_t)g->smem_optin) continue;
+        found = true;
+        break;
+    }
+    if (!found) return false;
+    // steps of a window in the two lanes: steps4 / steps8 ~ the measured ratio of the step times (G22 shape: 16.7 / 10.1 us)
+    double ratio = 1.65;
+    if (const char *e = getenv("OSCB_LOWDEG_MIXED_RATIO")) ratio = std::max(1.0, atof(e));
+    const int64_t slow = windows - turns;
+    int64_t w0 = (int64_t)std::llround((double)steps / ((double)slow + (double)turns * ratio));
+    int64_t steps8 = -1;
+    for (int64_t d = 0; d <= turns && steps8 < 0; ++d)
+        for (int64_t w : {w0 - d, w0 + d})
+            if (w >= 1 && steps - slow * w >= turns && (steps - slow * w) % turns == 0 && (steps - slow * w) / turns >= w) { steps8 = w; break; }
+    if (steps8 < 0) return false;
+    m->s4 = s4; m->tiles8 = (int)(octets - F); m->tiles4 = (int)(2 * F); m->fast_octets = (int)F;
+    m->windows = (int)windows; m->turns = (int)turns; m->steps8 = steps8; m->steps4 = (steps - slow * steps8) / turns;
+    return true;
 }
 
 bool lowdeg_applies(oscb_graph *g, const oscb_run_params *p, int64_t R, bool forced)
@@ -474,11 +536,11 @@ static void launch_lowdeg(oscb_graph *g, const LowdegArgs &a, const LowdegShape 
 }
 
 template <bool UNITW, bool IDS>
-static void launch_lowdeg_pair(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles, size_t smem)
+static void launch_lowdeg_pair(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles, size_t smem, cudaStream_t stream = nullptr)
 {
     auto go = [&](auto kernel) {
         OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        kernel<<<tiles, s.W * 32, smem, g->stream>>>(a);
+        kernel<<<tiles, s.W * 32, smem, stream ? stream : g->stream>>>(a);
     };
     switch (s.QPT) {
     case 1: go(k_lowdeg_pair<1, UNITW, IDS>); break;
@@ -565,7 +627,83 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
         else if (sh.uniform) launch_lowdeg<NM, true, false>(g, a, sh, tiles);
         else launch_lowdeg<NM, false, false>(g, a, sh, tiles);
     };
-    if (sh.rpl == 2) {
+    int launches = 1;
+    MixedTiles mix;
+    if (sh.rpl == 2 && plan_mixed_tiles(g, p, sh, R, steps, &mix)) {
+        // 8a + 4b = R replicas on a + b = all SMs (see plan_mixed_tiles): every window launches the a 8-replica tiles and the b
+        // 4-replica tiles side by side on two streams; a window ends when both have.
+        auto plan4 = get_lowdeg_plan(g, mix.s4, nmode);
+        LowdegArgs a4 = a;
+        a4.Qp = mix.s4.Qp; a4.RT = mix.s4.RT; a4.LRT = mix.s4.LRT; a4.C = mix.s4.C; a4.W = mix.s4.W;
+        lowdeg_smem_bytes(mix.s4, &a4.off_cnt, &a4.off_part, &a4.off_misc);
+        a4.quad_of = plan4->quad_of.p; a4.soff = plan4->soff.p; a4.sidx = plan4->sidx.p; a4.swt = plan4->swt.p;
+        a4.warp_start = plan4->warp_start.p; a4.row_groups = plan4->row_groups.p;
+        const size_t ids8 = (plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15, ids4 = (plan4->n_ids * sizeof(uint2) + 15) & ~(size_t)15;
+        a.off_ids = (uint32_t)sh.smem; a.n_ids = (uint32_t)plan->n_ids;
+        a4.off_ids = (uint32_t)mix.s4.smem; a4.n_ids = (uint32_t)plan4->n_ids;
+        const size_t smem8 = sh.smem + ids8, smem4 = mix.s4.smem + ids4;
+        launched_smem = smem8;
+        // per window: [tiles of 8: map, first step][tiles of 4: map, first step]
+        const int n8 = mix.tiles8, n4t = mix.tiles4, per = 2 * (n8 + n4t);
+        std::vector<int> h_map((size_t)mix.windows * per);
+        std::vector<int64_t> done(R / 8, 0);
+        for (int j = 0; j < mix.windows; ++j) {
+            int *m8 = &h_map[(size_t)j * per], *s8 = m8 + n8, *m4 = s8 + n8, *s4 = m4 + n4t;
+            std::vector<char> fast(R / 8, 0);
+            for (int i = 0; i < mix.fast_octets; ++i) fast[((int64_t)j * mix.fast_octets + i) % (R / 8)] = 1;
+            int c8 = 0, c4 = 0;
+            for (int o = 0; o < R / 8; ++o) {
+                const int at = (int)(p->first_step + done[o]);
+                if (fast[o]) {
+                    m4[c4] = 2 * o; s4[c4++] = at;
+                    m4[c4] = 2 * o + 1; s4[c4++] = at;
+                    done[o] += mix.steps4;
+                } else {
+                    m8[c8] = o; s8[c8++] = at;
+                    done[o] += mix.steps8;
+                }
+            }
+            OSCB_REQUIRE(c8 == n8 && c4 == n4t, "internal: mixed-tile window %d deals %d + %d tiles", j, c8, c4);
+        }
+        for (int o = 0; o < R / 8; ++o) OSCB_REQUIRE(done[o] == steps, "internal: mixed-tile schedule ends at step %lld", (long long)done[o]);
+        DevBuf<int> d_map(h_map.size());
+        d_map.upload(h_map.data(), h_map.size(), s);
+        OSCB_CUDA(cudaStreamSynchronize(s));
+        cudaStream_t s2;
+        OSCB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        std::vector<cudaEvent_t> e8(mix.windows), e4(mix.windows);
+        for (auto &e : e8) OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto &e : e4) OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        OSCB_CUDA(cudaEventRecord(ev0, s));                 // (again: the schedule upload is not part of the integration)
+        cudaEvent_t fork;
+        OSCB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        OSCB_CUDA(cudaEventRecord(fork, s));
+        OSCB_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+        a.window_steps = (int)mix.steps8;
+        a4.window_steps = (int)mix.steps4;
+        for (int j = 0; j < mix.windows; ++j) {
+            const int *base = d_map.p + (size_t)j * per;
+            a.tile_map = base; a.tile_step = base + n8;
+            a4.tile_map = base + 2 * n8; a4.tile_step = base + 2 * n8 + n4t;
+            if (j > 0) {
+                OSCB_CUDA(cudaStreamWaitEvent(s, e4[j - 1], 0));
+                OSCB_CUDA(cudaStreamWaitEvent(s2, e8[j - 1], 0));
+            }
+            launch_lowdeg_pair<true, true>(g, a, sh, n8, smem8, s);
+            launch_lowdeg_pair<true, true>(g, a4, mix.s4, n4t, smem4, s2);
+            OSCB_CUDA(cudaEventRecord(e8[j], s));
+            OSCB_CUDA(cudaEventRecord(e4[j], s2));
+        }
+        OSCB_CUDA(cudaStreamWaitEvent(s, e4[mix.windows - 1], 0));
+        OSCB_CUDA(cudaEventRecord(ev1, s));
+        OSCB_CUDA(cudaStreamSynchronize(s));                // the schedule, the events and the second stream go out of scope here
+        for (auto &e : e8) cudaEventDestroy(e);
+        for (auto &e : e4) cudaEventDestroy(e);
+        cudaEventDestroy(fork);
+        cudaStreamDestroy(s2);
+        launches = 2 * mix.windows;
+    }
+    else if (sh.rpl == 2) {
         // the slot stream goes to shared memory when it fits behind the pairs (OSCB_LOWDEG_IDS=0: never)
         const size_t ids_bytes = (plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15;
         const bool want_ids = !(getenv("OSCB_LOWDEG_IDS") && atoi(getenv("OSCB_LOWDEG_IDS")) == 0);
@@ -578,7 +716,7 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     }
     else if (nmode == 2) by_shape(std::integral_constant<int, 2>{});
     else by_shape(std::integral_constant<int, 3>{});
-    OSCB_CUDA(cudaEventRecord(ev1, s));
+    if (launches == 1) OSCB_CUDA(cudaEventRecord(ev1, s));
     {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) {
@@ -611,7 +749,7 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     if (out->first_hit_step)
         for (int r = 0; r < R; ++r) out->first_hit_step[r] = h_first[r];
     out->device_ms = ms;
-    out->kernel_launches = 1;
+    out->kernel_launches = launches;
     out->kernel_used = OSCB_KERNEL_LOWDEG;
     out->replicas_per_cta = RT;
     out->smem_bytes = (int64_t)launched_smem;

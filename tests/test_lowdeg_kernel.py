@@ -275,6 +275,46 @@ def test_pair_kernel_noise_is_a_function_of_seed_step_and_oscillator(pkg, monkey
 
 
 @gpu
+def test_mixed_tile_schedule_is_the_same_run(pkg, oracle, monkeypatch):
+    """1024 replicas of the G22 shape are 128 tiles of 8 on 148 SMs; the run is therefore cut into windows in which 20 of
+    the 128 octets take turns as 4-replica tiles on the idle SMs (plan_mixed_tiles).  With windows of a few steps forced:
+    the noise-free trajectory, the energy trace and the read-out still follow the oracle, the schedule is deterministic, and
+    with noise ON it stays next to the unbroken launch (same noise per (seed, step, oscillator); only the float32 summation
+    order differs between the tile shapes)."""
+    import bench
+    _, J, _, kind, R = bench.load_workload("G22x1024")
+    steps = 64
+    params = pkg.SolverParams.tuned_for(J.n, 2, seed=5, K=0.2, ks_max=1.0, kn=0.0)
+    seeds = [params.seed + r for r in range(R)]
+    stride = steps * params.h / 4.5
+    monkeypatch.setenv("OSCB_LOWDEG_MIXED_MIN_WINDOW", "1")
+    got = pkg.run_batch(J, params, kind, seeds, steps=steps, trace_stride=stride)
+    assert got.kernel == "lowdeg" and got.kernel_launches == 64 and got.steps == steps        # 32 windows x (tiles of 8 | tiles of 4)
+    sub = list(range(0, R, 37))                                   # octets of every phase of the rotation
+    want = oracle.simulate(J.indptr, J.indices, J.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period, kn=0.0,
+                           h=params.h, t_stop=steps * params.h, n_states=2, seeds=[seeds[r] for r in sub], objective=kind,
+                           trace_stride=stride, threads=oracle.max_threads())
+    assert circ_dist_rad(got.final_phases[sub], want.final_phases).max() <= 1e-4
+    assert np.array_equal(got.trace_t, want.trace_t)
+    scale = np.abs(J.data).sum() / 2
+    assert np.abs(got.energy[sub] - want.energy).max() <= 2e-5 * scale
+    assert np.array_equal(_objective(J, got.best_states, kind), got.best_objective)
+    assert np.all(np.diff(got.best_trace, axis=1) >= 0)
+    assert np.abs(got.best_objective[sub] - want.best_objective).max() <= max(2.0, 2e-3 * scale)
+    again = pkg.run_batch(J, params, kind, seeds, steps=steps, trace_stride=stride)
+    for f in ("final_phases", "best_states", "best_objective", "energy", "best_trace"):
+        assert np.array_equal(getattr(got, f), getattr(again, f)), f
+    # noise on: next to the unbroken launch
+    noisy = pkg.SolverParams.tuned_for(J.n, 2, seed=5, K=0.2, ks_max=1.0, kn=0.15)
+    a = pkg.run_batch(J, noisy, kind, seeds, steps=steps, want_states=False)
+    monkeypatch.setenv("OSCB_LOWDEG_MIXED", "0")
+    b = pkg.run_batch(J, noisy, kind, seeds, steps=steps, want_states=False)
+    assert a.kernel_launches == 64 and b.kernel_launches == 1 and b.kernel == "lowdeg"
+    assert circ_dist_rad(a.final_phases, b.final_phases).max() <= 2e-4
+    assert np.abs(a.best_objective - b.best_objective).max() <= 6.0
+
+
+@gpu
 @pytest.mark.parametrize("N,kind", [(2, "maxcut"), (3, "coloring")])
 def test_noise_on_distribution_matches_the_oracle(pkg, oracle, N, kind):
     """Noise ON (device Philox vs numpy's stream replayed by the oracle): best objectives over 128 seeds agree in
