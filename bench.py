@@ -808,6 +808,12 @@ def main():
                 "note": "the persistent kernel keeps phases and pairs on chip for the whole window, so DRAM traffic is ~0 "
                         "by design and the HBM fraction is small by construction; shared-memory gather bandwidth and "
                         "instruction issue bind (DESIGN.md section 4)"}
+    if last.kernel in ("resident", "lowdeg", "cluster") and last.kernel_launches > 1:
+        # the mixed-tile schedule of k_lowdeg_pair: windows of two concurrent grids (tiles of 8 and of 4 replicas); the unit
+        # the figures above are quoted per is the whole schedule of one bench step, not one of its launches
+        roofline["launches_per_step"] = int(last.kernel_launches)
+        roofline["note"] += ("; one bench step is a schedule of %d launches (windows x two concurrent grids on two streams), "
+                             "achieved = algorithmic bytes of the step / its device time" % last.kernel_launches)
 
     line = {
         "metric": "oscillator-edge updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
