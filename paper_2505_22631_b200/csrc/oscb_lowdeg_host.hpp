@@ -428,24 +428,32 @@ static bool lowdeg_pair_resident_shape(oscb_graph *g, const oscb_run_params *p, 
     int nmode;
     if (!lowdeg_kind(g, p, &nmode) || nmode != 2 || !g->unit_weights || g->max_degree <= 4 || g->max_degree > 1020) return false;
     if (getenv("OSCB_LOWDEG_RT") || getenv("OSCB_LOWDEG_QPT") || getenv("OSCB_LOWDEG_RPL")) return false;   // pinned shapes: the general chooser
-    if (p->replicas_per_cta > 0 && p->replicas_per_cta != 8) return false;
-    const int RT = 8, C = 8, Q = (int)((g->n + 3) / 4), rows = (Q + C - 1) / C;
-    int64_t min_tiles = (int64_t)g->sm_count * 3 / 4;
-    if (const char *e = getenv("OSCB_LOWDEG_PAIR_MIN_TILES")) min_tiles = atoll(e);       // (tuning experiments)
-    if ((R + RT - 1) / RT < min_tiles) return false;
-    for (int QPT : {4, 5}) {
-        const int W = (rows + QPT - 1) / QPT;
-        if (W < 8 || W > lowdeg_max_threads(2 * QPT) / 32) continue;
-        LowdegShape s;
-        s.RT = RT; s.LRT = 3; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = false; s.rpl = 2;
-        s.smem = lowdeg_smem_bytes(s, nullptr, nullptr, nullptr);
-        s.cost = 0.0;
-        if (s.smem > (size_t)g->smem_optin || (size_t)4 * s.Qp + OSCB_LD_PADS > 32768) continue;
-        if (s.smem + (size_t)g->nnz * 2 > (size_t)g->smem_optin) continue;        // even an unpadded stream would not fit
-        auto plan = get_lowdeg_plan(g, s, nmode);
-        if (s.smem + ((plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15) > (size_t)g->smem_optin) continue;
-        *out = s;
-        return true;
+    const int Q = (int)((g->n + 3) / 4);
+    const int64_t sms = g->sm_count;
+    // tiles of 8 replicas once tiles of 4 no longer fit one per SM (measured on the G22 shape: 2.45 T at 1024 replicas, 1.52 T
+    // at 640 against 1.29 T for k_resident_fast); tiles of 4 below that while they still fill most of the GPU (2.02 T at 512
+    // against 1.71 T, 2.34 T at 592 against 1.98 T); smaller batches stay with k_resident_fast's 1- and 2-replica tiles
+    for (int RT : {8, 4}) {
+        if (p->replicas_per_cta > 0 && p->replicas_per_cta != RT) continue;
+        const int64_t tiles = (R + RT - 1) / RT;
+        int64_t min_tiles = RT == 8 ? sms / 2 + 1 : sms * 3 / 5;
+        if (const char *e = getenv("OSCB_LOWDEG_PAIR_MIN_TILES")) min_tiles = atoll(e);       // (tuning experiments)
+        if (tiles < min_tiles || (RT == 4 && tiles > sms)) continue;
+        const int C = 64 / RT, rows = (Q + C - 1) / C;
+        for (int QPT : {4, 5, 2}) {
+            const int W = (rows + QPT - 1) / QPT;
+            if (W < (RT == 8 ? 8 : 4) || W > lowdeg_max_threads(2 * QPT) / 32) continue;
+            LowdegShape s;
+            s.RT = RT; s.LRT = RT == 8 ? 3 : 2; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = false; s.rpl = 2;
+            s.smem = lowdeg_smem_bytes(s, nullptr, nullptr, nullptr);
+            s.cost = 0.0;
+            if (s.smem > (size_t)g->smem_optin || (size_t)4 * s.Qp + OSCB_LD_PADS > 65536) continue;
+            if (s.smem + (size_t)g->nnz * 2 > (size_t)g->smem_optin) continue;        // even an unpadded stream would not fit
+            auto plan = get_lowdeg_plan(g, s, nmode);
+            if (s.smem + ((plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15) > (size_t)g->smem_optin) continue;
+            *out = s;
+            return true;
+        }
     }
     return false;
 }

@@ -350,6 +350,8 @@ def test_auto_selection_and_fallbacks(pkg):
     # ... unless the batch fills the GPU with 8-replica tiles whose slot stream fits in shared memory: k_lowdeg_pair
     big = pkg.run_batch(J22, p22, "maxcut", list(range(1024)), steps=4, want_phases=False, want_states=False)
     assert big.kernel == "lowdeg" and big.replicas_per_cta == 8
+    mid = pkg.run_batch(J22, p22, "maxcut", list(range(512)), steps=4, want_phases=False, want_states=False)
+    assert mid.kernel == "lowdeg" and mid.replicas_per_cta == 4          # tiles of 4 while they fit one per SM
     assert pkg.run_batch(J22, p22, "maxcut", list(range(8)), steps=4, kernel="lowdeg").kernel == "lowdeg"      # on request: any degree
     with pytest.raises(ValueError):
         pkg.run_batch(J22, p22, "maxcut", [0], steps=4, kernel="lowdeg", precision="f64")                      # float32 only

@@ -62,6 +62,12 @@ if "lowdeg-pair" in which:
     _, J22, p22, kind, _ = bench.load_workload("G22x1024")
     b = pkg.run_batch(J22, p22, kind, list(range(896)), steps=3, want_phases=False)
     print("lowdeg pair headline route", b.kernel, b.replicas_per_cta, b.best_objective.max())
+    os.environ["OSCB_LOWDEG_MIXED_MIN_WINDOW"] = "1"                     # the mixed-tile schedule with windows of a few steps
+    b = pkg.run_batch(J22, p22, kind, list(range(1024)), steps=64, want_phases=False)
+    print("lowdeg pair mixed-tile schedule", b.kernel, b.kernel_launches, b.best_objective.max())
+    del os.environ["OSCB_LOWDEG_MIXED_MIN_WINDOW"]
+    b = pkg.run_batch(J22, p22, kind, list(range(500)), steps=3, want_phases=False)
+    print("lowdeg pair tiles of 4", b.kernel, b.replicas_per_cta, b.best_objective.max())
 if "dense-splitk" in which:
     import os
     os.environ["OSCB_UMMA_SPLITK"] = "4"
