@@ -70,6 +70,8 @@ struct LowdegArgs {
 // threads per CTA by items per thread: the phases of QPT quads stay in registers, so more items need more registers
 // per thread (64 / 80 / 128)
 __host__ __device__ constexpr int lowdeg_max_threads(int qpt) { return qpt <= 4 ? 1024 : (qpt <= 7 ? 768 : 512); }
+// k_lowdeg_pair holds two replicas per lane: from two items per thread on it wants the 128 registers of a 512-thread CTA
+__host__ __device__ constexpr int lowdeg_pair_max_threads(int qpt) { return qpt <= 1 ? 1024 : 512; }
 
 // x - floor(x) on the FMA/ALU pipes for |x| < 2^22 (the conversion unit is as busy as the MUFU unit here): the
 // magic-number add rounds x to the nearest integer, a compare steps it down to the floor.  Anything larger (or
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
 // IDS: the slot stream is staged in shared memory behind the pairs (when both fit: G22 shape, 8 replicas: 129 + 95 KB), so
 // a group's slot numbers come back in an LDS latency instead of an L1 / L2 one.
 template <int QPT, bool UNITW, bool IDS>
-__global__ void __launch_bounds__(lowdeg_max_threads(2 * QPT), 1) k_lowdeg_pair(const LowdegArgs a)
+__global__ void __launch_bounds__(lowdeg_pair_max_threads(QPT), 1) k_lowdeg_pair(const LowdegArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

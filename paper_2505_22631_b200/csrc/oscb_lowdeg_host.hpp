@@ -341,7 +341,7 @@ static bool choose_lowdeg_shape(const oscb_graph *g, const oscb_run_params *p, i
         for (int QPT : kLowdegQpt) {
             if (want_qpt > 0 && QPT != want_qpt) continue;
             if (rpl == 2 && QPT > 5) continue;
-            const int maxW = lowdeg_max_threads(rpl * QPT) / 32;
+            const int maxW = (rpl == 2 ? lowdeg_pair_max_threads(QPT) : lowdeg_max_threads(QPT)) / 32;
             const int W = (rows + QPT - 1) / QPT;
             if (W > maxW || W < 1) continue;
             LowdegShape s;
@@ -440,9 +440,9 @@ static bool lowdeg_pair_resident_shape(oscb_graph *g, const oscb_run_params *p, 
         if (const char *e = getenv("OSCB_LOWDEG_PAIR_MIN_TILES")) min_tiles = atoll(e);       // (tuning experiments)
         if (tiles < min_tiles || (RT == 4 && tiles > sms)) continue;
         const int C = 64 / RT, rows = (Q + C - 1) / C;
-        for (int QPT : {4, 5, 2}) {
+        for (int QPT : {RT == 8 ? 4 : 2, RT == 8 ? 5 : 4, RT == 8 ? 2 : 5}) {          // (16 warps of 128 registers measured best on both)
             const int W = (rows + QPT - 1) / QPT;
-            if (W < (RT == 8 ? 8 : 4) || W > lowdeg_max_threads(2 * QPT) / 32) continue;
+            if (W < (RT == 8 ? 8 : 4) || W > lowdeg_pair_max_threads(QPT) / 32) continue;
             LowdegShape s;
             s.RT = RT; s.LRT = RT == 8 ? 3 : 2; s.C = C; s.W = W; s.QPT = QPT; s.Q = Q; s.Qp = W * QPT * C; s.uniform = false; s.rpl = 2;
             s.smem = lowdeg_smem_bytes(s, nullptr, nullptr, nullptr);
@@ -491,9 +491,9 @@ static bool plan_mixed_tiles(oscb_graph *g, const oscb_run_params *p, const Lowd
     LowdegShape s4;
     const int C = 16, rows = (s8.Q + C - 1) / C;
     bool found = false;
-    for (int QPT : {4, 2, 5}) {
+    for (int QPT : {2, 4, 5}) {
         const int W = (rows + QPT - 1) / QPT;
-        if (W < 4 || W > lowdeg_max_threads(2 * QPT) / 32) continue;
+        if (W < 4 || W > lowdeg_pair_max_threads(QPT) / 32) continue;
         s4.RT = 4; s4.LRT = 2; s4.C = C; s4.W = W; s4.QPT = QPT; s4.Q = s8.Q; s4.Qp = W * QPT * C; s4.uniform = false; s4.rpl = 2;
         s4.smem = lowdeg_smem_bytes(s4, nullptr, nullptr, nullptr);
         if (s4.smem > (size_t)g->smem_optin || (size_t)4 * s4.Qp + OSCB_LD_PADS > 65536) continue;
@@ -503,8 +503,8 @@ static bool plan_mixed_tiles(oscb_graph *g, const oscb_run_params *p, const Lowd
         break;
     }
     if (!found) return false;
-    // steps of a window in the two lanes: steps4 / steps8 ~ the measured ratio of the step times (G22 shape: 16.7 / 10.1 us)
-    double ratio = 1.65;
+    // steps of a window in the two lanes: steps4 / steps8 ~ the measured ratio of the step times (G22 shape: 16.7 / 9.2 us)
+    double ratio = 1.8;
     if (const char *e = getenv("OSCB_LOWDEG_MIXED_RATIO")) ratio = std::max(1.0, atof(e));
     const int64_t slow = windows - turns;
     int64_t w0 = (int64_t)std::llround((double)steps / ((double)slow + (double)turns * ratio));
