@@ -34,6 +34,7 @@
 
 namespace oscb {
 
+#define OSCB_LD_TAB 192       // most CTAs of one launch of a mixed-tile schedule
 #define OSCB_LD_PADS 16      // all-zero pad slots behind the 4 * Qp real ones (one per bank pair)
 
 struct LowdegArgs {
@@ -50,10 +51,12 @@ struct LowdegArgs {
     const uint4 *soff;              // byte offsets of a group's four neighbour slots (replica 0 of the tile)
     const uint2 *sidx;              // k_lowdeg_pair: the same groups as 4 x u16 SLOT numbers
     const uint32_t *row_groups;     // k_lowdeg_pair: [W][QPT] group counts of an item's four rows in visiting order, a byte each
-    // k_lowdeg_pair, one window of a mixed-tile schedule (null: CTA b is tile b and runs [step_begin, step_end)):
-    const int *tile_map;            // [grid] the tile (of RT replicas) CTA b integrates ...
-    const int *tile_step;           // [grid] ... from this step on, for window_steps steps (hks_table stays indexed from step_begin)
-    int window_steps;
+    // one window of a mixed-tile schedule (use_tab = 0: CTA b is tile b and runs [step_begin, step_end)): CTA b integrates tile
+    // tab_tile[b] (of RT replicas) from step tab_step[b] on for window_steps steps (hks_table stays indexed from step_begin).
+    // The table travels in the kernel parameters: a constant-bank read with a uniform index keeps the step counter and all
+    // that hangs on it (Philox counter, schedule look-up, cadence) on the uniform datapath, as in the unbroken launch.
+    int use_tab, window_steps;
+    int tab_tile[OSCB_LD_TAB], tab_step[OSCB_LD_TAB];
     const float4 *swt;              // N = 2: their couplings
     const int *warp_start;          // looped streams: first group row of each warp
     const float *hks_table;         // [steps + 1]  h ks(step) (x2 for N = 2), float64 on the host
@@ -90,14 +93,20 @@ __device__ __forceinline__ float xor_sign(float w, float c)       // w * sigma(c
 
 // NMODE 2: OIM max-cut, integer couplings;  NMODE 3: OPM 3-colouring, unit couplings.
 // RT1: one replica per CTA (a slot offset IS the shared-memory address of the pair).
-template <int NMODE, int QPT, bool UNIFORM, bool RT1>
+// WIN: one window of a mixed-tile schedule (the per-CTA table of LowdegArgs); a separate instantiation, so that the unbroken
+// launch keeps its code (with the table read behind a run-time flag the flat200 kernel lost 6 %).
+template <int NMODE, int QPT, bool UNIFORM, bool RT1, bool WIN = false>
 __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const LowdegArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int r = RT1 ? 0 : (lane & (a.RT - 1)), c = RT1 ? lane : (lane >> a.LRT);
-    const int tile = blockIdx.x, rg = tile * a.RT + r;
-    const bool live = rg < a.R_real;
+    // One window of a mixed-tile schedule: the tile and its first step come from the per-CTA table in the parameters (see
+    // LowdegArgs), re-read where needed instead of being held: this kernel has no register to spare (64 at 1024 threads).
+    auto tile_now = [&]() -> int { return WIN ? a.tab_tile[blockIdx.x] : (int)blockIdx.x; };
+    auto end_step = [&]() -> int { return WIN ? a.tab_step[blockIdx.x] + a.window_steps : a.step_end; };
+    const int sb = WIN ? a.tab_step[blockIdx.x] : a.step_begin;
+    const bool live = tile_now() * a.RT + r < a.R_real;
     const unsigned char *cs_lane = smem_raw + r * 8;                 // + slot byte offset
     const int WC = a.W * a.C;
     const int pos0 = warp * a.C + c;                                 // position of item 0; item t: + t * WC
@@ -122,15 +131,15 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const uint32_t i = 4u * q + k;
-            phi[t][k] = (q < (uint32_t)a.Q && i < (uint32_t)a.n && live) ? (float)a.io[(size_t)rg * a.n + i] : 0.0f;
+            phi[t][k] = (q < (uint32_t)a.Q && i < (uint32_t)a.n && live) ? (float)a.io[(size_t)(tile_now() * a.RT + r) * a.n + i] : 0.0f;
         }
     }
-    const uint64_t seed = a.seeds[rg];
+    const uint64_t seed = a.seeds[tile_now() * a.RT + r];
     const uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     for (int i = tid; i < OSCB_LD_PADS * a.RT; i += blockDim.x)
         reinterpret_cast<float2 *>(smem_raw + (size_t)4 * kbytes)[i] = make_float2(0.0f, 0.0f);
     if (tid < a.RT) {
-        best_s[tid] = a.best_obj[tile * a.RT + tid];
+        best_s[tid] = a.best_obj[tile_now() * a.RT + tid];
         improved_s[tid] = 0;
         cnt[tid] = 0;
     }
@@ -166,13 +175,13 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
     const int W4C = a.W * 4 * a.C;
 
     // what the state now in shared memory still owes: a cadence score, or a trace sample (column >= 0)
-    bool pending = true;
+    bool pending = WIN ? sb == a.step_begin : true;
     int pending_col = 0;                 // the t = 0 sample (dynamics.py:385)
     int pending_label = -1;
     int sample_cur = 0;
-    while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < a.step_begin) ++sample_cur;
+    while (sample_cur < a.n_sample_steps && a.sample_steps[sample_cur] < sb) ++sample_cur;
     int next_sample = sample_cur < a.n_sample_steps ? a.sample_steps[sample_cur] : -1;
-    int cmod = a.cadence > 0 ? a.step_begin % a.cadence : 1;
+    int cmod = a.cadence > 0 ? sb % a.cadence : 1;
 
     // ---- pass A ------------------------------------------------------------------------------------
     // MODE 0: update only; 1: + read-out count; 2: + read-out count + energy; 3: count + energy, no update
@@ -276,7 +285,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if (!(phi[t][k] == phi[t][k]) && quad(t) < (uint32_t)a.Q)
-                        flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)rg, 4u * quad(t) + k);
+                        flag_nonfinite(a.nonfinite, (uint64_t)step, (uint32_t)(tile_now() * a.RT + r), 4u * quad(t) + k);
         }
         if (MODE >= 1) {
             // read-out of the state that was in shared memory during this pass
@@ -296,7 +305,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
                 const double b = best_s[tid];
                 const bool better = a.maximize ? (obj > b) : (obj < b);       // strict: dynamics.py:370-375
                 improved_s[tid] = better ? 1 : 0;
-                const int gi = tile * a.RT + tid;
+                const int gi = tile_now() * a.RT + tid;
                 if (better) {
                     best_s[tid] = obj;
                     if (a.use_target && a.first_hit[gi] < 0 && (a.maximize ? (obj >= a.target) : (obj <= a.target)))
@@ -323,7 +332,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
                             const uint32_t st = NMODE == 2 ? (bits >> 31) : ((bits & 7u) >> 1);
                             packed |= st << (8 * k);
                         }
-                        *reinterpret_cast<uint32_t *>(a.best_states + (size_t)rg * a.n4 + 4u * q) = packed;
+                        *reinterpret_cast<uint32_t *>(a.best_states + (size_t)(tile_now() * a.RT + r) * a.n4 + 4u * q) = packed;
                     }
                 }
             }
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
 
     // ---- time loop ---------------------------------------------------------------------------------
 #pragma unroll 1
-    for (int step = a.step_begin; step < a.step_end; ++step) {
+    for (int step = sb; step < end_step(); ++step) {
         const float hks = __ldg(a.hks_table + (step - a.step_begin));
         if (!pending) {
             pass_a(M0{}, step, hks);
@@ -364,9 +373,9 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
             pending_label = step;
         }
     }
-    if (pending) pass_a(M3{}, a.step_end, 0.0f);
+    if (pending) pass_a(M3{}, end_step(), 0.0f);
 
-    if (tid < a.RT) a.best_obj[tile * a.RT + tid] = best_s[tid];
+    if (tid < a.RT) a.best_obj[tile_now() * a.RT + tid] = best_s[tid];
     if (live) {
 #pragma unroll
         for (int t = 0; t < QPT; ++t) {
@@ -374,7 +383,7 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const uint32_t i = 4u * q + k;
-                if (q < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)rg * a.n + i] = (double)phi[t][k];
+                if (q < (uint32_t)a.Q && i < (uint32_t)a.n) a.io[(size_t)(tile_now() * a.RT + r) * a.n + i] = (double)phi[t][k];
             }
         }
     }
@@ -400,8 +409,8 @@ __global__ void __launch_bounds__(lowdeg_pair_max_threads(QPT), 1) k_lowdeg_pair
     const int LPS = a.RT >> 1;                                       // lanes per slot
     const int q = lane & (LPS - 1), c = lane >> (a.LRT - 1);
     const int r0 = 2 * q;
-    const int tile = a.tile_map ? __ldg(a.tile_map + blockIdx.x) : (int)blockIdx.x, rg0 = tile * a.RT + r0;
-    const int sb = a.tile_map ? __ldg(a.tile_step + blockIdx.x) : a.step_begin, se = a.tile_map ? sb + a.window_steps : a.step_end;
+    const int tile = a.use_tab ? a.tab_tile[blockIdx.x] : (int)blockIdx.x, rg0 = tile * a.RT + r0;
+    const int sb = a.use_tab ? a.tab_step[blockIdx.x] : a.step_begin, se = a.use_tab ? sb + a.window_steps : a.step_end;
     const bool live[2] = {rg0 < a.R_real, rg0 + 1 < a.R_real};
     const unsigned char *cs_lane = smem_raw + r0 * 8;                // + slot byte offset: the pairs of replicas r0, r0 + 1
     const int WC = a.W * a.C;

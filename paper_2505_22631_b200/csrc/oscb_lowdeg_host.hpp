@@ -473,13 +473,19 @@ struct MixedTiles {
     int64_t steps8 = 0, steps4 = 0;
 };
 
-static bool plan_mixed_tiles(oscb_graph *g, const oscb_run_params *p, const LowdegShape &s8, int64_t R, int64_t steps, MixedTiles *m)
+// (k_lowdeg, one replica per lane, takes part too: flat200 x 4096 is 128 tiles of 32 replicas -> 108 tiles of 32 and 40 of 16.
+// The field names keep the numbers of the two-replica case: "8" = the big tile, "4" = the half-size one, octet = a group of
+// one big tile's replicas.)
+static bool plan_mixed_tiles(oscb_graph *g, const oscb_run_params *p, const LowdegShape &s8, int nmode, int64_t R, int64_t steps, MixedTiles *m)
 {
     if (const char *e = getenv("OSCB_LOWDEG_MIXED")) { if (atoi(e) == 0) return false; }
-    if (s8.rpl != 2 || s8.RT != 8 || !g->unit_weights || R % 8 != 0 || p->replicas_per_cta > 0) return false;
-    const int64_t sms = g->sm_count, octets = R / 8;
-    if (octets >= sms || R < 4 * sms) return false;                 // one tile of 8 per SM fills the GPU / tiles of 4 alone do
-    const int64_t F = sms - octets;                                 // a = octets - F tiles of 8, b = 2 F tiles of 4: a + b = sms
+    if (p->replicas_per_cta > 0 || getenv("OSCB_LOWDEG_RT") || getenv("OSCB_LOWDEG_QPT")) return false;     // pinned shapes run as they are
+    const int B = s8.RT;
+    if (s8.rpl == 2 ? (B != 8 || !g->unit_weights) : (B < 4)) return false;
+    if (R % B != 0) return false;
+    const int64_t sms = g->sm_count, octets = R / B;
+    if (octets >= sms || R < (B / 2) * sms) return false;           // one big tile per SM fills the GPU / half-size tiles alone do
+    const int64_t F = sms - octets;                                 // a = octets - F big tiles, b = 2 F half-size ones: a + b = sms
     if (F < 1 || octets - F < 1) return false;
     int64_t gg = octets, x = F;
     while (x) { const int64_t t = gg % x; gg = x; x = t; }
@@ -487,24 +493,34 @@ static bool plan_mixed_tiles(oscb_graph *g, const oscb_run_params *p, const Lowd
     int64_t min_window = 256;
     if (const char *e = getenv("OSCB_LOWDEG_MIXED_MIN_WINDOW")) min_window = std::max<long long>(1, atoll(e));     // (tests)
     if (windows > 64 || steps < windows * min_window) return false;
-    // the 4-replica tile shape: 16 quads per warp, slot stream in shared memory like the 8-replica one
+    // the half-size tile: twice the quads per warp; two replicas per lane: 16 warps of two items, slot stream in shared memory
     LowdegShape s4;
-    const int C = 16, rows = (s8.Q + C - 1) / C;
+    const int C = 2 * s8.C, rows = (s8.Q + C - 1) / C;
     bool found = false;
-    for (int QPT : {2, 4, 5}) {
+    const int qpt2[] = {2, 4, 5}, qpt1[] = {std::max(1, s8.QPT / 2), s8.QPT, 1, 2, 4, 5, 7, 10};
+    const int *cand = s8.rpl == 2 ? qpt2 : qpt1;
+    const int n_cand = s8.rpl == 2 ? 3 : 8;
+    for (int ci = 0; ci < n_cand && !found; ++ci) {
+        const int QPT = cand[ci];
+        if (std::find(std::begin(kLowdegQpt), std::end(kLowdegQpt), QPT) == std::end(kLowdegQpt)) continue;
         const int W = (rows + QPT - 1) / QPT;
-        if (W < 4 || W > lowdeg_pair_max_threads(QPT) / 32) continue;
-        s4.RT = 4; s4.LRT = 2; s4.C = C; s4.W = W; s4.QPT = QPT; s4.Q = s8.Q; s4.Qp = W * QPT * C; s4.uniform = false; s4.rpl = 2;
+        const int maxW = (s8.rpl == 2 ? lowdeg_pair_max_threads(QPT) : lowdeg_max_threads(QPT)) / 32;
+        if (W < (s8.rpl == 2 ? 4 : 1) || W > maxW) continue;
+        s4 = s8;
+        s4.RT = B / 2; s4.LRT = s8.LRT - 1; s4.C = C; s4.W = W; s4.QPT = QPT; s4.Qp = W * QPT * C;
         s4.smem = lowdeg_smem_bytes(s4, nullptr, nullptr, nullptr);
-        if (s4.smem > (size_t)g->smem_optin || (size_t)4 * s4.Qp + OSCB_LD_PADS > 65536) continue;
-        auto plan4 = get_lowdeg_plan(g, s4, 2);
-        if (s4.smem + ((plan4->n_ids * sizeof(uint2) + 15) & ~(size_t)15) > (size_t)g->smem_optin) continue;
+        if (s4.smem > (size_t)g->smem_optin) continue;
+        if (s8.rpl == 2) {
+            if ((size_t)4 * s4.Qp + OSCB_LD_PADS > 65536) continue;
+            auto plan4 = get_lowdeg_plan(g, s4, nmode);
+            if (s4.smem + ((plan4->n_ids * sizeof(uint2) + 15) & ~(size_t)15) > (size_t)g->smem_optin) continue;
+        }
         found = true;
-        break;
     }
     if (!found) return false;
-    // steps of a window in the two lanes: steps4 / steps8 ~ the measured ratio of the step times (G22 shape: 16.7 / 9.2 us)
-    double ratio = 1.8;
+    // steps of a window in the two lanes: steps4 / steps8 ~ the measured ratio of the step times (G22 shape, tiles of 8 and 4:
+    // 16.7 / 9.2 us; flat200, tiles of 32 and 16: 4.29 / 2.54 us)
+    double ratio = s8.rpl == 2 ? 1.8 : 1.7;
     if (const char *e = getenv("OSCB_LOWDEG_MIXED_RATIO")) ratio = std::max(1.0, atof(e));
     const int64_t slow = windows - turns;
     int64_t w0 = (int64_t)std::llround((double)steps / ((double)slow + (double)turns * ratio));
@@ -525,20 +541,21 @@ bool lowdeg_applies(oscb_graph *g, const oscb_run_params *p, int64_t R, bool for
     return forced && choose_lowdeg_shape(g, p, R, true, &s);
 }
 
-template <int NMODE, bool UNIFORM, bool RT1>
-static void launch_lowdeg(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles)
+template <int NMODE, bool UNIFORM, bool RT1, bool WIN = false>
+static void launch_lowdeg(oscb_graph *g, const LowdegArgs &a, const LowdegShape &s, int tiles, cudaStream_t stream = nullptr, size_t smem_request = 0)
 {
+    const size_t smem = std::max(s.smem, smem_request);
     auto go = [&](auto kernel) {
-        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem));
-        kernel<<<tiles, s.W * 32, s.smem, g->stream>>>(a);
+        OSCB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kernel<<<tiles, s.W * 32, smem, stream ? stream : g->stream>>>(a);
     };
     switch (s.QPT) {
-    case 1: go(k_lowdeg<NMODE, 1, UNIFORM, RT1>); break;
-    case 2: go(k_lowdeg<NMODE, 2, UNIFORM, RT1>); break;
-    case 4: go(k_lowdeg<NMODE, 4, UNIFORM, RT1>); break;
-    case 5: go(k_lowdeg<NMODE, 5, UNIFORM, RT1>); break;
-    case 7: go(k_lowdeg<NMODE, 7, UNIFORM, RT1>); break;
-    case 10: go(k_lowdeg<NMODE, 10, UNIFORM, RT1>); break;
+    case 1: go(k_lowdeg<NMODE, 1, UNIFORM, RT1, WIN>); break;
+    case 2: go(k_lowdeg<NMODE, 2, UNIFORM, RT1, WIN>); break;
+    case 4: go(k_lowdeg<NMODE, 4, UNIFORM, RT1, WIN>); break;
+    case 5: go(k_lowdeg<NMODE, 5, UNIFORM, RT1, WIN>); break;
+    case 7: go(k_lowdeg<NMODE, 7, UNIFORM, RT1, WIN>); break;
+    case 10: go(k_lowdeg<NMODE, 10, UNIFORM, RT1, WIN>); break;
     default: OSCB_REQUIRE(false, "internal: no lowdeg instantiation for %d items per thread", s.QPT);
     }
 }
@@ -637,74 +654,83 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
     };
     int launches = 1;
     MixedTiles mix;
-    if (sh.rpl == 2 && plan_mixed_tiles(g, p, sh, R, steps, &mix)) {
-        // 8a + 4b = R replicas on a + b = all SMs (see plan_mixed_tiles): every window launches the a 8-replica tiles and the b
-        // 4-replica tiles side by side on two streams; a window ends when both have.
+    if (plan_mixed_tiles(g, p, sh, nmode, R, steps, &mix)) {
+        // 8a + 4b = R replicas on a + b = all SMs (see plan_mixed_tiles): every window launches the a big tiles and the b
+        // half-size tiles side by side on two streams; a window ends when both have.
         auto plan4 = get_lowdeg_plan(g, mix.s4, nmode);
         LowdegArgs a4 = a;
         a4.Qp = mix.s4.Qp; a4.RT = mix.s4.RT; a4.LRT = mix.s4.LRT; a4.C = mix.s4.C; a4.W = mix.s4.W;
         lowdeg_smem_bytes(mix.s4, &a4.off_cnt, &a4.off_part, &a4.off_misc);
         a4.quad_of = plan4->quad_of.p; a4.soff = plan4->soff.p; a4.sidx = plan4->sidx.p; a4.swt = plan4->swt.p;
         a4.warp_start = plan4->warp_start.p; a4.row_groups = plan4->row_groups.p;
-        const size_t ids8 = (plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15, ids4 = (plan4->n_ids * sizeof(uint2) + 15) & ~(size_t)15;
-        a.off_ids = (uint32_t)sh.smem; a.n_ids = (uint32_t)plan->n_ids;
-        a4.off_ids = (uint32_t)mix.s4.smem; a4.n_ids = (uint32_t)plan4->n_ids;
-        const size_t smem8 = sh.smem + ids8, smem4 = mix.s4.smem + ids4;
-        launched_smem = smem8;
-        // per window: [tiles of 8: map, first step][tiles of 4: map, first step]
-        const int n8 = mix.tiles8, n4t = mix.tiles4, per = 2 * (n8 + n4t);
-        std::vector<int> h_map((size_t)mix.windows * per);
-        std::vector<int64_t> done(R / 8, 0);
-        for (int j = 0; j < mix.windows; ++j) {
-            int *m8 = &h_map[(size_t)j * per], *s8 = m8 + n8, *m4 = s8 + n8, *s4 = m4 + n4t;
-            std::vector<char> fast(R / 8, 0);
-            for (int i = 0; i < mix.fast_octets; ++i) fast[((int64_t)j * mix.fast_octets + i) % (R / 8)] = 1;
-            int c8 = 0, c4 = 0;
-            for (int o = 0; o < R / 8; ++o) {
-                const int at = (int)(p->first_step + done[o]);
-                if (fast[o]) {
-                    m4[c4] = 2 * o; s4[c4++] = at;
-                    m4[c4] = 2 * o + 1; s4[c4++] = at;
-                    done[o] += mix.steps4;
-                } else {
-                    m8[c8] = o; s8[c8++] = at;
-                    done[o] += mix.steps8;
-                }
-            }
-            OSCB_REQUIRE(c8 == n8 && c4 == n4t, "internal: mixed-tile window %d deals %d + %d tiles", j, c8, c4);
+        size_t smem8, smem4;
+        if (sh.rpl == 2) {
+            const size_t ids8 = (plan->n_ids * sizeof(uint2) + 15) & ~(size_t)15, ids4 = (plan4->n_ids * sizeof(uint2) + 15) & ~(size_t)15;
+            a.off_ids = (uint32_t)sh.smem; a.n_ids = (uint32_t)plan->n_ids;
+            a4.off_ids = (uint32_t)mix.s4.smem; a4.n_ids = (uint32_t)plan4->n_ids;
+            smem8 = sh.smem + ids8; smem4 = mix.s4.smem + ids4;
+        } else {
+            // small tiles: ask for more than half an SM's shared memory so that the tiles land one per SM
+            smem8 = std::max(sh.smem, (size_t)g->smem_optin / 2 + 2048);
+            smem4 = std::max(mix.s4.smem, (size_t)g->smem_optin / 2 + 2048);
         }
-        for (int o = 0; o < R / 8; ++o) OSCB_REQUIRE(done[o] == steps, "internal: mixed-tile schedule ends at step %lld", (long long)done[o]);
-        DevBuf<int> d_map(h_map.size());
-        d_map.upload(h_map.data(), h_map.size(), s);
-        OSCB_CUDA(cudaStreamSynchronize(s));
+        launched_smem = smem8;
+        auto launch_tiles = [&](const LowdegArgs &aa, const LowdegShape &ss, int grid, size_t smem, cudaStream_t st) {
+            if (ss.rpl == 2) launch_lowdeg_pair<true, true>(g, aa, ss, grid, smem, st);
+            else if (nmode == 2 && ss.uniform) launch_lowdeg<2, true, false, true>(g, aa, ss, grid, st, smem);
+            else if (nmode == 2) launch_lowdeg<2, false, false, true>(g, aa, ss, grid, st, smem);
+            else if (ss.uniform) launch_lowdeg<3, true, false, true>(g, aa, ss, grid, st, smem);
+            else launch_lowdeg<3, false, false, true>(g, aa, ss, grid, st, smem);
+        };
+        const int B = sh.RT;
+        // per window: the tiles of the two grids and the step each starts from (in the kernel parameters: LowdegArgs)
+        const int n8 = mix.tiles8, n4t = mix.tiles4;
+        OSCB_REQUIRE(n8 <= OSCB_LD_TAB && n4t <= OSCB_LD_TAB, "internal: mixed-tile grids of %d / %d CTAs", n8, n4t);
+        std::vector<int64_t> done(R / B, 0);
         cudaStream_t s2;
         OSCB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
         std::vector<cudaEvent_t> e8(mix.windows), e4(mix.windows);
         for (auto &e : e8) OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         for (auto &e : e4) OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        OSCB_CUDA(cudaEventRecord(ev0, s));                 // (again: the schedule upload is not part of the integration)
         cudaEvent_t fork;
         OSCB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
         OSCB_CUDA(cudaEventRecord(fork, s));
         OSCB_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+        a.use_tab = a4.use_tab = 1;
         a.window_steps = (int)mix.steps8;
         a4.window_steps = (int)mix.steps4;
+        std::vector<char> fast(R / B);
         for (int j = 0; j < mix.windows; ++j) {
-            const int *base = d_map.p + (size_t)j * per;
-            a.tile_map = base; a.tile_step = base + n8;
-            a4.tile_map = base + 2 * n8; a4.tile_step = base + 2 * n8 + n4t;
+            std::fill(fast.begin(), fast.end(), 0);
+            for (int i = 0; i < mix.fast_octets; ++i) fast[((int64_t)j * mix.fast_octets + i) % (R / B)] = 1;
+            int c8 = 0, c4 = 0;
+            for (int o = 0; o < R / B; ++o) {
+                const int at = (int)(p->first_step + done[o]);
+                if (fast[o]) {
+                    OSCB_REQUIRE(c4 + 2 <= n4t, "internal: mixed-tile window %d deals too many small tiles", j);
+                    a4.tab_tile[c4] = 2 * o; a4.tab_step[c4++] = at;
+                    a4.tab_tile[c4] = 2 * o + 1; a4.tab_step[c4++] = at;
+                    done[o] += mix.steps4;
+                } else {
+                    OSCB_REQUIRE(c8 < n8, "internal: mixed-tile window %d deals too many big tiles", j);
+                    a.tab_tile[c8] = o; a.tab_step[c8++] = at;
+                    done[o] += mix.steps8;
+                }
+            }
+            OSCB_REQUIRE(c8 == n8 && c4 == n4t, "internal: mixed-tile window %d deals %d + %d tiles", j, c8, c4);
             if (j > 0) {
                 OSCB_CUDA(cudaStreamWaitEvent(s, e4[j - 1], 0));
                 OSCB_CUDA(cudaStreamWaitEvent(s2, e8[j - 1], 0));
             }
-            launch_lowdeg_pair<true, true>(g, a, sh, n8, smem8, s);
-            launch_lowdeg_pair<true, true>(g, a4, mix.s4, n4t, smem4, s2);
+            launch_tiles(a, sh, n8, smem8, s);
+            launch_tiles(a4, mix.s4, n4t, smem4, s2);
             OSCB_CUDA(cudaEventRecord(e8[j], s));
             OSCB_CUDA(cudaEventRecord(e4[j], s2));
         }
+        for (int o = 0; o < R / B; ++o) OSCB_REQUIRE(done[o] == steps, "internal: mixed-tile schedule ends at step %lld", (long long)done[o]);
         OSCB_CUDA(cudaStreamWaitEvent(s, e4[mix.windows - 1], 0));
         OSCB_CUDA(cudaEventRecord(ev1, s));
-        OSCB_CUDA(cudaStreamSynchronize(s));                // the schedule, the events and the second stream go out of scope here
+        OSCB_CUDA(cudaStreamSynchronize(s));                // the events and the second stream go out of scope here
         for (auto &e : e8) cudaEventDestroy(e);
         for (auto &e : e4) cudaEventDestroy(e);
         cudaEventDestroy(fork);

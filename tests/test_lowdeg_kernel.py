@@ -315,6 +315,45 @@ def test_mixed_tile_schedule_is_the_same_run(pkg, oracle, monkeypatch):
 
 
 @gpu
+def test_mixed_tile_schedule_one_replica_per_lane(pkg, oracle, monkeypatch):
+    """The same schedule for k_lowdeg: flat200 x 4096 is 128 tiles of 32 replicas -> windows of 108 tiles of 32 and 40 of 16
+    (N = 3 colouring).  Forced to windows of a few steps: the noise-free run follows the oracle, read-out and traces included,
+    and stays within float32 rounding of the unbroken launch, noise on or off (a step that also reads the previous state out
+    is a separately compiled variant of the update, and a window boundary changes which steps those are)."""
+    import bench
+    _, J, _, kind, R = bench.load_workload("flat200x4096")
+    steps = 96
+    params = pkg.SolverParams.tuned_for(J.n, 3, seed=9, kn=0.0)
+    seeds = [params.seed + r for r in range(R)]
+    stride = steps * params.h / 4.5
+    monkeypatch.setenv("OSCB_LOWDEG_MIXED_MIN_WINDOW", "1")
+    got = pkg.run_batch(J, params, kind, seeds, steps=steps, trace_stride=stride)
+    assert got.kernel == "lowdeg" and got.kernel_launches == 64 and got.steps == steps
+    sub = list(range(0, R, 97))
+    want = oracle.simulate(J.indptr, J.indices, J.data, K=params.K, ks_max=params.ks_max, ks_period=params.ks_period, kn=0.0,
+                           h=params.h, t_stop=steps * params.h, n_states=3, seeds=[seeds[r] for r in sub], objective=kind,
+                           trace_stride=stride, threads=oracle.max_threads())
+    assert circ_dist_rad(got.final_phases[sub], want.final_phases).max() <= 1e-4
+    assert np.array_equal(_objective(J, got.best_states, kind), got.best_objective)
+    assert np.all(np.diff(got.best_trace, axis=1) <= 0)
+    assert np.abs(got.best_objective[sub] - want.best_objective).max() <= 2.0
+    monkeypatch.setenv("OSCB_LOWDEG_MIXED", "0")
+    solo = pkg.run_batch(J, params, kind, seeds, steps=steps, trace_stride=stride)
+    assert solo.kernel_launches == 1
+    d = circ_dist_rad(got.final_phases, solo.final_phases)
+    assert d.max() <= 2e-4 and np.quantile(d, 0.999) <= 1e-5          # (measured: 4e-5 / 2e-6 rad after 96 steps)
+    assert np.abs(got.best_objective - solo.best_objective).max() <= 2.0 and np.array_equal(got.trace_t, solo.trace_t)
+    noisy = pkg.SolverParams.tuned_for(J.n, 3, seed=9)
+    b = pkg.run_batch(J, noisy, kind, seeds, steps=steps)
+    monkeypatch.delenv("OSCB_LOWDEG_MIXED")
+    a = pkg.run_batch(J, noisy, kind, seeds, steps=steps)
+    assert a.kernel_launches == 64 and b.kernel_launches == 1
+    d = circ_dist_rad(a.final_phases, b.final_phases)
+    assert d.max() <= 1e-3 and np.quantile(d, 0.999) <= 2e-5
+    assert np.array_equal(_objective(J, a.best_states, kind), a.best_objective)
+
+
+@gpu
 @pytest.mark.parametrize("N,kind", [(2, "maxcut"), (3, "coloring")])
 def test_noise_on_distribution_matches_the_oracle(pkg, oracle, N, kind):
     """Noise ON (device Philox vs numpy's stream replayed by the oracle): best objectives over 128 seeds agree in

@@ -44,6 +44,14 @@ if "lowdeg" in which:
     Jc = pkg.CouplingMatrix.from_edges(203, (uc, vc, wc))
     b = pkg.run_batch(Jc, pkg.SolverParams.tuned_for(203, 3, seed=0, t_stop=0.4), "coloring", list(range(37)), kernel="lowdeg")
     print("lowdeg looped N=3", b.kernel, b.replicas_per_cta, b.best_objective.min())
+if "lowdeg" in which:
+    # the mixed-tile schedule of the one-replica-per-lane kernel (flat200 x 4096: tiles of 32 and of 16), windows of 3 steps
+    import os, bench
+    os.environ["OSCB_LOWDEG_MIXED_MIN_WINDOW"] = "1"
+    _, Jf, pf, kindf, Rf = bench.load_workload("flat200x4096")
+    b = pkg.run_batch(Jf, pf, kindf, list(range(Rf)), steps=96, want_phases=False)
+    print("lowdeg mixed-tile schedule N=3", b.kernel, b.kernel_launches, b.best_objective.min())
+    del os.environ["OSCB_LOWDEG_MIXED_MIN_WINDOW"]
 if "lowdeg-pair" in which:
     # k_lowdeg_pair pinned: weighted and unit couplings (slot stream in shared memory), and the headline route (G22 shape,
     # enough 8-replica tiles to fill the GPU) for a few steps
