@@ -1,6 +1,8 @@
-"""k_lowdeg (csrc/oscb_lowdeg.cuh), the persistent float32 kernel for low-degree graphs (G81 shape, flat200):
-its stream compiler on the CPU, and on the GPU its trajectories against the oracle, its read-out against the
-float64 threshold rule, the result contract, determinism and the noise-on distribution."""
+"""k_lowdeg and k_lowdeg_pair (csrc/oscb_lowdeg.cuh), the persistent float32 kernels that keep the phases in registers --
+k_lowdeg for low-degree graphs (G81 shape, flat200), k_lowdeg_pair (two replicas per lane) for N = 2 max-cut at any degree
+(the G22 headline): their stream compiler on the CPU, and on the GPU their trajectories against the oracle, the read-out
+against the float64 threshold rule, the result contract, determinism, the noise contract, the noise-on distribution, the
+kernel chooser, and the mixed-tile schedule that keeps all SMs busy."""
 import ctypes as C
 
 import numpy as np
