@@ -52,11 +52,13 @@ struct LowdegArgs {
     const uint2 *sidx;              // k_lowdeg_pair: the same groups as 4 x u16 SLOT numbers
     const uint32_t *row_groups;     // k_lowdeg_pair: [W][QPT] group counts of an item's four rows in visiting order, a byte each
     // one window of a mixed-tile schedule (use_tab = 0: CTA b is tile b and runs [step_begin, step_end)): CTA b integrates tile
-    // tab_tile[b] (of RT replicas) from step tab_step[b] on for window_steps steps (hks_table stays indexed from step_begin).
-    // The table travels in the kernel parameters: a constant-bank read with a uniform index keeps the step counter and all
-    // that hangs on it (Philox counter, schedule look-up, cadence) on the uniform datapath, as in the unbroken launch.
-    int use_tab, window_steps;
-    int tab_tile[OSCB_LD_TAB], tab_step[OSCB_LD_TAB];
+    // tab_tile[b] (of RT replicas) over [win_begin, win_begin + window_steps) (hks_table stays indexed from step_begin).  All
+    // CTAs of a launch share the window -- tiles with another history get a launch of their own -- so the step counter and
+    // all that hangs on it (Philox counter, schedule look-up, cadence) stay on the uniform datapath as in the unbroken launch
+    // (with a per-CTA first step k_lowdeg needed 63 registers instead of 56 and lost 6 %).  The table travels in the
+    // kernel parameters.
+    int use_tab, win_begin, window_steps;
+    int tab_tile[OSCB_LD_TAB];
     const float4 *swt;              // N = 2: their couplings
     const int *warp_start;          // looped streams: first group row of each warp
     const float *hks_table;         // [steps + 1]  h ks(step) (x2 for N = 2), float64 on the host
@@ -104,8 +106,8 @@ __global__ void __launch_bounds__(lowdeg_max_threads(QPT), 1) k_lowdeg(const Low
     // One window of a mixed-tile schedule: the tile and its first step come from the per-CTA table in the parameters (see
     // LowdegArgs), re-read where needed instead of being held: this kernel has no register to spare (64 at 1024 threads).
     auto tile_now = [&]() -> int { return WIN ? a.tab_tile[blockIdx.x] : (int)blockIdx.x; };
-    auto end_step = [&]() -> int { return WIN ? a.tab_step[blockIdx.x] + a.window_steps : a.step_end; };
-    const int sb = WIN ? a.tab_step[blockIdx.x] : a.step_begin;
+    auto end_step = [&]() -> int { return WIN ? a.win_begin + a.window_steps : a.step_end; };
+    const int sb = WIN ? a.win_begin : a.step_begin;
     const bool live = tile_now() * a.RT + r < a.R_real;
     const unsigned char *cs_lane = smem_raw + r * 8;                 // + slot byte offset
     const int WC = a.W * a.C;
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(lowdeg_pair_max_threads(QPT), 1) k_lowdeg_pair
     const int q = lane & (LPS - 1), c = lane >> (a.LRT - 1);
     const int r0 = 2 * q;
     const int tile = a.use_tab ? a.tab_tile[blockIdx.x] : (int)blockIdx.x, rg0 = tile * a.RT + r0;
-    const int sb = a.use_tab ? a.tab_step[blockIdx.x] : a.step_begin, se = a.use_tab ? sb + a.window_steps : a.step_end;
+    const int sb = a.use_tab ? a.win_begin : a.step_begin, se = a.use_tab ? sb + a.window_steps : a.step_end;
     const bool live[2] = {rg0 < a.R_real, rg0 + 1 < a.R_real};
     const unsigned char *cs_lane = smem_raw + r0 * 8;                // + slot byte offset: the pairs of replicas r0, r0 + 1
     const int WC = a.W * a.C;

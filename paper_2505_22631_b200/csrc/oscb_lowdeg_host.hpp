@@ -7,6 +7,7 @@
 #include "oscb_lowdeg.hpp"
 
 #include <algorithm>
+#include <map>
 #include <array>
 #include <cmath>
 #include <limits>
@@ -683,59 +684,68 @@ void run_lowdeg(oscb_graph *g, const oscb_run_params *p, int64_t steps, int64_t 
             else launch_lowdeg<3, false, false, true>(g, aa, ss, grid, st, smem);
         };
         const int B = sh.RT;
-        // per window: the tiles of the two grids and the step each starts from (in the kernel parameters: LowdegArgs)
+        // per window: the tiles of the two lanes, grouped by the step they start from (the rotation leaves at most two
+        // histories per lane) -- one launch per group, all of a window side by side on a pool of streams
         const int n8 = mix.tiles8, n4t = mix.tiles4;
         OSCB_REQUIRE(n8 <= OSCB_LD_TAB && n4t <= OSCB_LD_TAB, "internal: mixed-tile grids of %d / %d CTAs", n8, n4t);
         std::vector<int64_t> done(R / B, 0);
-        cudaStream_t s2;
-        OSCB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-        std::vector<cudaEvent_t> e8(mix.windows), e4(mix.windows);
-        for (auto &e : e8) OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        for (auto &e : e4) OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        cudaEvent_t fork;
-        OSCB_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-        OSCB_CUDA(cudaEventRecord(fork, s));
-        OSCB_CUDA(cudaStreamWaitEvent(s2, fork, 0));
+        std::vector<cudaStream_t> pool(1, s);
+        std::vector<cudaEvent_t> pool_done;
+        auto stream_at = [&](size_t i) {
+            while (pool.size() <= i) {
+                cudaStream_t st;
+                OSCB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+                pool.push_back(st);
+            }
+            while (pool_done.size() <= i) {
+                cudaEvent_t e;
+                OSCB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                pool_done.push_back(e);
+            }
+            return pool[i];
+        };
+        cudaEvent_t window_done;
+        OSCB_CUDA(cudaEventCreateWithFlags(&window_done, cudaEventDisableTiming));
+        OSCB_CUDA(cudaEventRecord(window_done, s));          // (the set-up above, on the run's stream)
         a.use_tab = a4.use_tab = 1;
         a.window_steps = (int)mix.steps8;
         a4.window_steps = (int)mix.steps4;
         std::vector<char> fast(R / B);
+        launches = 0;
         for (int j = 0; j < mix.windows; ++j) {
             std::fill(fast.begin(), fast.end(), 0);
             for (int i = 0; i < mix.fast_octets; ++i) fast[((int64_t)j * mix.fast_octets + i) % (R / B)] = 1;
-            int c8 = 0, c4 = 0;
+            std::map<int, std::vector<int>> big, small;          // first step -> tiles
             for (int o = 0; o < R / B; ++o) {
                 const int at = (int)(p->first_step + done[o]);
-                if (fast[o]) {
-                    OSCB_REQUIRE(c4 + 2 <= n4t, "internal: mixed-tile window %d deals too many small tiles", j);
-                    a4.tab_tile[c4] = 2 * o; a4.tab_step[c4++] = at;
-                    a4.tab_tile[c4] = 2 * o + 1; a4.tab_step[c4++] = at;
-                    done[o] += mix.steps4;
-                } else {
-                    OSCB_REQUIRE(c8 < n8, "internal: mixed-tile window %d deals too many big tiles", j);
-                    a.tab_tile[c8] = o; a.tab_step[c8++] = at;
-                    done[o] += mix.steps8;
+                if (fast[o]) { small[at].push_back(2 * o); small[at].push_back(2 * o + 1); done[o] += mix.steps4; }
+                else { big[at].push_back(o); done[o] += mix.steps8; }
+            }
+            size_t used = 0;
+            auto launch_groups = [&](std::map<int, std::vector<int>> &groups, LowdegArgs &aa, const LowdegShape &ss, size_t smem) {
+                for (auto &kv : groups) {
+                    OSCB_REQUIRE(kv.second.size() <= OSCB_LD_TAB, "internal: mixed-tile group of %zu CTAs", kv.second.size());
+                    aa.win_begin = kv.first;
+                    std::copy(kv.second.begin(), kv.second.end(), aa.tab_tile);
+                    cudaStream_t st = stream_at(used);
+                    if (st != s) OSCB_CUDA(cudaStreamWaitEvent(st, window_done, 0));
+                    launch_tiles(aa, ss, (int)kv.second.size(), smem, st);
+                    OSCB_CUDA(cudaEventRecord(pool_done[used], st));
+                    ++used;
+                    ++launches;
                 }
-            }
-            OSCB_REQUIRE(c8 == n8 && c4 == n4t, "internal: mixed-tile window %d deals %d + %d tiles", j, c8, c4);
-            if (j > 0) {
-                OSCB_CUDA(cudaStreamWaitEvent(s, e4[j - 1], 0));
-                OSCB_CUDA(cudaStreamWaitEvent(s2, e8[j - 1], 0));
-            }
-            launch_tiles(a, sh, n8, smem8, s);
-            launch_tiles(a4, mix.s4, n4t, smem4, s2);
-            OSCB_CUDA(cudaEventRecord(e8[j], s));
-            OSCB_CUDA(cudaEventRecord(e4[j], s2));
+            };
+            launch_groups(big, a, sh, smem8);
+            launch_groups(small, a4, mix.s4, smem4);
+            for (size_t i = 1; i < used; ++i) OSCB_CUDA(cudaStreamWaitEvent(s, pool_done[i], 0));
+            OSCB_CUDA(cudaEventRecord(window_done, s));
         }
         for (int o = 0; o < R / B; ++o) OSCB_REQUIRE(done[o] == steps, "internal: mixed-tile schedule ends at step %lld", (long long)done[o]);
-        OSCB_CUDA(cudaStreamWaitEvent(s, e4[mix.windows - 1], 0));
         OSCB_CUDA(cudaEventRecord(ev1, s));
-        OSCB_CUDA(cudaStreamSynchronize(s));                // the events and the second stream go out of scope here
-        for (auto &e : e8) cudaEventDestroy(e);
-        for (auto &e : e4) cudaEventDestroy(e);
-        cudaEventDestroy(fork);
-        cudaStreamDestroy(s2);
-        launches = 2 * mix.windows;
+        OSCB_CUDA(cudaStreamSynchronize(s));                // the events and the pool go out of scope here
+        for (auto &e : pool_done) cudaEventDestroy(e);
+        cudaEventDestroy(window_done);
+        for (size_t i = 1; i < pool.size(); ++i) cudaStreamDestroy(pool[i]);
     }
     else if (sh.rpl == 2) {
         // the slot stream goes to shared memory when it fits behind the pairs (OSCB_LOWDEG_IDS=0: never)
