@@ -123,6 +123,14 @@ int oscb_device_count(int *count);
  * blocks (cudaFree).  Never needed for correctness. */
 int oscb_pool_trim(void);
 
+/* Symmetric CSR from an edge list, built on the device: the GPU form of CouplingMatrix.from_edges (reference
+ * model.py:151-200).  m entries (i[e], j[e], x[e]), one per unordered pair, HOST buffers; out: indptr [n + 1], indices and data
+ * [*nnz <= 2 m] (caller provides 2 m entries each), rows and the columns of a row ascending, entries with x == 0 dropped -- bit
+ * for bit what the reference's host build returns.  OSCB_EINVAL with the reference's messages, in the reference's order: an
+ * index outside [0, n), a diagonal entry, a pair listed twice (zero-valued entries count).  device_ms (may be NULL): time of
+ * the kernels alone, CUDA events.  n < 2^31. */
+int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64_t *i, const int64_t *j, const double *x,
+                        int64_t *indptr, int64_t *indices, double *data, int64_t *nnz, double *device_ms);
 int oscb_graph_create_csr(int device, int64_t n, const int64_t *indptr, const int64_t *indices,
                           const double *data, oscb_graph **out);
 /* Dense couplings.  Integer couplings |J| <= 127 on 128-row aligned shards also get the tile images of the

@@ -69,6 +69,8 @@ SYMBOLS = {
     "oscb_version": (C.c_int, []),
     "oscb_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "oscb_pool_trim": (C.c_int, []),
+    "oscb_csr_from_edges": (C.c_int, [C.c_int, C.c_int64, C.c_int64, _P, _P, _P, _P, _P, _P, C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_double)]),
     "oscb_graph_create_csr": (C.c_int, [C.c_int, C.c_int64, _P, _P, _P, C.POINTER(_P)]),
     "oscb_graph_create_dense": (C.c_int, [C.c_int, C.c_int64, _P, C.c_int64, C.c_int64, C.POINTER(_P)]),
     "oscb_graph_destroy": (C.c_int, [_P]),

@@ -1,0 +1,393 @@
+// oscb_csr_build.cu -- device-side build of the symmetric CSR from an edge list: the GPU form of
+// CouplingMatrix.from_edges (reference model.py:151-200).  One (i, j, x) entry per unordered pair in, the canonical CSR
+// out (both directions, rows ascending, columns ascending inside a row, entries with x == 0 dropped) -- the same arrays,
+// bit for bit, as the vectorised host build in model.py, with the reference's validation in the reference's order
+// (index range, then self-coupling, then a pair listed twice -- zero-valued entries included, as the reference checks
+// before it filters).
+//
+// Integer / byte work, HBM-bound, no sort of the whole list:
+//   k_csr_count        degree histogram with atomics + range / diagonal / has-zero flags        24 B read per entry
+//   k_csr_scan         exclusive scan of the degrees -> indptr (one CTA; n words, negligible)
+//   k_csr_fill         scatter both directions into the rows in arrival order                   24 B read, 24 B written
+//   k_csr_sort_short   rows of <= 32 entries: a warp per row, rank by counting over shuffles    12 B read, 16 B written per entry
+//   k_csr_sort_long    longer rows, a CTA per row.  Columns of a row are unique, so the position of column c is the number
+//                      of set bits below c in the row's column BITMAP (n bits in shared memory, a popcount prefix per 1024
+//                      columns): O(n / 32 + d) per row, and a bit found set twice is the duplicate pair.  Rows too short to
+//                      pay for clearing the bitmap (or n beyond shared memory) rank by counting, O(d^2 / threads).
+//   k_csr_compact      only when some x == 0: per-row stable compaction to the final arrays
+#include "oscb_host.hpp"
+
+#include <algorithm>
+#include <exception>
+
+namespace oscb {
+
+constexpr uint32_t CSR_ERANGE = 1u, CSR_EDIAG = 2u, CSR_EDUP = 4u, CSR_HASZERO = 8u;
+constexpr int CSR_LONG_THREADS = 512;
+
+__global__ void __launch_bounds__(256) k_csr_count(int64_t m, int64_t n, const int64_t *__restrict__ ei, const int64_t *__restrict__ ej,
+                                                   const double *__restrict__ ex, uint32_t *deg, uint32_t *flags)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
+        const int64_t e = base + threadIdx.x;
+        uint32_t f = 0;
+        if (e < m) {
+            const int64_t a = ei[e], b = ej[e];
+            if (a < 0 || b < 0 || a >= n || b >= n) f |= CSR_ERANGE;
+            else if (a == b) f |= CSR_EDIAG;
+            else {
+                atomicAdd(&deg[a], 1u);
+                atomicAdd(&deg[b], 1u);
+            }
+            if (ex[e] == 0.0) f |= CSR_HASZERO;
+        }
+        f = __reduce_or_sync(0xffffffffu, f);
+        if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+    }
+}
+
+// exclusive scan of cnt[0..n) into out[0..n], out[n] = total.  One CTA of 1024 threads, 4 entries per thread and trip.
+__global__ void __launch_bounds__(1024) k_csr_scan(int64_t n, const uint32_t *__restrict__ cnt, int64_t *__restrict__ out)
+{
+    __shared__ long long warp_tot[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    long long carry = 0;
+    for (int64_t base = 0; base < n; base += 4096) {
+        const int64_t i0 = base + 4 * (int64_t)tid;
+        long long d[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[k] = i0 + k < n ? (long long)cnt[i0 + k] : 0;
+        const long long mine = (d[0] + d[1]) + (d[2] + d[3]);
+        long long incl = mine;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const long long up = __shfl_up_sync(0xffffffffu, incl, off);
+            if (lane >= off) incl += up;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            const long long t = warp_tot[lane];
+            long long s = t;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const long long up = __shfl_up_sync(0xffffffffu, s, off);
+                if (lane >= off) s += up;
+            }
+            warp_tot[lane] = s - t;                       // exclusive prefix of the warps
+        }
+        __syncthreads();
+        long long p = carry + warp_tot[warp] + (incl - mine);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (i0 + k < n) out[i0 + k] = p;
+            p += d[k];
+        }
+        // the CTA's total of this trip: prefix of the last warp + its inclusive sum
+        __shared__ long long trip_total;
+        if (tid == 1023) trip_total = warp_tot[31] + incl;
+        __syncthreads();
+        carry += trip_total;
+        __syncthreads();
+    }
+    if (tid == 0) out[n] = carry;
+}
+
+// both directions of every entry into its rows, in arrival order (the sort kernels put a row in column order).  `deg` counts
+// down to zero: it is the cursor.
+__global__ void __launch_bounds__(256) k_csr_fill(int64_t m, const int64_t *__restrict__ ei, const int64_t *__restrict__ ej,
+                                                  const double *__restrict__ ex, const int64_t *__restrict__ indptr, uint32_t *deg,
+                                                  int32_t *__restrict__ tcols, double *__restrict__ tvals)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
+        const int64_t a = ei[e], b = ej[e];
+        const double v = ex[e];
+        const int64_t pa = indptr[a] + (int64_t)(atomicSub(&deg[a], 1u) - 1u);
+        tcols[pa] = (int32_t)b;
+        tvals[pa] = v;
+        const int64_t pb = indptr[b] + (int64_t)(atomicSub(&deg[b], 1u) - 1u);
+        tcols[pb] = (int32_t)a;
+        tvals[pb] = v;
+    }
+}
+
+// rows of <= 32 entries: one warp per row, a lane per entry, its place = the number of smaller columns in the row (32
+// shuffles).  Longer rows go on a list for k_csr_sort_long.
+__global__ void __launch_bounds__(256) k_csr_sort_short(int64_t n, const int64_t *__restrict__ indptr, const int32_t *__restrict__ tcols,
+                                                        const double *__restrict__ tvals, int64_t *__restrict__ ocols,
+                                                        double *__restrict__ ovals, int32_t *long_rows, uint32_t *n_long, uint32_t *flags)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int64_t lo = indptr[row];
+        const int64_t d = indptr[row + 1] - lo;
+        if (d > 32) {
+            if (lane == 0) long_rows[atomicAdd(n_long, 1u)] = (int32_t)row;
+            continue;
+        }
+        const bool mine = lane < d;
+        const int32_t c = mine ? tcols[lo + lane] : 0x7fffffff;
+        const double v = mine ? tvals[lo + lane] : 0.0;
+        int rank = 0;
+        bool dup = false;
+        for (int l = 0; l < (int)d; ++l) {
+            const int32_t cl = __shfl_sync(0xffffffffu, c, l);
+            rank += cl < c;
+            dup = dup || (cl == c && l != lane);
+        }
+        if (mine) {
+            if (dup) atomicOr(flags, CSR_EDUP);
+            else {
+                ocols[lo + rank] = c;
+                ovals[lo + rank] = v;
+            }
+        }
+    }
+}
+
+// rows of more than 32 entries, one CTA per row (see the header of this file)
+__global__ void __launch_bounds__(CSR_LONG_THREADS) k_csr_sort_long(int64_t n, int bitmap_fits, const int64_t *__restrict__ indptr,
+                                                                    const int32_t *__restrict__ tcols, const double *__restrict__ tvals,
+                                                                    int64_t *__restrict__ ocols, double *__restrict__ ovals,
+                                                                    const int32_t *__restrict__ long_rows, const uint32_t *__restrict__ n_long,
+                                                                    uint32_t *flags)
+{
+    extern __shared__ uint32_t csr_sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t W = (uint32_t)((n + 31) >> 5), CH = (W + 31) >> 5;     // bitmap words; chunks of 32 words
+    uint32_t *bitmap = csr_sm, *cpre = csr_sm + W;
+    const uint32_t count = *n_long;
+    for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+        const int64_t row = long_rows[li];
+        const int64_t lo = indptr[row];
+        const int64_t d = indptr[row + 1] - lo;
+        const int32_t *rc = tcols + lo;
+        const double *rv = tvals + lo;
+        bool dup = false;
+        if (bitmap_fits && d * d > (n >> 3) + 32 * d) {
+            for (uint32_t w = tid; w < W; w += CSR_LONG_THREADS) bitmap[w] = 0u;
+            __syncthreads();
+            for (int64_t e = tid; e < d; e += CSR_LONG_THREADS) {
+                const uint32_t c = (uint32_t)rc[e], bit = 1u << (c & 31);
+                dup = dup || (atomicOr(&bitmap[c >> 5], bit) & bit);
+            }
+            __syncthreads();
+            for (uint32_t ch = warp; ch < CH; ch += CSR_LONG_THREADS / 32) {
+                const uint32_t w = ch * 32 + lane;
+                const uint32_t tot = __reduce_add_sync(0xffffffffu, w < W ? (uint32_t)__popc(bitmap[w]) : 0u);
+                if (lane == 0) cpre[ch] = tot;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                uint32_t carry = 0;
+                for (uint32_t base = 0; base < CH; base += 32) {
+                    const uint32_t t = base + lane < CH ? cpre[base + lane] : 0u;
+                    uint32_t s = t;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const uint32_t up = __shfl_up_sync(0xffffffffu, s, off);
+                        if (lane >= off) s += up;
+                    }
+                    if (base + lane < CH) cpre[base + lane] = carry + s - t;
+                    carry += __shfl_sync(0xffffffffu, s, 31);
+                }
+            }
+            __syncthreads();
+            if (!__syncthreads_or(dup)) {
+                for (int64_t e = tid; e < d; e += CSR_LONG_THREADS) {
+                    const uint32_t c = (uint32_t)rc[e], wd = c >> 5, ch = wd >> 5;
+                    uint32_t rank = cpre[ch];
+                    for (uint32_t w = ch * 32; w < wd; ++w) rank += __popc(bitmap[w]);
+                    rank += __popc(bitmap[wd] & ((1u << (c & 31)) - 1u));
+                    ocols[lo + rank] = (int64_t)c;
+                    ovals[lo + rank] = rv[e];
+                }
+            }
+            __syncthreads();
+        } else {
+            for (int64_t e = tid; e < d; e += CSR_LONG_THREADS) {
+                const int32_t c = rc[e];
+                int64_t rank = 0;
+                bool twice = false;
+                for (int64_t f = 0; f < d; ++f) {
+                    const int32_t cf = rc[f];
+                    rank += cf < c;
+                    twice = twice || (cf == c && f != e);
+                }
+                if (twice) dup = true;
+                else {
+                    ocols[lo + rank] = (int64_t)c;
+                    ovals[lo + rank] = rv[e];
+                }
+            }
+        }
+        if (dup) atomicOr(flags, CSR_EDUP);
+    }
+}
+
+// entries of a row with x != 0 (reference model.py:178: the filter comes after the validation)
+__global__ void __launch_bounds__(256) k_csr_nzcount(int64_t n, const int64_t *__restrict__ indptr, const double *__restrict__ vals, uint32_t *cnt)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int64_t lo = indptr[row], hi = indptr[row + 1];
+        uint32_t c = 0;
+        for (int64_t e = lo + lane; e < hi; e += 32) c += vals[e] != 0.0;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) cnt[row] = c;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_csr_compact(int64_t n, const int64_t *__restrict__ indptr, const int64_t *__restrict__ indptr2,
+                                                     const int64_t *__restrict__ cols, const double *__restrict__ vals,
+                                                     int64_t *__restrict__ ccols, double *__restrict__ cvals)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
+        const int64_t lo = indptr[row], hi = indptr[row + 1];
+        int64_t dst = indptr2[row];
+        for (int64_t base = lo; base < hi; base += 32) {
+            const int64_t e = base + lane;
+            const double v = e < hi ? vals[e] : 0.0;
+            const bool keep = e < hi && v != 0.0;
+            const uint32_t mask = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int64_t p = dst + __popc(mask & ((1u << lane) - 1u));
+                ccols[p] = cols[e];
+                cvals[p] = v;
+            }
+            dst += __popc(mask);
+        }
+    }
+}
+
+namespace {
+// plain cudaMalloc blocks: a one-off build of a large graph should not park gigabytes in the run-time pool
+template <typename T> struct Scratch {
+    T *p = nullptr;
+    explicit Scratch(size_t count) { OSCB_CUDA(cudaMalloc(&p, (count ? count : 1) * sizeof(T))); }
+    Scratch(const Scratch &) = delete;
+    Scratch &operator=(const Scratch &) = delete;
+    ~Scratch() { if (p) cudaFree(p); }
+};
+struct Events {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Events() { OSCB_CUDA(cudaEventCreate(&a)); OSCB_CUDA(cudaEventCreate(&b)); }
+    ~Events() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
+};
+} // namespace
+
+} // namespace oscb
+
+extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64_t *i, const int64_t *j, const double *x,
+                                   int64_t *indptr, int64_t *indices, double *data, int64_t *nnz, double *device_ms)
+{
+    using namespace oscb;
+    try {
+        OSCB_REQUIRE(n >= 1, "n must be >= 1");
+        OSCB_REQUIRE(n < (int64_t)0x7fffffff && m >= 0 && m < ((int64_t)1 << 40), "graph too large for the device CSR build");
+        OSCB_REQUIRE(indptr && nnz && (m == 0 || (i && j && x && indices && data)), "null buffer");
+        int count = 0;
+        OSCB_CUDA(cudaGetDeviceCount(&count));
+        OSCB_REQUIRE(device >= 0 && device < count, "no such CUDA device: %d", device);
+        OSCB_CUDA(cudaSetDevice(device));
+        int sms = 0, smem_optin = 0;
+        OSCB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+        OSCB_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+        cudaStream_t s = nullptr;                      // the legacy default stream: this call is synchronous anyway
+        const size_t E = 2 * (size_t)m;
+
+        Scratch<int64_t> d_i(m), d_j(m), d_indptr(n + 1), d_ocols(E);
+        Scratch<double> d_x(m), d_tvals(E), d_ovals(E);
+        Scratch<int32_t> d_tcols(E), d_long(n);
+        Scratch<uint32_t> d_deg(n), d_misc(2);         // [0] flags, [1] number of long rows
+        if (m) {
+            OSCB_CUDA(cudaMemcpyAsync(d_i.p, i, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            OSCB_CUDA(cudaMemcpyAsync(d_j.p, j, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
+            OSCB_CUDA(cudaMemcpyAsync(d_x.p, x, m * sizeof(double), cudaMemcpyHostToDevice, s));
+        }
+        OSCB_CUDA(cudaMemsetAsync(d_deg.p, 0, n * sizeof(uint32_t), s));
+        OSCB_CUDA(cudaMemsetAsync(d_misc.p, 0, 2 * sizeof(uint32_t), s));
+
+        Events ev;
+        float ms_a = 0.f, ms_b = 0.f;
+        const int grid_e = (int)std::min<int64_t>((m + 255) / 256 + 1, (int64_t)sms * 16);
+        const int grid_r = (int)std::min<int64_t>((n * 32 + 255) / 256 + 1, (int64_t)sms * 16);
+        OSCB_CUDA(cudaEventRecord(ev.a, s));
+        k_csr_count<<<grid_e, 256, 0, s>>>(m, n, d_i.p, d_j.p, d_x.p, d_deg.p, d_misc.p);
+        OSCB_CUDA(cudaGetLastError());
+        OSCB_CUDA(cudaEventRecord(ev.b, s));
+        uint32_t misc[2] = {0, 0};
+        OSCB_CUDA(cudaMemcpyAsync(misc, d_misc.p, sizeof(misc), cudaMemcpyDeviceToHost, s));
+        OSCB_CUDA(cudaStreamSynchronize(s));
+        OSCB_CUDA(cudaEventElapsedTime(&ms_a, ev.a, ev.b));
+        // the reference's order of complaints (model.py:165-176)
+        OSCB_REQUIRE(!(misc[0] & CSR_ERANGE), "coupling index out of range");
+        OSCB_REQUIRE(!(misc[0] & CSR_EDIAG), "diagonal entries must be zero (no self-coupling)");
+        const bool has_zero = (misc[0] & CSR_HASZERO) != 0;
+
+        const size_t words = ((size_t)n + 31) / 32, bitmap_bytes = (words + (words + 31) / 32 + 1) * sizeof(uint32_t);
+        const int bitmap_fits = bitmap_bytes <= (size_t)smem_optin ? 1 : 0;
+        if (bitmap_fits)
+            OSCB_CUDA(cudaFuncSetAttribute(k_csr_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bitmap_bytes));
+        OSCB_CUDA(cudaEventRecord(ev.a, s));
+        k_csr_scan<<<1, 1024, 0, s>>>(n, d_deg.p, d_indptr.p);
+        if (m) {
+            k_csr_fill<<<grid_e, 256, 0, s>>>(m, d_i.p, d_j.p, d_x.p, d_indptr.p, d_deg.p, d_tcols.p, d_tvals.p);
+            k_csr_sort_short<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_tcols.p, d_tvals.p, d_ocols.p, d_ovals.p, d_long.p, d_misc.p + 1,
+                                                    d_misc.p);
+            // few long rows at a time keep many bitmaps' worth of shared memory from idling: a CTA per SM and bitmap
+            const int per_sm = bitmap_fits ? std::max(1, std::min(4, (int)((size_t)smem_optin / std::max<size_t>(bitmap_bytes, 1)))) : 4;
+            k_csr_sort_long<<<sms * per_sm, CSR_LONG_THREADS, bitmap_fits ? bitmap_bytes : 0, s>>>(
+                n, bitmap_fits, d_indptr.p, d_tcols.p, d_tvals.p, d_ocols.p, d_ovals.p, d_long.p, d_misc.p + 1, d_misc.p);
+        }
+        OSCB_CUDA(cudaGetLastError());
+        OSCB_CUDA(cudaEventRecord(ev.b, s));
+        OSCB_CUDA(cudaMemcpyAsync(misc, d_misc.p, sizeof(misc), cudaMemcpyDeviceToHost, s));
+        OSCB_CUDA(cudaStreamSynchronize(s));
+        OSCB_CUDA(cudaEventElapsedTime(&ms_b, ev.a, ev.b));
+        OSCB_REQUIRE(!(misc[0] & CSR_EDUP), "duplicate coupling entry on an unordered pair");
+
+        float ms_c = 0.f;
+        if (!has_zero) {
+            *nnz = (int64_t)E;
+            OSCB_CUDA(cudaMemcpyAsync(indptr, d_indptr.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            if (E) {
+                OSCB_CUDA(cudaMemcpyAsync(indices, d_ocols.p, E * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                OSCB_CUDA(cudaMemcpyAsync(data, d_ovals.p, E * sizeof(double), cudaMemcpyDeviceToHost, s));
+            }
+            OSCB_CUDA(cudaStreamSynchronize(s));
+        } else {
+            Scratch<int64_t> d_indptr2(n + 1), d_ccols(E);
+            Scratch<double> d_cvals(E);
+            OSCB_CUDA(cudaEventRecord(ev.a, s));
+            k_csr_nzcount<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_ovals.p, d_deg.p);
+            k_csr_scan<<<1, 1024, 0, s>>>(n, d_deg.p, d_indptr2.p);
+            k_csr_compact<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_indptr2.p, d_ocols.p, d_ovals.p, d_ccols.p, d_cvals.p);
+            OSCB_CUDA(cudaGetLastError());
+            OSCB_CUDA(cudaEventRecord(ev.b, s));
+            OSCB_CUDA(cudaMemcpyAsync(indptr, d_indptr2.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+            OSCB_CUDA(cudaStreamSynchronize(s));
+            OSCB_CUDA(cudaEventElapsedTime(&ms_c, ev.a, ev.b));
+            const int64_t kept = indptr[n];
+            *nnz = kept;
+            if (kept) {
+                OSCB_CUDA(cudaMemcpyAsync(indices, d_ccols.p, kept * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                OSCB_CUDA(cudaMemcpyAsync(data, d_cvals.p, kept * sizeof(double), cudaMemcpyDeviceToHost, s));
+            }
+            OSCB_CUDA(cudaStreamSynchronize(s));
+        }
+        if (device_ms) *device_ms = (double)ms_a + (double)ms_b + (double)ms_c;
+        return OSCB_OK;
+    } catch (const OscbFail &f) {
+        return f.code;
+    } catch (const std::exception &e) {
+        set_error("oscb_csr_from_edges: %s", e.what());
+        return OSCB_ECUDA;
+    }
+}
