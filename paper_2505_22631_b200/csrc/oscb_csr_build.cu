@@ -7,7 +7,7 @@
 //
 // Integer / byte work, HBM-bound, no sort of the whole list:
 //   k_csr_count        degree histogram with atomics + range / diagonal / has-zero flags        24 B read per entry
-//   k_csr_scan         exclusive scan of the degrees -> indptr (one CTA; n words, negligible)
+//   k_csr_scan         exclusive scan of the degrees -> indptr (block totals | scan of the totals | prefixes; n words)
 //   k_csr_fill         scatter both directions into the rows in arrival order                   24 B read, 24 B written
 //   k_csr_sort_short   rows of <= 32 entries: a warp per row, rank by counting over shuffles    12 B read, 16 B written per entry
 //   k_csr_sort_long    longer rows, a CTA per row.  Columns of a row are unique, so the position of column c is the number
@@ -47,17 +47,58 @@ __global__ void __launch_bounds__(256) k_csr_count(int64_t m, int64_t n, const i
     }
 }
 
-// exclusive scan of cnt[0..n) into out[0..n], out[n] = total.  One CTA of 1024 threads, 4 entries per thread and trip.
-__global__ void __launch_bounds__(1024) k_csr_scan(int64_t n, const uint32_t *__restrict__ cnt, int64_t *__restrict__ out)
+// the same histogram through a shared-memory copy of the counters (n <= CSR_SMEM_COUNTERS): on dense graphs every entry hits
+// one of a few thousand counters and the global atomics queue up in L2 (complete graph on 4096 oscillators: 404 us -> see
+// DESIGN 4d); a CTA counts privately and adds its non-zero counters once.
+constexpr int CSR_SMEM_COUNTERS = 16384;
+__global__ void __launch_bounds__(512) k_csr_count_smem(int64_t m, int64_t n, const int64_t *__restrict__ ei, const int64_t *__restrict__ ej,
+                                                        const double *__restrict__ ex, uint32_t *deg, uint32_t *flags)
+{
+    extern __shared__ uint32_t csr_hist[];
+    for (int k = threadIdx.x; k < (int)n; k += blockDim.x) csr_hist[k] = 0u;
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
+        const int64_t e = base + threadIdx.x;
+        uint32_t f = 0;
+        if (e < m) {
+            const int64_t a = ei[e], b = ej[e];
+            if (a < 0 || b < 0 || a >= n || b >= n) f |= CSR_ERANGE;
+            else if (a == b) f |= CSR_EDIAG;
+            else {
+                atomicAdd(&csr_hist[a], 1u);
+                atomicAdd(&csr_hist[b], 1u);
+            }
+            if (ex[e] == 0.0) f |= CSR_HASZERO;
+        }
+        f = __reduce_or_sync(0xffffffffu, f);
+        if (f && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < (int)n; k += blockDim.x)
+        if (csr_hist[k]) atomicAdd(&deg[k], csr_hist[k]);
+}
+
+// Exclusive scan in three launches of one kernel.  CTA b scans cnt[b * L, (b + 1) * L) in trips of 4096 entries (1024 threads x
+// 4), starting from block_off[b] (0 when NULL); it writes the prefixes to out (skipped when NULL), its own total to tot[b]
+// (skipped when NULL), and the CTA that reaches n writes out[n].  Pass 1: totals of 4096-entry blocks; pass 2: one CTA scans
+// the totals; pass 3: the prefixes.  (One CTA walking the whole array took 0.78 ms at n = 10^6 -- 3.2 us per dependent trip --
+// which was 60 % of the build.)
+template <typename T>
+__global__ void __launch_bounds__(1024) k_csr_scan(int64_t n, int64_t L, const T *__restrict__ cnt, int64_t *__restrict__ out,
+                                                   const int64_t *__restrict__ block_off, unsigned long long *__restrict__ tot)
 {
     __shared__ long long warp_tot[32];
+    __shared__ long long trip_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    long long carry = 0;
-    for (int64_t base = 0; base < n; base += 4096) {
+    const int64_t begin = (int64_t)blockIdx.x * L, end = begin + L < n ? begin + L : n;
+    const long long start = block_off ? (long long)block_off[blockIdx.x] : 0;
+    long long carry = start;
+    for (int64_t base = begin; base < end; base += 4096) {
         const int64_t i0 = base + 4 * (int64_t)tid;
         long long d[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) d[k] = i0 + k < n ? (long long)cnt[i0 + k] : 0;
+        for (int k = 0; k < 4; ++k) d[k] = i0 + k < end ? (long long)cnt[i0 + k] : 0;
         const long long mine = (d[0] + d[1]) + (d[2] + d[3]);
         long long incl = mine;
 #pragma unroll
@@ -79,19 +120,22 @@ __global__ void __launch_bounds__(1024) k_csr_scan(int64_t n, const uint32_t *__
         }
         __syncthreads();
         long long p = carry + warp_tot[warp] + (incl - mine);
+        if (out) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (i0 + k < n) out[i0 + k] = p;
-            p += d[k];
+            for (int k = 0; k < 4; ++k) {
+                if (i0 + k < end) out[i0 + k] = p;
+                p += d[k];
+            }
         }
-        // the CTA's total of this trip: prefix of the last warp + its inclusive sum
-        __shared__ long long trip_total;
-        if (tid == 1023) trip_total = warp_tot[31] + incl;
+        if (tid == 1023) trip_total = warp_tot[31] + incl;     // prefix of the last warp + its inclusive sum
         __syncthreads();
         carry += trip_total;
         __syncthreads();
     }
-    if (tid == 0) out[n] = carry;
+    if (tid == 0) {
+        if (tot) tot[blockIdx.x] = (unsigned long long)(carry - start);
+        if (out && end == n && (begin < n || blockIdx.x == 0)) out[n] = carry;
+    }
 }
 
 // both directions of every entry into its rows, in arrival order (the sort kernels put a row in column order).  `deg` counts
@@ -280,6 +324,18 @@ struct Events {
     Events() { OSCB_CUDA(cudaEventCreate(&a)); OSCB_CUDA(cudaEventCreate(&b)); }
     ~Events() { if (a) cudaEventDestroy(a); if (b) cudaEventDestroy(b); }
 };
+// exclusive scan of cnt[0..n) into out[0..n] (out[n] = total): the three passes of k_csr_scan
+static void launch_scan(int64_t n, const uint32_t *cnt, int64_t *out, unsigned long long *sums, int64_t *offs, cudaStream_t s)
+{
+    const int64_t B = (n + 4095) / 4096;
+    if (B <= 1) {
+        k_csr_scan<uint32_t><<<1, 1024, 0, s>>>(n, 4096, cnt, out, nullptr, nullptr);
+        return;
+    }
+    k_csr_scan<uint32_t><<<(unsigned)B, 1024, 0, s>>>(n, 4096, cnt, nullptr, nullptr, sums);
+    k_csr_scan<unsigned long long><<<1, 1024, 0, s>>>(B, B, sums, offs, nullptr, nullptr);
+    k_csr_scan<uint32_t><<<(unsigned)B, 1024, 0, s>>>(n, 4096, cnt, out, offs, nullptr);
+}
 } // namespace
 
 } // namespace oscb
@@ -306,6 +362,9 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
         Scratch<double> d_x(m), d_tvals(E), d_ovals(E);
         Scratch<int32_t> d_tcols(E), d_long(n);
         Scratch<uint32_t> d_deg(n), d_misc(2);         // [0] flags, [1] number of long rows
+        const size_t scan_blocks = ((size_t)n + 4095) / 4096;
+        Scratch<unsigned long long> d_sums(scan_blocks);
+        Scratch<int64_t> d_offs(scan_blocks + 1);
         if (m) {
             OSCB_CUDA(cudaMemcpyAsync(d_i.p, i, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
             OSCB_CUDA(cudaMemcpyAsync(d_j.p, j, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -319,7 +378,12 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
         const int grid_e = (int)std::min<int64_t>((m + 255) / 256 + 1, (int64_t)sms * 16);
         const int grid_r = (int)std::min<int64_t>((n * 32 + 255) / 256 + 1, (int64_t)sms * 16);
         OSCB_CUDA(cudaEventRecord(ev.a, s));
-        k_csr_count<<<grid_e, 256, 0, s>>>(m, n, d_i.p, d_j.p, d_x.p, d_deg.p, d_misc.p);
+        if (n <= CSR_SMEM_COUNTERS && m >= 16 * n) {
+            OSCB_CUDA(cudaFuncSetAttribute(k_csr_count_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, CSR_SMEM_COUNTERS * (int)sizeof(uint32_t)));
+            k_csr_count_smem<<<(int)std::min<int64_t>((m + 511) / 512, (int64_t)sms * 4), 512, (size_t)n * sizeof(uint32_t), s>>>(
+                m, n, d_i.p, d_j.p, d_x.p, d_deg.p, d_misc.p);
+        } else
+            k_csr_count<<<grid_e, 256, 0, s>>>(m, n, d_i.p, d_j.p, d_x.p, d_deg.p, d_misc.p);
         OSCB_CUDA(cudaGetLastError());
         OSCB_CUDA(cudaEventRecord(ev.b, s));
         uint32_t misc[2] = {0, 0};
@@ -336,7 +400,7 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
         if (bitmap_fits)
             OSCB_CUDA(cudaFuncSetAttribute(k_csr_sort_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bitmap_bytes));
         OSCB_CUDA(cudaEventRecord(ev.a, s));
-        k_csr_scan<<<1, 1024, 0, s>>>(n, d_deg.p, d_indptr.p);
+        launch_scan(n, d_deg.p, d_indptr.p, d_sums.p, d_offs.p, s);
         if (m) {
             k_csr_fill<<<grid_e, 256, 0, s>>>(m, d_i.p, d_j.p, d_x.p, d_indptr.p, d_deg.p, d_tcols.p, d_tvals.p);
             k_csr_sort_short<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_tcols.p, d_tvals.p, d_ocols.p, d_ovals.p, d_long.p, d_misc.p + 1,
@@ -367,7 +431,7 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
             Scratch<double> d_cvals(E);
             OSCB_CUDA(cudaEventRecord(ev.a, s));
             k_csr_nzcount<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_ovals.p, d_deg.p);
-            k_csr_scan<<<1, 1024, 0, s>>>(n, d_deg.p, d_indptr2.p);
+            launch_scan(n, d_deg.p, d_indptr2.p, d_sums.p, d_offs.p, s);
             k_csr_compact<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_indptr2.p, d_ocols.p, d_ovals.p, d_ccols.p, d_cvals.p);
             OSCB_CUDA(cudaGetLastError());
             OSCB_CUDA(cudaEventRecord(ev.b, s));
