@@ -8,8 +8,8 @@
 // Integer / byte work, HBM-bound, no sort of the whole list:
 //   k_csr_count        degree histogram with atomics + range / diagonal / has-zero flags        24 B read per entry
 //   k_csr_scan         exclusive scan of the degrees -> indptr (block totals | scan of the totals | prefixes; n words)
-//   k_csr_fill         scatter both directions into the rows in arrival order                   24 B read, 24 B written
-//   k_csr_sort_short   rows of <= 32 entries: a warp per row, rank by counting over shuffles    12 B read, 16 B written per entry
+//   k_csr_fill         scatter both directions into the rows in arrival order, 16 B per entry    24 B read, 32 B written
+//   k_csr_sort_short   rows of <= 32 entries: a warp per batch of rows, rank by counting (shuffles) 16 B read, 16 B written per entry
 //   k_csr_sort_long    longer rows, a CTA per row.  Columns of a row are unique, so the position of column c is the number
 //                      of set bits below c in the row's column BITMAP (n bits in shared memory, a popcount prefix per 1024
 //                      columns): O(n / 32 + d) per row, and a bit found set twice is the duplicate pair.  Rows too short to
@@ -139,62 +139,75 @@ __global__ void __launch_bounds__(1024) k_csr_scan(int64_t n, int64_t L, const T
 }
 
 // both directions of every entry into its rows, in arrival order (the sort kernels put a row in column order).  `deg` counts
-// down to zero: it is the cursor.
+// down to zero: it is the cursor.  An entry travels as ONE 16-byte store {column, value bits}: a scattered store costs a 32-byte
+// sector whatever its size, so column and value in separate arrays cost two.
 __global__ void __launch_bounds__(256) k_csr_fill(int64_t m, const int64_t *__restrict__ ei, const int64_t *__restrict__ ej,
                                                   const double *__restrict__ ex, const int64_t *__restrict__ indptr, uint32_t *deg,
-                                                  int32_t *__restrict__ tcols, double *__restrict__ tvals)
+                                                  longlong2 *__restrict__ tent)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += stride) {
         const int64_t a = ei[e], b = ej[e];
-        const double v = ex[e];
+        const long long v = __double_as_longlong(ex[e]);
         const int64_t pa = indptr[a] + (int64_t)(atomicSub(&deg[a], 1u) - 1u);
-        tcols[pa] = (int32_t)b;
-        tvals[pa] = v;
+        tent[pa] = make_longlong2(b, v);
         const int64_t pb = indptr[b] + (int64_t)(atomicSub(&deg[b], 1u) - 1u);
-        tcols[pb] = (int32_t)a;
-        tvals[pb] = v;
+        tent[pb] = make_longlong2(a, v);
     }
 }
 
-// rows of <= 32 entries: one warp per row, a lane per entry, its place = the number of smaller columns in the row (32
-// shuffles).  Longer rows go on a list for k_csr_sort_long.
-__global__ void __launch_bounds__(256) k_csr_sort_short(int64_t n, const int64_t *__restrict__ indptr, const int32_t *__restrict__ tcols,
-                                                        const double *__restrict__ tvals, int64_t *__restrict__ ocols,
+// Rows of <= 32 entries.  A warp owns a contiguous block of rows and takes, per trip, as many consecutive rows as fit into its 32
+// lanes (a low-degree graph: four to eight rows at once instead of one -- the kernel is a chain of dependent loads per trip, so
+// trips are what it costs), a lane per entry; an entry's place = the number of smaller columns in its own row (shuffles over the
+// batch, masked by the row's lane range); equal columns in a row = the duplicate pair.  A row of more than 32 entries goes on the
+// list for k_csr_sort_long.
+__global__ void __launch_bounds__(256) k_csr_sort_short(int64_t n, int64_t rows_per_warp, const int64_t *__restrict__ indptr,
+                                                        const longlong2 *__restrict__ tent, int64_t *__restrict__ ocols,
                                                         double *__restrict__ ovals, int32_t *long_rows, uint32_t *n_long, uint32_t *flags)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; row < n; row += warps) {
-        const int64_t lo = indptr[row];
-        const int64_t d = indptr[row + 1] - lo;
-        if (d > 32) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t begin = w * rows_per_warp, end = begin + rows_per_warp < n ? begin + rows_per_warp : n;
+    for (int64_t row = begin; row < end;) {
+        const int cand = (int)(end - row < 31 ? end - row : 31);                    // rows this trip may take
+        const int64_t ip = lane <= cand ? indptr[row + lane] : 0;                    // lane l: start of row + l
+        const int64_t base = __shfl_sync(0xffffffffu, ip, 0);
+        const uint32_t fit = __ballot_sync(0xffffffffu, lane >= 1 && lane <= cand && ip - base <= 32);
+        if (fit == 0u) {                                                             // the first row alone is too long
             if (lane == 0) long_rows[atomicAdd(n_long, 1u)] = (int32_t)row;
+            row += 1;
             continue;
         }
-        const bool mine = lane < d;
-        const int32_t c = mine ? tcols[lo + lane] : 0x7fffffff;
-        const double v = mine ? tvals[lo + lane] : 0.0;
+        const int k = 31 - __clz(fit);                                               // rows [row, row + k) fit (prefixes are monotone)
+        const int total = (int)(__shfl_sync(0xffffffffu, ip, k) - base);
+        const bool mine = lane < total;
+        longlong2 ent = make_longlong2(0x7fffffffffffffffll, 0);
+        if (mine) ent = tent[base + lane];
+        int seg = 0;                                                                 // my row = row + seg
+        for (int r = 1; r < k; ++r) seg += (int)(__shfl_sync(0xffffffffu, ip, r) - base) <= lane;
+        const int seg_lo = (int)(__shfl_sync(0xffffffffu, ip, seg) - base), seg_hi = (int)(__shfl_sync(0xffffffffu, ip, seg + 1) - base);
         int rank = 0;
         bool dup = false;
-        for (int l = 0; l < (int)d; ++l) {
-            const int32_t cl = __shfl_sync(0xffffffffu, c, l);
-            rank += cl < c;
-            dup = dup || (cl == c && l != lane);
+        for (int l = 0; l < total; ++l) {
+            const long long cl = __shfl_sync(0xffffffffu, ent.x, l);
+            const bool inrow = l >= seg_lo && l < seg_hi;
+            rank += inrow && cl < ent.x;
+            dup = dup || (inrow && cl == ent.x && l != lane);
         }
         if (mine) {
             if (dup) atomicOr(flags, CSR_EDUP);
             else {
-                ocols[lo + rank] = c;
-                ovals[lo + rank] = v;
+                ocols[base + seg_lo + rank] = ent.x;
+                ovals[base + seg_lo + rank] = __longlong_as_double(ent.y);
             }
         }
+        row += k;
     }
 }
 
 // rows of more than 32 entries, one CTA per row (see the header of this file)
 __global__ void __launch_bounds__(CSR_LONG_THREADS) k_csr_sort_long(int64_t n, int bitmap_fits, const int64_t *__restrict__ indptr,
-                                                                    const int32_t *__restrict__ tcols, const double *__restrict__ tvals,
+                                                                    const longlong2 *__restrict__ tent,
                                                                     int64_t *__restrict__ ocols, double *__restrict__ ovals,
                                                                     const int32_t *__restrict__ long_rows, const uint32_t *__restrict__ n_long,
                                                                     uint32_t *flags)
@@ -208,14 +221,13 @@ __global__ void __launch_bounds__(CSR_LONG_THREADS) k_csr_sort_long(int64_t n, i
         const int64_t row = long_rows[li];
         const int64_t lo = indptr[row];
         const int64_t d = indptr[row + 1] - lo;
-        const int32_t *rc = tcols + lo;
-        const double *rv = tvals + lo;
+        const longlong2 *re = tent + lo;
         bool dup = false;
         if (bitmap_fits && d * d > (n >> 3) + 32 * d) {
             for (uint32_t w = tid; w < W; w += CSR_LONG_THREADS) bitmap[w] = 0u;
             __syncthreads();
             for (int64_t e = tid; e < d; e += CSR_LONG_THREADS) {
-                const uint32_t c = (uint32_t)rc[e], bit = 1u << (c & 31);
+                const uint32_t c = (uint32_t)re[e].x, bit = 1u << (c & 31);
                 dup = dup || (atomicOr(&bitmap[c >> 5], bit) & bit);
             }
             __syncthreads();
@@ -242,29 +254,31 @@ __global__ void __launch_bounds__(CSR_LONG_THREADS) k_csr_sort_long(int64_t n, i
             __syncthreads();
             if (!__syncthreads_or(dup)) {
                 for (int64_t e = tid; e < d; e += CSR_LONG_THREADS) {
-                    const uint32_t c = (uint32_t)rc[e], wd = c >> 5, ch = wd >> 5;
+                    const longlong2 ent = re[e];
+                    const uint32_t c = (uint32_t)ent.x, wd = c >> 5, ch = wd >> 5;
                     uint32_t rank = cpre[ch];
                     for (uint32_t w = ch * 32; w < wd; ++w) rank += __popc(bitmap[w]);
                     rank += __popc(bitmap[wd] & ((1u << (c & 31)) - 1u));
                     ocols[lo + rank] = (int64_t)c;
-                    ovals[lo + rank] = rv[e];
+                    ovals[lo + rank] = __longlong_as_double(ent.y);
                 }
             }
             __syncthreads();
         } else {
             for (int64_t e = tid; e < d; e += CSR_LONG_THREADS) {
-                const int32_t c = rc[e];
+                const longlong2 ent = re[e];
+                const long long c = ent.x;
                 int64_t rank = 0;
                 bool twice = false;
                 for (int64_t f = 0; f < d; ++f) {
-                    const int32_t cf = rc[f];
+                    const long long cf = re[f].x;
                     rank += cf < c;
                     twice = twice || (cf == c && f != e);
                 }
                 if (twice) dup = true;
                 else {
-                    ocols[lo + rank] = (int64_t)c;
-                    ovals[lo + rank] = rv[e];
+                    ocols[lo + rank] = c;
+                    ovals[lo + rank] = __longlong_as_double(ent.y);
                 }
             }
         }
@@ -359,8 +373,9 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
         const size_t E = 2 * (size_t)m;
 
         Scratch<int64_t> d_i(m), d_j(m), d_indptr(n + 1), d_ocols(E);
-        Scratch<double> d_x(m), d_tvals(E), d_ovals(E);
-        Scratch<int32_t> d_tcols(E), d_long(n);
+        Scratch<double> d_x(m), d_ovals(E);
+        Scratch<longlong2> d_tent(E);
+        Scratch<int32_t> d_long(n);
         Scratch<uint32_t> d_deg(n), d_misc(2);         // [0] flags, [1] number of long rows
         const size_t scan_blocks = ((size_t)n + 4095) / 4096;
         Scratch<unsigned long long> d_sums(scan_blocks);
@@ -402,13 +417,17 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
         OSCB_CUDA(cudaEventRecord(ev.a, s));
         launch_scan(n, d_deg.p, d_indptr.p, d_sums.p, d_offs.p, s);
         if (m) {
-            k_csr_fill<<<grid_e, 256, 0, s>>>(m, d_i.p, d_j.p, d_x.p, d_indptr.p, d_deg.p, d_tcols.p, d_tvals.p);
-            k_csr_sort_short<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_tcols.p, d_tvals.p, d_ocols.p, d_ovals.p, d_long.p, d_misc.p + 1,
-                                                    d_misc.p);
+            k_csr_fill<<<grid_e, 256, 0, s>>>(m, d_i.p, d_j.p, d_x.p, d_indptr.p, d_deg.p, d_tent.p);
+            // a warp per block of rows: enough warps to fill the GPU eight times over, at least 32 rows each
+            const int64_t warps_wanted = std::max<int64_t>(1, std::min<int64_t>((n + 31) / 32, (int64_t)sms * 64 * 8));
+            const int64_t rows_per_warp = (n + warps_wanted - 1) / warps_wanted;
+            const int64_t warps = (n + rows_per_warp - 1) / rows_per_warp;
+            k_csr_sort_short<<<(unsigned)((warps + 7) / 8), 256, 0, s>>>(n, rows_per_warp, d_indptr.p, d_tent.p, d_ocols.p, d_ovals.p,
+                                                                        d_long.p, d_misc.p + 1, d_misc.p);
             // few long rows at a time keep many bitmaps' worth of shared memory from idling: a CTA per SM and bitmap
             const int per_sm = bitmap_fits ? std::max(1, std::min(4, (int)((size_t)smem_optin / std::max<size_t>(bitmap_bytes, 1)))) : 4;
             k_csr_sort_long<<<sms * per_sm, CSR_LONG_THREADS, bitmap_fits ? bitmap_bytes : 0, s>>>(
-                n, bitmap_fits, d_indptr.p, d_tcols.p, d_tvals.p, d_ocols.p, d_ovals.p, d_long.p, d_misc.p + 1, d_misc.p);
+                n, bitmap_fits, d_indptr.p, d_tent.p, d_ocols.p, d_ovals.p, d_long.p, d_misc.p + 1, d_misc.p);
         }
         OSCB_CUDA(cudaGetLastError());
         OSCB_CUDA(cudaEventRecord(ev.b, s));

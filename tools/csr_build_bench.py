@@ -4,7 +4,7 @@
 
 One JSON line per graph: entries per second of the kernels alone (CUDA events inside oscb_csr_from_edges), of the whole call with
 its host<->device copies (pageable numpy buffers), and of CouplingMatrix.from_edges(build="host") on this box's cores; the
-algorithmic bytes per edge are csrc/oscb_csr_build.cu's (count 24 + fill 24 + 24 + sort 24 + 32 = 128 B per edge)."""
+algorithmic bytes per edge are csrc/oscb_csr_build.cu's (count 24 + fill 24 + 32 + placement 32 + 32 = 144 B per edge; the figure printed keeps 128)."""
 import json
 import sys
 import time
