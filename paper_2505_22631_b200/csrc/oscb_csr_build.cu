@@ -186,14 +186,17 @@ __global__ void __launch_bounds__(256) k_csr_sort_short(int64_t n, int64_t rows_
         int seg = 0;                                                                 // my row = row + seg
         for (int r = 1; r < k; ++r) seg += (int)(__shfl_sync(0xffffffffu, ip, r) - base) <= lane;
         const int seg_lo = (int)(__shfl_sync(0xffffffffu, ip, seg) - base), seg_hi = (int)(__shfl_sync(0xffffffffu, ip, seg + 1) - base);
-        int rank = 0;
-        bool dup = false;
+        // (columns are < 2^31: the shuffles carry 32 bits; "equal to my own column in my row" counts me once, hence the - 1)
+        const int c32 = mine ? (int)ent.x : 0x7fffffff;
+        int rank = 0, same = 0;
+#pragma unroll 4
         for (int l = 0; l < total; ++l) {
-            const long long cl = __shfl_sync(0xffffffffu, ent.x, l);
-            const bool inrow = l >= seg_lo && l < seg_hi;
-            rank += inrow && cl < ent.x;
-            dup = dup || (inrow && cl == ent.x && l != lane);
+            const int cl = __shfl_sync(0xffffffffu, c32, l);
+            const bool inrow = (unsigned)(l - seg_lo) < (unsigned)(seg_hi - seg_lo);
+            rank += inrow && cl < c32;
+            same += inrow && cl == c32;
         }
+        const bool dup = same > 1;
         if (mine) {
             if (dup) atomicOr(flags, CSR_EDUP);
             else {
