@@ -175,3 +175,12 @@ def test_build_argument_is_validated():
     assert not model._csr_build_on_device(None, 10)
     J = pkg.CouplingMatrix.from_edges(3, [(0, 1, 1.0), (1, 2, -1.0)])
     assert J.nnz == 4
+
+
+def test_device_build_fails_loudly_without_a_gpu():
+    # explicit build="device" never falls back to the host build (no CPU path behind the C ABI)
+    from paper_2505_22631_b200 import _native
+    if _native.device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(RuntimeError, match="oscb_csr_from_edges"):
+        pkg.CouplingMatrix.from_edges(3, [(0, 1, 1.0), (1, 2, -1.0)], build="device")
