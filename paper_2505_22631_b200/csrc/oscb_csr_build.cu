@@ -328,13 +328,26 @@ __global__ void __launch_bounds__(256) k_csr_compact(int64_t n, const int64_t *_
 }
 
 namespace {
-// plain cudaMalloc blocks: a one-off build of a large graph should not park gigabytes in the run-time pool
+// Scratch of a build.  Small builds (<= 512 MB in total) take their blocks from the run-time pool (cudaMalloc + cudaFree of a
+// dozen blocks is 5-8 ms, as much as the rest of a 2 x 10^6-edge call); a large one uses plain cudaMalloc blocks and gives them
+// back, so that a one-off build of a large graph does not park gigabytes in the pool.
 template <typename T> struct Scratch {
     T *p = nullptr;
-    explicit Scratch(size_t count) { OSCB_CUDA(cudaMalloc(&p, (count ? count : 1) * sizeof(T))); }
+    size_t bytes = 0;
+    bool pooled = false;
+    Scratch(size_t count, bool use_pool) : bytes((count ? count : 1) * sizeof(T)), pooled(use_pool)
+    {
+        if (pooled) p = static_cast<T *>(pool_alloc(bytes));
+        else OSCB_CUDA(cudaMalloc(&p, bytes));
+    }
     Scratch(const Scratch &) = delete;
     Scratch &operator=(const Scratch &) = delete;
-    ~Scratch() { if (p) cudaFree(p); }
+    ~Scratch()
+    {
+        if (!p) return;
+        if (pooled) pool_free(p, bytes);
+        else cudaFree(p);
+    }
 };
 struct Events {
     cudaEvent_t a = nullptr, b = nullptr;
@@ -375,14 +388,15 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
         cudaStream_t s = nullptr;                      // the legacy default stream: this call is synchronous anyway
         const size_t E = 2 * (size_t)m;
 
-        Scratch<int64_t> d_i(m), d_j(m), d_indptr(n + 1), d_ocols(E);
-        Scratch<double> d_x(m), d_ovals(E);
-        Scratch<longlong2> d_tent(E);
-        Scratch<int32_t> d_long(n);
-        Scratch<uint32_t> d_deg(n), d_misc(2);         // [0] flags, [1] number of long rows
+        const bool pooled = 24 * (size_t)m + 40 * E + 24 * (size_t)n <= ((size_t)512 << 20);
+        Scratch<int64_t> d_i(m, pooled), d_j(m, pooled), d_indptr(n + 1, pooled), d_ocols(E, pooled);
+        Scratch<double> d_x(m, pooled), d_ovals(E, pooled);
+        Scratch<longlong2> d_tent(E, pooled);
+        Scratch<int32_t> d_long(n, pooled);
+        Scratch<uint32_t> d_deg(n, pooled), d_misc(2, pooled);         // [0] flags, [1] number of long rows
         const size_t scan_blocks = ((size_t)n + 4095) / 4096;
-        Scratch<unsigned long long> d_sums(scan_blocks);
-        Scratch<int64_t> d_offs(scan_blocks + 1);
+        Scratch<unsigned long long> d_sums(scan_blocks, pooled);
+        Scratch<int64_t> d_offs(scan_blocks + 1, pooled);
         if (m) {
             OSCB_CUDA(cudaMemcpyAsync(d_i.p, i, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
             OSCB_CUDA(cudaMemcpyAsync(d_j.p, j, m * sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -449,8 +463,8 @@ extern "C" int oscb_csr_from_edges(int device, int64_t n, int64_t m, const int64
             }
             OSCB_CUDA(cudaStreamSynchronize(s));
         } else {
-            Scratch<int64_t> d_indptr2(n + 1), d_ccols(E);
-            Scratch<double> d_cvals(E);
+            Scratch<int64_t> d_indptr2(n + 1, pooled), d_ccols(E, pooled);
+            Scratch<double> d_cvals(E, pooled);
             OSCB_CUDA(cudaEventRecord(ev.a, s));
             k_csr_nzcount<<<grid_r, 256, 0, s>>>(n, d_indptr.p, d_ovals.p, d_deg.p);
             launch_scan(n, d_deg.p, d_indptr2.p, d_sums.p, d_offs.p, s);
